@@ -1,0 +1,280 @@
+/*
+ * spx.h -- C ABI of the B200-native Causal-RoPE sequence-parallel self-attention path.
+ *
+ * This is the drop-in boundary for the hot path of the reference "spattn" engine
+ * (/root/reference/proj, namespace spattn). Every entry point cites the reference
+ * interface it replaces (file:line under proj/). Conventions:
+ *
+ *   - plain C types only; tensors are caller-owned DEVICE pointers (bf16 unless stated)
+ *     in the reference's row-major (B, S, H, D) layout (proj/include/spattn/tensor.hpp:12-14);
+ *   - every call returns spx_status; on failure spx_last_error() holds a message
+ *     (thread-local). No C++ exception crosses the ABI;
+ *   - "stream" arguments are cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - allocation happens only in *_create calls, never in the per-layer hot path.
+ */
+#ifndef SPX_H_
+#define SPX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPX_ABI_VERSION 1
+
+/* 1:1 with the reference exception taxonomy (proj/include/spattn/errors.hpp:8-36),
+ * plus device/transport failures the CPU reference cannot have. */
+typedef enum spx_status {
+    SPX_OK = 0,
+    SPX_ERR_SHAPE = 1,       /* ShapeError       */
+    SPX_ERR_PARTITION = 2,   /* PartitionError   */
+    SPX_ERR_CONFIG = 3,      /* ConfigError      */
+    SPX_ERR_RANGE = 4,       /* RangeError       */
+    SPX_ERR_ALIGNMENT = 5,   /* AlignmentError   */
+    SPX_ERR_EMPTY_CACHE = 6, /* EmptyCacheError  */
+    SPX_ERR_COLLECTIVE = 7,  /* CollectiveError  */
+    SPX_ERR_CUDA = 8,
+    SPX_ERR_NCCL = 9,
+    SPX_ERR_UNSUPPORTED = 10
+} spx_status;
+
+int spx_abi_version(void);
+const char* spx_last_error(void);
+const char* spx_status_name(int status);
+/* number of spx kernels launched by this process so far (bench "gpu_launches" claim) */
+int64_t spx_launch_count(void);
+/* SM count of a device (host query; used to size persistent grids) */
+spx_status spx_device_info(int device, int32_t out[4]); /* sm_count, cc_major, cc_minor, n_devices */
+
+/* ---------------------------------------------------------------------------------------
+ * Host RNG exactly as the reference draws its synthetic inputs
+ * (Rng / derive_seed / random_tensor: proj/src/tensor.cpp:108-159).
+ * ------------------------------------------------------------------------------------- */
+uint64_t spx_derive_seed(uint64_t base, uint64_t a, uint64_t b, uint64_t c);
+/* N(0,1)/sqrt(head_dim) noise of one block at one denoise step
+ * (block_noise, proj/src/generator.cpp:42-46): n = B*L*H*D doubles */
+spx_status spx_block_noise(uint64_t seed, int64_t block, int64_t step, int64_t n,
+                           int64_t head_dim, double* out);
+/* AttentionLayerParams::seeded(model_dim, derive_seed(seed, 0x20, layer))
+ * (proj/src/sp_attention.cpp:29-40, generator.cpp:62-67): four [dim][dim] matrices */
+spx_status spx_layer_weights(uint64_t seed, int64_t layer, int64_t model_dim, double* wq,
+                             double* wk, double* wv, double* wo);
+/* host fp64 -> bf16 (round to nearest even), n elements */
+spx_status spx_f64_to_bf16(const double* in, uint16_t* out, int64_t n);
+
+/* ---------------------------------------------------------------------------------------
+ * 3-D RoPE table (BandSplit / precompute_frequencies: proj/src/rope.cpp:15-64,
+ * proj/include/spattn/rope.hpp:35-99). Built on the host in fp64 (the reference's exact
+ * values), uploaded once per device as fp32 (cos, sin) pairs.
+ * ------------------------------------------------------------------------------------- */
+typedef struct spx_rope_table spx_rope_table;
+
+spx_status spx_band_split_defaults(int64_t head_dim, int64_t out_split[3]);
+/* split == NULL -> BandSplit::defaults_for(head_dim) */
+spx_status spx_rope_table_create(int64_t max_frames, int64_t max_h, int64_t max_w,
+                                 int64_t head_dim, double base, const int64_t* split,
+                                 spx_rope_table** out);
+void spx_rope_table_destroy(spx_rope_table* table);
+/* out: max_frames, max_h, max_w, p_T, p_H, p_W, head_dim */
+spx_status spx_rope_table_info(const spx_rope_table* table, int64_t out[7]);
+/* band 0 = temporal, 1 = height, 2 = width (RopeFrequencyTable::cos_at/sin_at) */
+spx_status spx_rope_table_at(const spx_rope_table* table, int32_t band, int64_t pos,
+                             int64_t pair, double* cos_out, double* sin_out);
+
+/* global_time_index (proj/src/rope.cpp:66-70) */
+int64_t spx_global_time_index(int64_t i_local, int64_t rank, int64_t local_len, int64_t grid_hw,
+                              int64_t start_frame);
+/* (t, h, w) of every local row of rank `rank` (rotate_rows index math, rope.cpp:97-101),
+ * computed by the SAME device function the fused kernel uses; t/h/w are device int32[L/P] */
+spx_status spx_rope_positions(const int64_t grid[3], int64_t start_frame, int64_t rank,
+                              int64_t world_size, int32_t* t, int32_t* h, int32_t* w,
+                              void* stream);
+
+/* K3: [QK-RMSNorm] + Causal-RoPE + bf16 cast (apply_rope_causal_local, rope.cpp:145-164).
+ * x, y: device bf16 (B, L/P, H, D); y may alias x. norm_weight: NULL (reference semantics)
+ * or device bf16 [H*D] for the Wan-mode RMSNorm over the model dimension. */
+spx_status spx_rope_apply_causal_local(const spx_rope_table* table, const void* x, void* y,
+                                       int64_t batch, int64_t local_len, int64_t heads,
+                                       int64_t head_dim, const int64_t grid[3],
+                                       int64_t start_frame, int64_t rank, int64_t world_size,
+                                       const void* norm_weight, float norm_eps, void* stream);
+/* apply_rope_global (rope.cpp:135-143): the P = 1 instance over a full block */
+spx_status spx_rope_apply_global(const spx_rope_table* table, const void* x, void* y,
+                                 int64_t batch, int64_t seq_len, int64_t heads, int64_t head_dim,
+                                 const int64_t grid[3], int64_t start_frame, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Dense ops
+ * ------------------------------------------------------------------------------------- */
+/* K2/K8 project_tokens (proj/src/sp_attention.cpp:51-75): y[t,:] = W x[t,:].
+ * x (tokens, c_in) bf16, w (c_out, c_in) bf16 row-major, y (tokens, c_out) bf16. */
+spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tokens,
+                              int64_t c_in, int64_t c_out, void* stream);
+/* K6 scaled_dot_product_attention (proj/src/tensor.cpp:161-209), no mask.
+ * q (B, Sq, H, D), k/v (B, Skv, H, D), o (B, Sq, H, D); bf16, B == 1, D in {64, 128}. */
+spx_status spx_attention(const void* q, const void* k, const void* v, void* o, int64_t batch,
+                         int64_t sq, int64_t skv, int64_t heads, int64_t head_dim, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Rolling KV ring (KvCache: proj/include/spattn/kv_cache.hpp:16-50, proj/src/kv_cache.cpp).
+ * One device ring of capacity_frames frame slots; frames are appended in generation order,
+ * the same block re-denoised overwrites its own slots, a window evicts whole frames from the
+ * front. Reads never copy: attention walks the (at most two) chronological segments.
+ * ------------------------------------------------------------------------------------- */
+typedef struct spx_kv_ring spx_kv_ring;
+
+/* window_frames < 0 -> unlimited; capacity_frames <= 0 -> derived (window rounded up to a
+ * multiple of 3 frames, or 64 frames when unlimited) */
+spx_status spx_kv_ring_create(int device, int64_t tokens_per_frame, int64_t window_frames,
+                              int64_t capacity_frames, int64_t heads, int64_t head_dim,
+                              spx_kv_ring** out);
+void spx_kv_ring_destroy(spx_kv_ring* ring);
+/* KvCache::update(block_index, k_block, v_block): k/v device bf16 (1, seq_len, H, D) */
+spx_status spx_kv_ring_update(spx_kv_ring* ring, int64_t block_index, const void* k_block,
+                              const void* v_block, int64_t seq_len, void* stream);
+/* KvCache::read(): chronological copy (debug; the hot path never copies) */
+spx_status spx_kv_ring_read(const spx_kv_ring* ring, void* k_out, void* v_out, void* stream);
+/* out: cached_frames, seq_len, oldest_block_index (-1 if empty), capacity_frames */
+spx_status spx_kv_ring_info(const spx_kv_ring* ring, int64_t out[4]);
+/* attention of q (1, sq, H, D) over everything cached, o (1, sq, H, D) */
+spx_status spx_kv_ring_attention(const spx_kv_ring* ring, const void* q, void* o, int64_t sq,
+                                 void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Communicator (CommWorld: proj/include/spattn/collectives.hpp:39-113,
+ * proj/src/collectives.cpp). Two transports behind one interface:
+ *   LOCAL : all ranks live in this process (one stream each; devices may repeat, i.e.
+ *           several ranks can share one GPU); chunks move by direct (peer) stores.
+ *   NCCL  : one rank per process, grouped ncclSend/ncclRecv over NVLink.
+ * Buffers passed to the collectives are indexed by LOCAL rank (1 entry for NCCL).
+ * ------------------------------------------------------------------------------------- */
+typedef struct spx_world spx_world;
+
+typedef struct spx_comm_stats {
+    int64_t all_gather;
+    int64_t all_to_all;
+    int64_t fused_all_to_all;
+    int64_t elements_sent;
+    int64_t rounds;
+} spx_comm_stats; /* CommStats, collectives.hpp:20-33 */
+
+enum { SPX_AXIS_BATCH = 0, SPX_AXIS_SEQ = 1, SPX_AXIS_HEADS = 2, SPX_AXIS_HEAD_DIM = 3 };
+enum { SPX_TRANSPORT_LOCAL = 0, SPX_TRANSPORT_NCCL = 1 };
+
+/* devices == NULL -> every rank on the current device */
+spx_status spx_world_create_local(int world_size, const int* devices, spx_world** out);
+spx_status spx_nccl_get_unique_id(uint8_t out_id[128]);
+spx_status spx_world_create_nccl(int rank, int world_size, const uint8_t id[128], int device,
+                                 spx_world** out);
+void spx_world_destroy(spx_world* world);
+/* out: world_size, local_ranks, first_local_rank, transport */
+spx_status spx_world_info(const spx_world* world, int32_t out[4]);
+spx_status spx_world_stream(const spx_world* world, int local_rank, void** stream_out);
+spx_status spx_world_synchronize(spx_world* world);
+spx_status spx_world_stats(const spx_world* world, spx_comm_stats* out);
+spx_status spx_world_reset_stats(spx_world* world);
+
+/* all_to_all(rank, x, scatter, gather) (collectives.cpp:203-235); shape = per-rank input
+ * (B, S, H, D); elem_bytes in {1,2,4,8}; out holds the per-rank result */
+spx_status spx_all_to_all(spx_world* world, void* const* in, void* const* out,
+                          const int64_t shape[4], int32_t elem_bytes, int32_t scatter_axis,
+                          int32_t gather_axis);
+/* fused_all_to_all(rank, q, k, v) (collectives.cpp:237-276): one invocation, one round */
+spx_status spx_fused_all_to_all(spx_world* world, void* const* q_in, void* const* k_in,
+                                void* const* v_in, void* const* q_out, void* const* k_out,
+                                void* const* v_out, const int64_t shape[4], int32_t elem_bytes,
+                                int32_t scatter_axis, int32_t gather_axis);
+/* all_gather(rank, x, dim) (collectives.cpp:180-201) */
+spx_status spx_all_gather(spx_world* world, void* const* in, void* const* out,
+                          const int64_t shape[4], int32_t elem_bytes, int32_t axis);
+
+/* ---------------------------------------------------------------------------------------
+ * Engine: the optimized Causal-RoPE SP schedule (sp_self_attention_engine, all flags on:
+ * proj/src/sp_attention.cpp:197-313) and the block-wise AR driver (generate:
+ * proj/src/generator.cpp:50-147) on device.
+ *
+ *   x_local --K2 QKV GEMM--> qkv --K3 [norm]+Causal-RoPE+pack--> {q, k, v} straight into the
+ *   destination ranks' q buffers and KV-ring slots (one fused exchange round)
+ *   --K6 attention over the ring--> o straight into the sources' output slabs (one round)
+ *   --K8 O GEMM (3-D TMA un-interleaves the head-group slabs)--> y_local
+ *
+ * Ulysses needs H % P == 0; otherwise P = G * S with G head groups (G | H) and S query
+ * splits (the P = 8, H = 12 case runs 4 head groups x 2 query halves).
+ * ------------------------------------------------------------------------------------- */
+typedef struct spx_engine spx_engine;
+
+typedef struct spx_engine_config {
+    int64_t frames, grid_h, grid_w;   /* GridSpec per block (F = tau, H_g, W_g) */
+    int64_t num_blocks;
+    int64_t layers;
+    int64_t denoise_steps;
+    int64_t batch;                    /* must be 1 on device */
+    int64_t heads;
+    int64_t head_dim;
+    int64_t window_frames;            /* < 0: unlimited */
+    double rope_base;
+    int64_t band_split[3];            /* all < 0: BandSplit::defaults_for(head_dim) */
+    uint64_t seed;
+    int32_t force_start_frame_zero;   /* fault injection (generator.hpp:30-32) */
+    int32_t qk_norm;                  /* 0 = reference semantics; 1 = Wan QK-RMSNorm */
+    float norm_eps;
+    int32_t profile;                  /* 1: CUDA-event stage timing on every call */
+} spx_engine_config;
+
+/* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */
+void spx_engine_config_defaults(spx_engine_config* cfg);
+/* GenerationConfig::validate (proj/src/generator.cpp:7-38) + device constraints */
+spx_status spx_engine_config_validate(const spx_engine_config* cfg, int32_t world_size);
+spx_status spx_engine_create(spx_world* world, const spx_engine_config* cfg, spx_engine** out);
+void spx_engine_destroy(spx_engine* engine);
+/* out: G (head groups), S (query splits), L (block len), L/P, heads per group, query rows
+ * per rank, kv ring capacity frames, model dim */
+spx_status spx_engine_info(const spx_engine* engine, int64_t out[8]);
+/* weights from the reference's seeded init, rounded to bf16 (host -> every device) */
+spx_status spx_engine_seed_weights(spx_engine* engine);
+/* explicit weights: host bf16 [dim][dim] each ([out][in], y = W x) */
+spx_status spx_engine_set_layer_weights(spx_engine* engine, int64_t layer, const uint16_t* wq,
+                                        const uint16_t* wk, const uint16_t* wv,
+                                        const uint16_t* wo);
+/* QK-RMSNorm weights (host bf16 [dim] each); only used when cfg.qk_norm = 1 */
+spx_status spx_engine_set_norm_weights(spx_engine* engine, int64_t layer, const uint16_t* wq,
+                                       const uint16_t* wk);
+/* KvCache::update bookkeeping for a block (once per denoise step; every layer's ring gets
+ * the same slots) -- generate() calls this itself */
+spx_status spx_engine_begin_block(spx_engine* engine, int64_t block_index);
+/* one optimized_sp_self_attention call on every local rank: x_local / y_local are device
+ * bf16 (1, L/P, H, D), indexed by local rank; y may not alias x */
+spx_status spx_engine_layer(spx_engine* engine, int64_t layer, int64_t block_index,
+                            int64_t start_frame, void* const* x_local, void* const* y_local);
+/* the whole block (denoise_steps x layers calls). noise_host: bf16 (steps, L, H, D) of the
+ * FULL block or NULL (draw it from cfg.seed with the reference RNG); out_host: bf16
+ * (L/P, H, D) rows of every local rank in rank order (a full block on a LOCAL world).
+ * Host buffers should be pinned for async copies. */
+spx_status spx_engine_generate_block(spx_engine* engine, int64_t block, const uint16_t* noise_host,
+                                     uint16_t* out_host);
+/* generate(cfg): every block; out_host: (num_blocks, rows_local, H, D) bf16 */
+spx_status spx_engine_generate(spx_engine* engine, uint16_t* out_host);
+spx_status spx_engine_synchronize(spx_engine* engine);
+/* per-stage device time (ms, summed over calls on local rank 0) in the reference's stage
+ * order qkv, rope, gather_or_fused, cache, attention, output_exchange
+ * (sp_attention.hpp:92-97); calls = number of profiled layer calls */
+spx_status spx_engine_stage_times(spx_engine* engine, double out_ms[6], int64_t* calls);
+spx_status spx_engine_reset_stage_times(spx_engine* engine);
+spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
+
+/* ---------------------------------------------------------------------------------------
+ * Debug / GPU-oracle kernels (fp32 SIMT; tests only)
+ * ------------------------------------------------------------------------------------- */
+spx_status spx_debug_naive_gemm(const void* a, const void* b, float* out, int64_t m, int64_t n,
+                                int64_t k, void* stream);
+spx_status spx_debug_naive_attention(const void* q, const void* k, const void* v, float* out,
+                                     int64_t batch, int64_t sq, int64_t skv, int64_t heads,
+                                     int64_t head_dim, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPX_H_ */

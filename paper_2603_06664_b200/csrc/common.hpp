@@ -1,0 +1,66 @@
+// common.hpp -- host-side error taxonomy and CUDA checking for the spx library.
+//
+// The C++ side throws spx::Error carrying an spx_status; every extern "C" entry point
+// converts it into a status code plus a thread-local message (spx_last_error). The status
+// set is 1:1 with the reference's exception classes (proj/include/spattn/errors.hpp:8-36).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/spx.h"
+
+namespace spx {
+
+struct Error : std::runtime_error {
+    spx_status status;
+    Error(spx_status s, const std::string& what) : std::runtime_error(what), status(s) {}
+};
+
+[[noreturn]] inline void fail(spx_status s, const std::string& what) { throw Error(s, what); }
+
+inline void require(bool cond, spx_status s, const std::string& what) {
+    if (!cond) fail(s, what);
+}
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw Error(SPX_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " at " +
+                                      file + ":" + std::to_string(line));
+    }
+}
+
+#define SPX_CUDA(call) ::spx::cuda_check((call), #call, __FILE__, __LINE__)
+#define SPX_CUDA_LAUNCH() ::spx::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+spx_status guarded(F&& f) {
+    try {
+        f();
+        return SPX_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        set_last_error(std::string("host allocation failed: ") + e.what());
+        return SPX_ERR_CUDA;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SPX_ERR_CONFIG;
+    }
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Device-side kernel launch counter (the bench's gpu_launches claim).
+void count_launch(int n = 1);
+int64_t launch_count();
+
+int device_sm_count(int device);
+
+}  // namespace spx

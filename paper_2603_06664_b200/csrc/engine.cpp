@@ -1,0 +1,616 @@
+// engine.cpp -- see engine.hpp.
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "common.hpp"
+#include "host_rng.hpp"
+
+namespace spx {
+
+int64_t choose_head_groups(int64_t P, int64_t H) {
+    for (int64_t g = P; g >= 1; --g)
+        if (P % g == 0 && H % g == 0) return g;
+    return 1;
+}
+
+namespace {
+
+void fill_matrix_bf16(uint64_t seed, int64_t rows, int64_t cols, uint16_t* out) {
+    HostRng rng(seed);
+    const double scale = 1.0 / std::sqrt(static_cast<double>(cols));
+    const int64_t n = rows * cols;
+    for (int64_t i = 0; i < n; ++i) out[i] = f64_to_bf16(rng.next_normal() * scale);
+}
+
+template <class T>
+T* dev_alloc(RankState& rs, size_t count) {
+    void* p = nullptr;
+    SPX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    SPX_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+    rs.allocations.push_back(p);
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+// GenerationConfig::validate (proj/src/generator.cpp:7-38) plus the device constraints.
+void Engine::validate(const spx_engine_config& c, int world_size) {
+    require(c.frames >= 1 && c.grid_h >= 1 && c.grid_w >= 1, SPX_ERR_SHAPE,
+            "grid extents must be >= 1, got (" + std::to_string(c.frames) + ", " +
+                std::to_string(c.grid_h) + ", " + std::to_string(c.grid_w) + ")");
+    require(c.num_blocks >= 1 && c.layers >= 1 && c.denoise_steps >= 1, SPX_ERR_CONFIG,
+            "num_blocks, layers and denoise_steps must be >= 1");
+    require(c.batch >= 1 && c.heads >= 1 && c.head_dim >= 2 && c.head_dim % 2 == 0,
+            SPX_ERR_CONFIG, "batch/heads must be >= 1 and head_dim even");
+    require(world_size >= 1, SPX_ERR_CONFIG, "world_size must be >= 1");
+    const int64_t L = c.frames * c.grid_h * c.grid_w;
+    require(L % world_size == 0, SPX_ERR_PARTITION,
+            "block length " + std::to_string(L) + " not divisible by world size " +
+                std::to_string(world_size));
+    BandSplit split = BandSplit::defaults_for(c.head_dim);
+    if (c.band_split[0] >= 0 || c.band_split[1] >= 0 || c.band_split[2] >= 0)
+        split = BandSplit{c.band_split[0], c.band_split[1], c.band_split[2]};
+    require(split.total() == c.head_dim / 2, SPX_ERR_CONFIG, "band split must sum to head_dim/2");
+    require(c.window_frames < 0 || c.window_frames >= c.frames, SPX_ERR_CONFIG,
+            "window_frames smaller than one block is not supported");
+    // device path constraints
+    require(c.batch == 1, SPX_ERR_UNSUPPORTED, "device engine runs batch 1");
+    require(c.head_dim == 64 || c.head_dim == 128, SPX_ERR_UNSUPPORTED,
+            "device engine needs head_dim 64 or 128");
+    const int64_t C = c.heads * c.head_dim;
+    require(C % 64 == 0 && C <= 2048, SPX_ERR_UNSUPPORTED,
+            "device engine needs a model dim that is a multiple of 64 and <= 2048");
+    const int64_t G = choose_head_groups(world_size, c.heads);
+    require(G <= 8 && world_size / G <= 8, SPX_ERR_PARTITION,
+            "partition needs <= 8 head groups and <= 8 query splits");
+}
+
+Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_(cfg) {
+    validate(cfg, world->size());
+    F_ = cfg.frames;
+    Hg_ = cfg.grid_h;
+    Wg_ = cfg.grid_w;
+    HW_ = Hg_ * Wg_;
+    L_ = F_ * HW_;
+    H_ = cfg.heads;
+    D_ = cfg.head_dim;
+    C_ = H_ * D_;
+    P_ = world->size();
+    G_ = choose_head_groups(P_, H_);
+    S_ = P_ / G_;
+    Lp_ = L_ / P_;
+    Lq_ = L_ / S_;
+    Hl_ = H_ / G_;
+    cap_frames_ = cfg.window_frames < 0 ? cfg.num_blocks * F_
+                                        : ceil_div(cfg.window_frames, F_) * F_;
+    frames_ = FrameRing(cap_frames_, cfg.window_frames);
+    BandSplit split = BandSplit::defaults_for(D_);
+    if (cfg.band_split[0] >= 0 || cfg.band_split[1] >= 0 || cfg.band_split[2] >= 0)
+        split = BandSplit{cfg.band_split[0], cfg.band_split[1], cfg.band_split[2]};
+    // temporal extent: every frame the run can address (generator.cpp:57-60)
+    table_ = std::make_unique<RopeTable>(cfg.num_blocks * F_, Hg_, Wg_, D_, cfg.rope_base, split);
+    allocate();
+    build_plans();
+}
+
+Engine::~Engine() {
+    for (RankState& rs : ranks_) {
+        cudaSetDevice(rs.device);
+        cudaStreamSynchronize(rs.stream);
+        for (auto& ring : rs.rings) ring.release();
+        for (void* p : rs.allocations) cudaFree(p);
+        if (rs.ev_k3) cudaEventDestroy(rs.ev_k3);
+        if (rs.ev_attn) cudaEventDestroy(rs.ev_attn);
+    }
+    for (auto& kv : weights_) {
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second.wqkv);
+        cudaFree(kv.second.wo);
+        cudaFree(kv.second.norm_q);
+        cudaFree(kv.second.norm_k);
+    }
+    for (auto* set : {&pending_events_, &free_events_})
+        for (StageEvents& se : *set)
+            for (cudaEvent_t e : se.ev) cudaEventDestroy(e);
+    if (noise_pinned_) cudaFreeHost(noise_pinned_);
+}
+
+int Engine::local_of(int rank) const { return world_->local_index(rank); }
+
+void Engine::allocate() {
+    const bool nccl = world_->transport() == SPX_TRANSPORT_NCCL;
+    const size_t slab = static_cast<size_t>(Lp_ * Hl_ * D_);
+    for (int li = 0; li < world_->num_local(); ++li) {
+        const LocalRank& lr = world_->local(li);
+        SPX_CUDA(cudaSetDevice(lr.device));
+        if (!weights_.count(lr.device)) {
+            DeviceWeights w;
+            w.device = lr.device;
+            const size_t nqkv = static_cast<size_t>(cfg_.layers * 3 * C_ * C_);
+            const size_t no = static_cast<size_t>(cfg_.layers * C_ * C_);
+            const size_t nn = static_cast<size_t>(cfg_.layers * C_);
+            SPX_CUDA(cudaMalloc(&w.wqkv, nqkv * sizeof(bf16)));
+            SPX_CUDA(cudaMalloc(&w.wo, no * sizeof(bf16)));
+            SPX_CUDA(cudaMalloc(&w.norm_q, nn * sizeof(bf16)));
+            SPX_CUDA(cudaMalloc(&w.norm_k, nn * sizeof(bf16)));
+            SPX_CUDA(cudaMemset(w.wqkv, 0, nqkv * sizeof(bf16)));
+            SPX_CUDA(cudaMemset(w.wo, 0, no * sizeof(bf16)));
+            // norm weights default to 1.0 (bf16 0x3F80)
+            std::vector<uint16_t> ones(nn, 0x3F80u);
+            SPX_CUDA(cudaMemcpy(w.norm_q, ones.data(), nn * 2, cudaMemcpyHostToDevice));
+            SPX_CUDA(cudaMemcpy(w.norm_k, ones.data(), nn * 2, cudaMemcpyHostToDevice));
+            weights_[lr.device] = w;
+        }
+        RankState rs;
+        rs.rank = lr.rank;
+        rs.local = li;
+        rs.device = lr.device;
+        rs.stream = lr.stream;
+        rs.g = static_cast<int>(lr.rank % G_);
+        rs.p = static_cast<int>(lr.rank / G_);
+        rs.x[0] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
+        rs.x[1] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
+        rs.qkv = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * 3 * C_));
+        rs.q_recv = dev_alloc<bf16>(rs, static_cast<size_t>(Lq_ * Hl_ * D_));
+        rs.o_recv = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+        if (nccl) {
+            rs.q_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+            rs.k_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+            rs.v_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+            rs.o_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+        }
+        rs.rings.resize(static_cast<size_t>(cfg_.layers));
+        for (auto& ring : rs.rings) {
+            ring.device = lr.device;
+            ring.tokens_per_frame = HW_;
+            ring.capacity_frames = cap_frames_;
+            ring.heads = Hl_;
+            ring.head_dim = D_;
+            ring.allocate();
+        }
+        SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_k3, cudaEventDisableTiming));
+        SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_attn, cudaEventDisableTiming));
+        ranks_.push_back(std::move(rs));
+    }
+}
+
+void Engine::build_plans() {
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        const int sms = device_sm_count(rs.device);
+        const DeviceWeights& w = weights_.at(rs.device);
+        rs.qkv_plan.resize(static_cast<size_t>(cfg_.layers));
+        rs.o_plan.resize(static_cast<size_t>(cfg_.layers));
+        rs.attn_plan.resize(static_cast<size_t>(cfg_.layers));
+        for (int64_t l = 0; l < cfg_.layers; ++l) {
+            GemmOperands q{};
+            q.a = rs.x[l % 2];
+            q.a_row_stride = C_;
+            q.a_group_stride = Lp_ * C_;
+            q.groups = 1;
+            q.k_inner = static_cast<int>(C_);
+            q.b = w.wqkv + l * 3 * C_ * C_;
+            q.b_row_stride = C_;
+            q.out = rs.qkv;
+            q.out_row_stride = 3 * C_;
+            q.M = static_cast<int>(Lp_);
+            q.N = static_cast<int>(3 * C_);
+            q.K = static_cast<int>(C_);
+            gemm_plan(&rs.qkv_plan[l], q, sms);
+
+            GemmOperands o{};
+            o.a = rs.o_recv;
+            o.a_row_stride = Hl_ * D_;
+            o.a_group_stride = Lp_ * Hl_ * D_;
+            o.groups = static_cast<int>(G_);
+            o.k_inner = static_cast<int>(Hl_ * D_);
+            o.b = w.wo + l * C_ * C_;
+            o.b_row_stride = C_;
+            o.out = rs.x[(l + 1) % 2];
+            o.out_row_stride = C_;
+            o.M = static_cast<int>(Lp_);
+            o.N = static_cast<int>(C_);
+            o.K = static_cast<int>(C_);
+            gemm_plan(&rs.o_plan[l], o, sms);
+
+            AttnOperands a{};
+            a.q = rs.q_recv;
+            a.q_rows = Lq_;
+            a.k = rs.rings[l].k;
+            a.v = rs.rings[l].v;
+            a.kv_rows = rs.rings[l].rows();
+            a.batch = 1;
+            a.heads = static_cast<int>(Hl_);
+            a.head_dim = static_cast<int>(D_);
+            a.sq = static_cast<int>(Lq_);
+            a.seg_start[0] = 0;
+            a.seg_len[0] = static_cast<int>(HW_);  // placeholder until begin_block
+            a.num_segs = 1;
+            a.rows_per_chunk = static_cast<int>(Lp_);
+            a.out_row_stride = Hl_ * D_;
+            attn_plan(&rs.attn_plan[l], a);
+        }
+    }
+}
+
+void Engine::info(int64_t out[8]) const {
+    out[0] = G_;
+    out[1] = S_;
+    out[2] = L_;
+    out[3] = Lp_;
+    out[4] = Hl_;
+    out[5] = Lq_;
+    out[6] = cap_frames_;
+    out[7] = C_;
+}
+
+void Engine::seed_weights() {
+    const int64_t layers = cfg_.layers;
+    const size_t mat = static_cast<size_t>(C_ * C_);
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    for (int64_t l0 = 0; l0 < layers; l0 += hw) {
+        const int64_t l1 = std::min<int64_t>(layers, l0 + hw);
+        std::vector<std::vector<uint16_t>> bufs(static_cast<size_t>(l1 - l0));
+        std::vector<std::thread> threads;
+        for (int64_t l = l0; l < l1; ++l) {
+            threads.emplace_back([&, l] {
+                std::vector<uint16_t>& b = bufs[static_cast<size_t>(l - l0)];
+                b.resize(4 * mat);
+                // AttentionLayerParams::seeded(H*D, derive_seed(seed, 0x20, layer))
+                const uint64_t base = derive_seed(cfg_.seed, 0x20, static_cast<uint64_t>(l));
+                for (int m = 0; m < 4; ++m)
+                    fill_matrix_bf16(derive_seed(base, 11 + m), C_, C_, b.data() + m * mat);
+            });
+        }
+        for (auto& t : threads) t.join();
+        for (int64_t l = l0; l < l1; ++l) {
+            const uint16_t* b = bufs[static_cast<size_t>(l - l0)].data();
+            set_layer_weights(l, b, b + mat, b + 2 * mat, b + 3 * mat);
+        }
+    }
+}
+
+void Engine::set_layer_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk,
+                               const uint16_t* wv, const uint16_t* wo) {
+    require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    const size_t mat = static_cast<size_t>(C_ * C_);
+    for (auto& kv : weights_) {
+        SPX_CUDA(cudaSetDevice(kv.first));
+        bf16* base = kv.second.wqkv + layer * 3 * mat;
+        SPX_CUDA(cudaMemcpy(base, wq, mat * 2, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(base + mat, wk, mat * 2, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(base + 2 * mat, wv, mat * 2, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(kv.second.wo + layer * mat, wo, mat * 2, cudaMemcpyHostToDevice));
+    }
+}
+
+void Engine::set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk) {
+    require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    for (auto& kv : weights_) {
+        SPX_CUDA(cudaSetDevice(kv.first));
+        SPX_CUDA(cudaMemcpy(kv.second.norm_q + layer * C_, wq, C_ * 2, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(kv.second.norm_k + layer * C_, wk, C_ * 2, cudaMemcpyHostToDevice));
+    }
+}
+
+void Engine::begin_block(int64_t block_index) {
+    const int64_t first = frames_.update(block_index, F_);
+    require(first + F_ <= cap_frames_, SPX_ERR_ALIGNMENT,
+            "block frames straddle the ring end (capacity must be a multiple of the block)");
+    block_base_row_ = first * HW_;
+    auto segs = frames_.segments();
+    require(!segs.empty() && segs.size() <= 2, SPX_ERR_RANGE, "kv ring segments");
+    num_segs_ = static_cast<int>(segs.size());
+    for (int s = 0; s < num_segs_; ++s) {
+        seg_start_[s] = static_cast<int>(segs[static_cast<size_t>(s)].first * HW_);
+        seg_len_[s] = static_cast<int>(segs[static_cast<size_t>(s)].second * HW_);
+    }
+    have_block_ = true;
+    current_block_ = block_index;
+}
+
+RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const {
+    const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
+    RopeLaunch rl{};
+    rl.in = rs.qkv;
+    rl.in_row_stride = 3 * C_;
+    rl.rows = Lp_;
+    rl.rows_per_batch = Lp_;
+    rl.heads = static_cast<int>(H_);
+    rl.head_dim = static_cast<int>(D_);
+    rl.groups = static_cast<int>(G_);
+    rl.has_kv = 1;
+    rl.row_offset = static_cast<int64_t>(rs.rank) * Lp_;  // i_g = r * L/P + i
+    rl.hw = HW_;
+    rl.grid_w = Wg_;
+    rl.start_frame = start_frame;
+    const DeviceRopeTable& t = table_->on_device(rs.device);
+    for (int b = 0; b < 3; ++b) {
+        rl.tab[b] = t.band[b];
+        rl.pairs[b] = static_cast<int>(table_->pairs(b));
+    }
+    if (cfg_.qk_norm) {
+        const DeviceWeights& w = weights_.at(rs.device);
+        rl.norm = 1;
+        rl.norm_w_q = w.norm_q + layer * C_;
+        rl.norm_w_k = w.norm_k + layer * C_;
+        rl.norm_eps = cfg_.norm_eps;
+    }
+    const int64_t slab = Lp_ * Hl_ * D_;
+    const int64_t row_elems = Hl_ * D_;
+    for (int64_t g = 0; g < G_; ++g) {
+        const int d = static_cast<int>(rs.p * G_ + g);
+        if (local) {
+            rl.dst.q[g] = ranks_[static_cast<size_t>(local_of(d))].q_recv + (rs.rank % G_) * slab;
+        } else {
+            rl.dst.q[g] = d == rs.rank ? rs.q_recv + (rs.rank % G_) * slab : rs.q_send + g * slab;
+        }
+        for (int64_t c = 0; c < S_; ++c) {
+            const int dk = static_cast<int>(c * G_ + g);
+            const int64_t row0 = block_base_row_ + static_cast<int64_t>(rs.rank) * Lp_;
+            if (local || dk == rs.rank) {
+                const RankState& dst = local ? ranks_[static_cast<size_t>(local_of(dk))] : rs;
+                rl.dst.k[g][c] = dst.rings[static_cast<size_t>(layer)].k + row0 * row_elems;
+                rl.dst.v[g][c] = dst.rings[static_cast<size_t>(layer)].v + row0 * row_elems;
+            } else {
+                rl.dst.k[g][c] = rs.k_send + g * slab;
+                rl.dst.v[g][c] = rs.v_send + g * slab;
+            }
+        }
+    }
+    rl.dst.copies = static_cast<int>(S_);
+    rl.dst_row_stride = row_elems;
+    return rl;
+}
+
+void Engine::run_layer(int64_t layer, int64_t start_frame,
+                       const std::vector<const GemmPlan*>& qkv,
+                       const std::vector<const GemmPlan*>& oproj) {
+    require(have_block_, SPX_ERR_EMPTY_CACHE, "layer call before any block was registered");
+    const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
+    const int nl = static_cast<int>(ranks_.size());
+    const int64_t slab = Lp_ * Hl_ * D_;
+    const size_t slab_bytes = static_cast<size_t>(slab) * sizeof(bf16);
+    const int64_t row_elems = Hl_ * D_;
+
+    StageEvents* prof = nullptr;
+    if (cfg_.profile) {
+        SPX_CUDA(cudaSetDevice(ranks_[0].device));
+        if (free_events_.empty()) {
+            StageEvents se;
+            for (auto& e : se.ev) SPX_CUDA(cudaEventCreate(&e));
+            free_events_.push_back(se);
+        }
+        pending_events_.push_back(free_events_.back());
+        free_events_.pop_back();
+        prof = &pending_events_.back();
+    }
+    auto mark = [&](int li, int k) {
+        if (prof && li == 0) SPX_CUDA(cudaEventRecord(prof->ev[k], ranks_[0].stream));
+    };
+
+    // K2 + K3 (the fused exchange is carried by K3's stores on the LOCAL transport)
+    for (int li = 0; li < nl; ++li) {
+        RankState& rs = ranks_[static_cast<size_t>(li)];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        mark(li, 0);
+        gemm_run(*qkv[static_cast<size_t>(li)], rs.stream);
+        mark(li, 1);
+        rope_run(rope_launch(rs, layer, start_frame), rs.stream);
+        mark(li, 2);
+        if (local) SPX_CUDA(cudaEventRecord(rs.ev_k3, rs.stream));
+    }
+    if (local) {
+        for (int li = 0; li < nl; ++li) {
+            RankState& rs = ranks_[static_cast<size_t>(li)];
+            SPX_CUDA(cudaSetDevice(rs.device));
+            for (int lj = 0; lj < nl; ++lj)
+                if (lj != li)
+                    SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(lj)].ev_k3, 0));
+        }
+    } else if (P_ > 1) {
+        RankState& rs = ranks_[0];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        KvRingStorage& ring = rs.rings[static_cast<size_t>(layer)];
+        world_->group_start();
+        for (int64_t g = 0; g < G_; ++g) {
+            const int d = static_cast<int>(rs.p * G_ + g);
+            if (d != rs.rank) world_->send(rs.q_send + g * slab, slab_bytes, d, rs.stream);
+        }
+        for (int d = 0; d < P_; ++d) {
+            if (d == rs.rank) continue;
+            const int64_t gd = d % G_;
+            world_->send(rs.k_send + gd * slab, slab_bytes, d, rs.stream);
+            world_->send(rs.v_send + gd * slab, slab_bytes, d, rs.stream);
+        }
+        for (int64_t c = 0; c < G_; ++c) {
+            const int i = static_cast<int>(rs.p * G_ + c);
+            if (i != rs.rank) world_->recv(rs.q_recv + c * slab, slab_bytes, i, rs.stream);
+        }
+        for (int i = 0; i < P_; ++i) {
+            if (i == rs.rank) continue;
+            const int64_t row0 = block_base_row_ + static_cast<int64_t>(i) * Lp_;
+            world_->recv(ring.k + row0 * row_elems, slab_bytes, i, rs.stream);
+            world_->recv(ring.v + row0 * row_elems, slab_bytes, i, rs.stream);
+        }
+        world_->group_end();
+    }
+    // ledger: one fused exchange (q: G-1 peers, k/v: P-1 peers per source) ...
+    world_->add_stats(0, 0, 1, P_ * ((G_ - 1) + 2 * (P_ - 1)) * slab, 1);
+
+    // K6 attention, output rows stored straight into their source's o_recv slab
+    for (int li = 0; li < nl; ++li) {
+        RankState& rs = ranks_[static_cast<size_t>(li)];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        mark(li, 3);
+        mark(li, 4);  // cache: bookkeeping only, the exchange already wrote the ring slots
+        AttnPlan plan = rs.attn_plan[static_cast<size_t>(layer)];
+        attn_set_segments(&plan, seg_start_, seg_len_, num_segs_);
+        for (int64_t c = 0; c < G_; ++c) {
+            const int i = static_cast<int>(rs.p * G_ + c);
+            if (local) {
+                plan.ops.out_base[c] = ranks_[static_cast<size_t>(local_of(i))].o_recv + rs.g * slab;
+            } else {
+                plan.ops.out_base[c] = i == rs.rank ? rs.o_recv + rs.g * slab : rs.o_send + c * slab;
+            }
+        }
+        attn_run(plan, rs.stream);
+        mark(li, 5);
+        if (local) SPX_CUDA(cudaEventRecord(rs.ev_attn, rs.stream));
+    }
+    if (local) {
+        for (int li = 0; li < nl; ++li) {
+            RankState& rs = ranks_[static_cast<size_t>(li)];
+            SPX_CUDA(cudaSetDevice(rs.device));
+            for (int64_t g = 0; g < G_; ++g) {
+                const int d = static_cast<int>(rs.p * G_ + g);
+                const int ld = local_of(d);
+                if (ld != li)
+                    SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(ld)].ev_attn, 0));
+            }
+        }
+    } else if (P_ > 1) {
+        RankState& rs = ranks_[0];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        world_->group_start();
+        for (int64_t c = 0; c < G_; ++c) {
+            const int i = static_cast<int>(rs.p * G_ + c);
+            if (i != rs.rank) world_->send(rs.o_send + c * slab, slab_bytes, i, rs.stream);
+        }
+        for (int64_t c = 0; c < G_; ++c) {
+            const int j = static_cast<int>(rs.p * G_ + c);
+            if (j != rs.rank) world_->recv(rs.o_recv + (j % G_) * slab, slab_bytes, j, rs.stream);
+        }
+        world_->group_end();
+    }
+    // ... and one output all-to-all (G-1 peers per rank)
+    world_->add_stats(0, 1, 0, P_ * (G_ - 1) * slab, 1);
+
+    // K8 output projection
+    for (int li = 0; li < nl; ++li) {
+        RankState& rs = ranks_[static_cast<size_t>(li)];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        gemm_run(*oproj[static_cast<size_t>(li)], rs.stream);
+        mark(li, 6);
+    }
+}
+
+void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,
+                            void* const* y) {
+    require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    require(start_frame >= 0 && start_frame + F_ <= cfg_.num_blocks * F_, SPX_ERR_RANGE,
+            "block frames [" + std::to_string(start_frame) + ", " +
+                std::to_string(start_frame + F_) + ") exceed table max_frames " +
+                std::to_string(cfg_.num_blocks * F_));
+    begin_block(block);  // KvCache::update of this call (idempotent within a block)
+    std::vector<GemmPlan> qp(ranks_.size()), op(ranks_.size());
+    std::vector<const GemmPlan*> qv, ov;
+    for (size_t li = 0; li < ranks_.size(); ++li) {
+        RankState& rs = ranks_[li];
+        SPX_CUDA(cudaSetDevice(rs.device));
+        GemmOperands q = rs.qkv_plan[static_cast<size_t>(layer)].ops;
+        q.a = static_cast<const bf16*>(x[li]);
+        gemm_plan(&qp[li], q, device_sm_count(rs.device));
+        GemmOperands o = rs.o_plan[static_cast<size_t>(layer)].ops;
+        o.out = static_cast<bf16*>(y[li]);
+        gemm_plan(&op[li], o, device_sm_count(rs.device));
+        qv.push_back(&qp[li]);
+        ov.push_back(&op[li]);
+    }
+    run_layer(layer, start_frame, qv, ov);
+}
+
+void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host) {
+    require(block >= 0 && block < cfg_.num_blocks, SPX_ERR_RANGE, "block out of range");
+    const int64_t start = cfg_.force_start_frame_zero ? 0 : block * F_;
+    begin_block(block);
+    const size_t block_elems = static_cast<size_t>(L_ * C_);
+    for (int64_t step = 0; step < cfg_.denoise_steps; ++step) {
+        const uint16_t* src = nullptr;
+        if (noise_host) {
+            src = noise_host + static_cast<size_t>(step) * block_elems;
+        } else {
+            // block_noise (generator.cpp:42-46), drawn in full on every rank, then sliced
+            if (!noise_pinned_) {
+                SPX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&noise_pinned_),
+                                        block_elems * sizeof(uint16_t)));
+            }
+            world_->synchronize();  // the previous H2D from the staging buffer is done
+            noise_f64_.resize(block_elems);
+            fill_noise(derive_seed(cfg_.seed, 0x10, static_cast<uint64_t>(block),
+                                   static_cast<uint64_t>(step)),
+                       static_cast<int64_t>(block_elems), D_, noise_f64_.data());
+            for (size_t i = 0; i < block_elems; ++i) noise_pinned_[i] = f64_to_bf16(noise_f64_[i]);
+            src = noise_pinned_;
+        }
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            SPX_CUDA(cudaMemcpyAsync(rs.x[0], src + static_cast<size_t>(rs.rank * Lp_ * C_),
+                                     static_cast<size_t>(Lp_ * C_) * sizeof(bf16),
+                                     cudaMemcpyHostToDevice, rs.stream));
+        }
+        for (int64_t l = 0; l < cfg_.layers; ++l) {
+            std::vector<const GemmPlan*> qv, ov;
+            for (RankState& rs : ranks_) {
+                qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
+                ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
+            }
+            run_layer(l, start, qv, ov);
+        }
+    }
+    const int fin = static_cast<int>(cfg_.layers % 2);
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        SPX_CUDA(cudaMemcpyAsync(out_host + static_cast<size_t>(rs.local) * Lp_ * C_, rs.x[fin],
+                                 static_cast<size_t>(Lp_ * C_) * sizeof(bf16),
+                                 cudaMemcpyDeviceToHost, rs.stream));
+    }
+    synchronize();
+}
+
+void Engine::generate(uint16_t* out_host) {
+    const size_t per_block = static_cast<size_t>(ranks_.size()) * Lp_ * C_;
+    for (int64_t b = 0; b < cfg_.num_blocks; ++b)
+        generate_block(b, nullptr, out_host + static_cast<size_t>(b) * per_block);
+}
+
+void Engine::synchronize() {
+    world_->synchronize();
+    harvest_events();
+}
+
+void Engine::harvest_events() {
+    if (pending_events_.empty()) return;
+    SPX_CUDA(cudaSetDevice(ranks_[0].device));
+    for (StageEvents& se : pending_events_) {
+        SPX_CUDA(cudaEventSynchronize(se.ev[6]));
+        for (int k = 0; k < 6; ++k) {
+            float ms = 0.0f;
+            SPX_CUDA(cudaEventElapsedTime(&ms, se.ev[k], se.ev[k + 1]));
+            stage_ms_[k] += ms;
+        }
+        ++profiled_calls_;
+        free_events_.push_back(se);
+    }
+    pending_events_.clear();
+}
+
+void Engine::stage_times(double out_ms[6], int64_t* calls) {
+    synchronize();
+    for (int k = 0; k < 6; ++k) out_ms[k] = stage_ms_[k];
+    if (calls) *calls = profiled_calls_;
+}
+
+void Engine::reset_stage_times() {
+    synchronize();
+    for (double& v : stage_ms_) v = 0.0;
+    profiled_calls_ = 0;
+}
+
+}  // namespace spx

@@ -1,0 +1,132 @@
+// engine.hpp -- the optimized Causal-RoPE SP schedule and the block-wise AR driver on device.
+//
+// Reference: sp_self_attention_engine with every ablation flag on
+// (proj/src/sp_attention.cpp:197-313) driven by generate() (proj/src/generator.cpp:50-147).
+//
+// Partition: P = G * S ranks; rank r serves head group g = r mod G (H/G heads) and query
+// split p = r / G (rows [p L/S, (p+1) L/S) of the block). Pure Ulysses is S = 1. Token rows
+// stay sharded by rank (L/P each) for the projections.
+//
+// Per layer call and rank (one CUDA stream each):
+//   K2  qkv[L/P][3C]      = x[L/P][C] W_qkv^T                       (tcgen05 GEMM)
+//   K3  [RMSNorm] + Causal-RoPE(q, k), bf16, written straight into
+//         q_recv of rank (p_src, g)   rows (src mod G) * L/P           (fused exchange,
+//         KV ring of ranks (*, g)     rows base + src * L/P             one round)
+//   K6  o = softmax(q K^T / sqrt D) V over the ring's <= 2 segments, rows scattered into
+//         o_recv[g] of their source rank                              (output exchange)
+//   K8  y[L/P][C]         = o_recv[G][L/P][H/G*D] W_o^T (3-D TMA un-interleave)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "../../include/spx.h"
+#include "kernels.hpp"
+#include "kv_ring.hpp"
+#include "rope_table.hpp"
+#include "world.hpp"
+
+namespace spx {
+
+struct DeviceWeights {
+    int device = 0;
+    bf16* wqkv = nullptr;  // [layers][3C][C]
+    bf16* wo = nullptr;    // [layers][C][C]
+    bf16* norm_q = nullptr;  // [layers][C]
+    bf16* norm_k = nullptr;
+};
+
+struct RankState {
+    int rank = 0;
+    int local = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int g = 0, p = 0;
+    bf16* x[2] = {nullptr, nullptr};  // (L/P, C) ping-pong
+    bf16* qkv = nullptr;              // (L/P, 3C)
+    bf16* q_recv = nullptr;           // (L/S, H/G, D)
+    bf16* o_recv = nullptr;           // [G][L/P][H/G*D]
+    bf16* q_send = nullptr;           // NCCL: [G][L/P][H/G][D]
+    bf16* k_send = nullptr;
+    bf16* v_send = nullptr;
+    bf16* o_send = nullptr;           // NCCL: [G][L/P][H/G*D]
+    std::vector<KvRingStorage> rings; // per layer
+    std::vector<GemmPlan> qkv_plan;   // per layer, A = x[layer % 2]
+    std::vector<GemmPlan> o_plan;     // per layer, out = x[(layer + 1) % 2]
+    std::vector<AttnPlan> attn_plan;  // per layer
+    cudaEvent_t ev_k3 = nullptr;
+    cudaEvent_t ev_attn = nullptr;
+    std::vector<void*> allocations;
+};
+
+struct StageEvents {
+    cudaEvent_t ev[7];
+};
+
+class Engine {
+  public:
+    Engine(World* world, const spx_engine_config& cfg);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    static void validate(const spx_engine_config& cfg, int world_size);
+
+    void info(int64_t out[8]) const;
+    void seed_weights();
+    void set_layer_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk,
+                           const uint16_t* wv, const uint16_t* wo);
+    void set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk);
+    void begin_block(int64_t block_index);
+    void layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,
+                        void* const* y);
+    void generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host);
+    void generate(uint16_t* out_host);
+    void synchronize();
+    void stage_times(double out_ms[6], int64_t* calls);
+    void reset_stage_times();
+    spx_comm_stats stats() const { return world_->stats(); }
+
+  private:
+    void allocate();
+    void build_plans();
+    void run_layer(int64_t layer, int64_t start_frame, const std::vector<const GemmPlan*>& qkv,
+                   const std::vector<const GemmPlan*>& oproj);
+    void harvest_events();
+    RopeLaunch rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const;
+    int local_of(int rank) const;
+
+    World* world_;
+    spx_engine_config cfg_;
+    // geometry
+    int64_t F_, Hg_, Wg_, HW_, L_, H_, D_, C_, P_, G_, S_, Lp_, Lq_, Hl_;
+    int64_t cap_frames_ = 0;
+    std::unique_ptr<RopeTable> table_;
+    std::map<int, DeviceWeights> weights_;
+    std::vector<RankState> ranks_;  // local ranks
+    FrameRing frames_;
+    int64_t block_base_row_ = 0;
+    int seg_start_[2] = {0, 0};
+    int seg_len_[2] = {0, 0};
+    int num_segs_ = 0;
+    bool have_block_ = false;
+    int64_t current_block_ = -1;
+    // pinned staging for generated noise
+    uint16_t* noise_pinned_ = nullptr;
+    std::vector<double> noise_f64_;
+    // profiling
+    std::vector<StageEvents> pending_events_;
+    std::vector<StageEvents> free_events_;
+    double stage_ms_[6] = {0, 0, 0, 0, 0, 0};
+    int64_t profiled_calls_ = 0;
+};
+
+// G (head groups) for P ranks and H heads: the largest divisor of P that divides H
+int64_t choose_head_groups(int64_t P, int64_t H);
+
+}  // namespace spx

@@ -1,0 +1,282 @@
+// gemm.cu -- K2/K8: the QKV and output projections (reference: project_tokens,
+// proj/src/sp_attention.cpp:51-75, y[t,:] = W x[t,:] with W [out][in] row-major) as one
+// persistent, warp-specialised tcgen05 GEMM:
+//
+//   out[M][N] = A[M][K] * B[N][K]^T        A = tokens (bf16), B = W (bf16, K-major)
+//
+//   warp 0      : TMA producer (A box 64x128 from a 3-D [G][M][k_inner] map, B box 64xBN)
+//   warp 1      : single-thread tcgen05.mma issuer, M=128 x N=BN x K=16 per instruction,
+//                 fp32 accumulator double-buffered in TMEM (2 x BN columns)
+//   warp 2      : TMEM allocator
+//   warps 4..7  : epilogue, tcgen05.ld -> (gate, residual) -> bf16 -> global
+//
+// The smem ring is 4 stages of (A 16 KB + B BN*128 B), SWIZZLE_128B everywhere.
+#include "common.hpp"
+#include "kernels.hpp"
+#include "sm100.cuh"
+#include "tma.hpp"
+
+namespace spx {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+
+struct GemmParams {
+    int M, N, K, k_inner;
+    int num_m_tiles, num_n_tiles;
+    bf16* out;
+    int64_t ldo;
+    int epi_mode;
+    const bf16* residual;
+    int64_t ldr;
+    const float* gate;
+};
+
+template <int BN>
+constexpr size_t gemm_smem_bytes() {
+    return 1024 + static_cast<size_t>(kStages) * (kBM * kBK * 2 + BN * kBK * 2) + 256;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    constexpr uint32_t kABytes = kBM * kBK * 2;
+    constexpr uint32_t kBBytes = BN * kBK * 2;
+    constexpr uint32_t kTmemCols = 2 * BN;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+    const int num_kt = p.K / kBK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_a);
+        tma_prefetch_desc(&map_b);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % p.num_m_tiles) * kBM;
+                const int n0 = (tile / p.num_m_tiles) * BN;
+                for (int kt = 0; kt < num_kt; ++kt) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
+                    const int k0 = kt * kBK;
+                    tma_load_3d(sA + stage * kABytes, &map_a, &full[stage], k0 % p.k_inner, m0,
+                                k0 / p.k_inner);
+                    tma_load_2d(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, false, false);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kt = 0; kt < num_kt; ++kt) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * kABytes);
+                    const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        umma_bf16_ss(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
+                                     make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                                     (kt | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            const int m0 = (tile % p.num_m_tiles) * kBM;
+            const int n0 = (tile / p.num_m_tiles) * BN;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int row = m0 + ew * 32 + lane;
+            const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(t_row + c * 32, r);
+                tmem_ld_wait();
+                const int col0 = n0 + c * 32;
+                if (row < p.M && col0 < p.N) {
+                    float f[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+                    if (p.epi_mode == 1) {
+                        const uint4* res =
+                            reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint4 rv = res[q];
+                            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float2 rr = unpack_bf16x2(rw[e]);
+                                const int j = q * 8 + e * 2;
+                                f[j] = rr.x + p.gate[col0 + j] * f[j];
+                                f[j + 1] = rr.y + p.gate[col0 + j + 1] * f[j + 1];
+                            }
+                        }
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + row * p.ldo + col0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]),
+                                            pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                                            pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]),
+                                            pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem_base);
+    }
+}
+
+template <int BN>
+void set_smem_attr() {
+    static bool done[64] = {};  // the attribute is per function per device
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 63]) {
+        SPX_CUDA(cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(gemm_smem_bytes<BN>())));
+        done[dev & 63] = true;
+    }
+}
+
+}  // namespace
+
+void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
+    require(ops.M > 0 && ops.N > 0 && ops.K > 0, SPX_ERR_SHAPE, "gemm: empty problem");
+    require(ops.K % kBK == 0, SPX_ERR_SHAPE, "gemm: K must be a multiple of 64");
+    require(ops.k_inner % kBK == 0 && ops.groups * ops.k_inner == ops.K, SPX_ERR_SHAPE,
+            "gemm: K must split into groups of a multiple of 64");
+    require(ops.N % 32 == 0, SPX_ERR_SHAPE, "gemm: N must be a multiple of 32");
+    require((reinterpret_cast<uintptr_t>(ops.out) & 15) == 0 && ops.out_row_stride % 8 == 0,
+            SPX_ERR_ALIGNMENT, "gemm: output must be 16-byte aligned");
+    plan->ops = ops;
+    // BN: 256 unless 128 gives a better wave quantisation over the SMs
+    const int64_t mt = ceil_div(ops.M, kBM);
+    auto waste = [&](int bn) {
+        const int64_t tiles = mt * ceil_div(ops.N, bn);
+        const int64_t waves = ceil_div(tiles, sm_count);
+        return static_cast<double>(waves * sm_count * bn) / static_cast<double>(tiles * bn) *
+               (ops.N % bn == 0 ? 1.0 : 1.0 + static_cast<double>(bn - ops.N % bn) / ops.N);
+    };
+    plan->bn = (ops.N % 256 == 0 && waste(256) <= waste(128) * 1.05) ? 256 : 128;
+    char err[256];
+    {
+        const uint64_t dims[3] = {static_cast<uint64_t>(ops.k_inner), static_cast<uint64_t>(ops.M),
+                                  static_cast<uint64_t>(ops.groups)};
+        const uint64_t strides[2] = {static_cast<uint64_t>(ops.a_row_stride) * 2,
+                                     static_cast<uint64_t>(ops.a_group_stride) * 2};
+        const uint32_t box[3] = {kBK, kBM, 1};
+        require(make_tma_map_bf16(&plan->map_a, ops.a, 3, dims, strides, box, err, sizeof(err)),
+                SPX_ERR_ALIGNMENT, err);
+    }
+    {
+        const uint64_t dims[2] = {static_cast<uint64_t>(ops.K), static_cast<uint64_t>(ops.N)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(ops.b_row_stride) * 2};
+        const uint32_t box[2] = {kBK, static_cast<uint32_t>(plan->bn)};
+        require(make_tma_map_bf16(&plan->map_b, ops.b, 2, dims, strides, box, err, sizeof(err)),
+                SPX_ERR_ALIGNMENT, err);
+    }
+    const int64_t tiles = mt * ceil_div(ops.N, plan->bn);
+    plan->grid = static_cast<int>(tiles < sm_count ? tiles : sm_count);
+}
+
+void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
+    const GemmOperands& o = plan.ops;
+    GemmParams p{};
+    p.M = o.M;
+    p.N = o.N;
+    p.K = o.K;
+    p.k_inner = o.k_inner;
+    p.num_m_tiles = static_cast<int>(ceil_div(o.M, kBM));
+    p.num_n_tiles = static_cast<int>(ceil_div(o.N, plan.bn));
+    p.out = o.out;
+    p.ldo = o.out_row_stride;
+    p.epi_mode = o.epi_mode;
+    p.residual = o.residual;
+    p.ldr = o.residual_row_stride;
+    p.gate = o.gate;
+    if (plan.bn == 256) {
+        set_smem_attr<256>();
+        gemm_bf16_tn_kernel<256><<<plan.grid, kThreads, gemm_smem_bytes<256>(), stream>>>(
+            plan.map_a, plan.map_b, p);
+    } else {
+        set_smem_attr<128>();
+        gemm_bf16_tn_kernel<128><<<plan.grid, kThreads, gemm_smem_bytes<128>(), stream>>>(
+            plan.map_a, plan.map_b, p);
+    }
+    SPX_CUDA_LAUNCH();
+    count_launch();
+}
+
+}  // namespace spx

@@ -1,0 +1,145 @@
+// kernels.hpp -- host launchers for the spx sm_100a kernels (one translation unit each).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace spx {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------------------------------
+// K2 / K8: tcgen05 GEMM  out[M][N] = A[M][K] * B[N][K]^T  (bf16 in, fp32 TMEM accumulate)
+//   A is addressed as a 3-D tensor [G][M][k_inner] (K = G * k_inner): the output all-to-all
+//   lands head-group slabs side by side and the A-operand TMA un-interleaves them.
+// ---------------------------------------------------------------------------------------
+struct GemmOperands {
+    const bf16* a = nullptr;
+    int64_t a_row_stride = 0;    // elements between consecutive rows of one group slab
+    int64_t a_group_stride = 0;  // elements between group slabs
+    int groups = 1;
+    int k_inner = 0;
+    const bf16* b = nullptr;     // [N][K] row-major (K-major)
+    int64_t b_row_stride = 0;
+    bf16* out = nullptr;
+    int64_t out_row_stride = 0;
+    int M = 0, N = 0, K = 0;
+    // epilogue: 0 -> out = acc ; 1 -> out = residual + gate[col] * acc (adaLN gate + residual)
+    int epi_mode = 0;
+    const bf16* residual = nullptr;
+    int64_t residual_row_stride = 0;
+    const float* gate = nullptr;
+};
+
+struct GemmPlan {
+    CUtensorMap map_a;
+    CUtensorMap map_b;
+    GemmOperands ops;
+    int bn = 256;
+    int grid = 0;
+};
+
+void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count);
+void gemm_run(const GemmPlan& plan, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------------------
+// K6: chunk-causal flash attention, tcgen05/TMEM, TMA-fed.
+//   q  : [B][Sq][H][D]    k/v : [B][Skv_rows][H][D] addressed through up to two row
+//   segments (the rolling KV ring wraps).  Output rows are scattered to up to 8 destination
+//   slabs (the output all-to-all is fused into the epilogue).
+// ---------------------------------------------------------------------------------------
+struct AttnOperands {
+    const bf16* q = nullptr;
+    int64_t q_rows = 0;          // rows per batch in q
+    const bf16* k = nullptr;
+    const bf16* v = nullptr;
+    int64_t kv_rows = 0;         // rows per batch in the k/v buffers (ring capacity rows)
+    int batch = 1, heads = 0, head_dim = 0;
+    int sq = 0;                  // query rows to compute (<= q_rows)
+    int seg_start[2] = {0, 0};
+    int seg_len[2] = {0, 0};
+    int num_segs = 1;
+    // output element (b, i, h, d) -> out_base[i / rows_per_chunk] + b * out_batch_stride
+    //                                 + (i % rows_per_chunk) * out_row_stride + h * D + d
+    bf16* out_base[8] = {};
+    int rows_per_chunk = 0;
+    int64_t out_row_stride = 0;
+    int64_t out_batch_stride = 0;
+};
+
+struct AttnPlan {
+    CUtensorMap map_q;
+    CUtensorMap map_k;
+    CUtensorMap map_v;
+    AttnOperands ops;
+};
+
+void attn_plan(AttnPlan* plan, const AttnOperands& ops);
+void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs);
+void attn_run(const AttnPlan& plan, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------------------
+// K3: fused [QK-RMSNorm] + Causal-RoPE + bf16 cast + all-to-all pack.
+//   Input rows are the QKV GEMM output [rows][3C] (or a single tensor, see RopeTensorMode);
+//   every 16-byte vector of head h goes to destination slab group g = h / heads_per_group.
+// ---------------------------------------------------------------------------------------
+struct RopeTable;  // device copy, see rope_table.hpp
+
+struct RopeDest {
+    bf16* q[8] = {};           // per head group: base of the (rows, H/G, D) q slab
+    bf16* k[8][8] = {};        // per head group, per query split copy
+    bf16* v[8][8] = {};
+    int copies = 1;            // query-split copies of k/v to write (S)
+};
+
+struct RopeLaunch {
+    const bf16* in = nullptr;        // rows of the input
+    int64_t in_row_stride = 0;       // elements
+    int64_t rows = 0;                // tokens (local), batch folded
+    int64_t rows_per_batch = 0;      // L/P (for the time index)
+    int heads = 0, head_dim = 0;
+    int groups = 1;                  // head groups (destinations)
+    int has_kv = 0;                  // 1: input holds q|k|v, 0: a single tensor rotated into q
+    // position math (rope.cpp:97-101): i_g = row_offset + i, t = start + i_g / hw ...
+    int64_t row_offset = 0;
+    int64_t hw = 0, grid_w = 0, start_frame = 0;
+    // table (device, fp32 cos/sin interleaved per band)
+    const float2* tab[3] = {};
+    int pairs[3] = {0, 0, 0};
+    // optional QK-RMSNorm over the C = H*D channels
+    const bf16* norm_w_q = nullptr;
+    const bf16* norm_w_k = nullptr;
+    float norm_eps = 1e-6f;
+    int norm = 0;
+    RopeDest dst;
+    int64_t dst_row_stride = 0;      // elements between rows in a destination slab (H/G * D)
+};
+
+void rope_run(const RopeLaunch& l, cudaStream_t stream);
+// Debug probe: the kernel's own (t, h, w) index math for every local row.
+void rope_positions_run(int64_t rows, int64_t row_offset, int64_t hw, int64_t grid_w,
+                        int64_t start_frame, int32_t* t, int32_t* h, int32_t* w,
+                        cudaStream_t stream);
+
+// ---------------------------------------------------------------------------------------
+// Byte movers (all-to-all / all-gather on any axes, any element width) and helpers.
+// ---------------------------------------------------------------------------------------
+struct Box4 {
+    int64_t ext[4];     // extents copied
+    int64_t src_str[4]; // element strides of the source
+    int64_t dst_str[4];
+};
+void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------
+// Kd: naive fp32 SIMT reference kernels (GPU oracle at shapes the CPU oracle cannot reach).
+// ---------------------------------------------------------------------------------------
+void naive_gemm_run(const bf16* a, const bf16* b, float* out, int M, int N, int K,
+                    cudaStream_t s);
+void naive_attention_run(const bf16* q, const bf16* k, const bf16* v, float* out, int batch,
+                         int sq, int skv, int heads, int head_dim, cudaStream_t s);
+
+}  // namespace spx

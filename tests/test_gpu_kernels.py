@@ -1,0 +1,113 @@
+"""GPU numerics of the individual sm_100a kernels against fp32 references of the same op.
+
+K2/K8 GEMM vs torch fp32 matmul, K6 attention vs fp32 softmax attention (torch on the same
+bf16 inputs, and the library's own fp32 SIMT kernel at the Wan shape), K3 index math vs the
+reference formula (bit-exact). Calls go through the C ABI (libspx.so).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _t():
+    import torch
+
+    return torch
+
+
+def _stream():
+    return _t().cuda.current_stream().cuda_stream
+
+
+def _lib():
+    from paper_2603_06664_b200._lib import lib
+
+    return lib()
+
+
+def _check(status):
+    from paper_2603_06664_b200._lib import check
+
+    check(status)
+
+
+def rel_l2(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("M,K,N", [(192, 256, 768), (300, 256, 256), (4680, 1536, 4608),
+                                   (585, 1536, 1536), (1170, 1536, 4608)])
+def test_project_tokens_matches_fp32(cuda, M, K, N):
+    torch = _t()
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    y = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    _check(_lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(), M, K, N, _stream()))
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t()
+    # bf16 output rounding: |err| <= 2^-8 |y|
+    assert rel_l2(y.float(), ref) < 4e-3
+    assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
+
+
+@pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),
+                                        (4680, 4680, 12, 128), (1170, 9360, 3, 128)])
+def test_attention_matches_fp32(cuda, sq, skv, H, D):
+    torch = _t()
+    g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
+    # O(1) logits (well-conditioned softmax), as in the tolerance tier of SURVEY 8c
+    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq, skv,
+                                H, D, _stream()))
+    torch.cuda.synchronize()
+    qf, kf, vf = (t.float().transpose(1, 2) for t in (q, k, v))
+    ref = torch.softmax(qf @ kf.transpose(-1, -2) / math.sqrt(D), dim=-1) @ vf
+    ref = ref.transpose(1, 2)
+    assert rel_l2(o.float(), ref) < 1e-2
+
+
+def test_attention_matches_simt_kernel(cuda):
+    torch = _t()
+    sq, skv, H, D = 640, 1560, 2, 128
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    ref = torch.empty(1, sq, H, D, device=cuda, dtype=torch.float32)
+    _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq, skv,
+                                H, D, _stream()))
+    _check(_lib().spx_debug_naive_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), ref.data_ptr(),
+                                            1, sq, skv, H, D, _stream()))
+    torch.cuda.synchronize()
+    assert rel_l2(o.float(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("grid,P,start", [((3, 30, 52), 8, 18), ((3, 8, 8), 2, 3), ((3, 4, 4), 4, 0)])
+def test_rope_positions_bit_exact(cuda, grid, P, start):
+    torch = _t()
+    from paper_2603_06664_b200._lib import i64_array
+
+    F, Hg, Wg = grid
+    L = F * Hg * Wg
+    Lp = L // P
+    for r in range(P):
+        t = torch.empty(Lp, dtype=torch.int32, device=cuda)
+        h = torch.empty_like(t)
+        w = torch.empty_like(t)
+        _check(_lib().spx_rope_positions(i64_array(grid), start, r, P, t.data_ptr(), h.data_ptr(),
+                                         w.data_ptr(), _stream()))
+        torch.cuda.synchronize()
+        ig = r * Lp + np.arange(Lp)
+        np.testing.assert_array_equal(t.cpu().numpy(), start + ig // (Hg * Wg))
+        np.testing.assert_array_equal(h.cpu().numpy(), (ig % (Hg * Wg)) // Wg)
+        np.testing.assert_array_equal(w.cpu().numpy(), ig % Wg)
