@@ -254,6 +254,10 @@ spx_status spx_engine_layer(spx_engine* engine, int64_t layer, int64_t block_ind
  * Host buffers should be pinned for async copies. */
 spx_status spx_engine_generate_block(spx_engine* engine, int64_t block, const uint16_t* noise_host,
                                      uint16_t* out_host);
+/* device-resident variant for benchmarking: noise_dev[local rank] holds (steps, L/P, H, D),
+ * out_dev[local rank] receives (L/P, H, D); asynchronous on the world's streams */
+spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
+                                            const void* const* noise_dev, void* const* out_dev);
 /* generate(cfg): every block; out_host: (num_blocks, rows_local, H, D) bf16 */
 spx_status spx_engine_generate(spx_engine* engine, uint16_t* out_host);
 spx_status spx_engine_synchronize(spx_engine* engine);
@@ -262,6 +266,8 @@ spx_status spx_engine_synchronize(spx_engine* engine);
  * (sp_attention.hpp:92-97); calls = number of profiled layer calls */
 spx_status spx_engine_stage_times(spx_engine* engine, double out_ms[6], int64_t* calls);
 spx_status spx_engine_reset_stage_times(spx_engine* engine);
+/* switch the CUDA-event stage timing on (1) / off (0) for subsequent calls */
+spx_status spx_engine_set_profile(spx_engine* engine, int32_t on);
 spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
 
 /* ---------------------------------------------------------------------------------------

@@ -151,10 +151,12 @@ _SIGS = [
     ("spx_engine_layer", c_int, [c_void_p, c_int64, c_int64, c_int64, POINTER(c_void_p),
                                  POINTER(c_void_p)]),
     ("spx_engine_generate_block", c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    ("spx_engine_generate_block_device", c_int, [c_void_p, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
     ("spx_engine_generate", c_int, [c_void_p, c_void_p]),
     ("spx_engine_synchronize", c_int, [c_void_p]),
     ("spx_engine_stage_times", c_int, [c_void_p, POINTER(c_double), POINTER(c_int64)]),
     ("spx_engine_reset_stage_times", c_int, [c_void_p]),
+    ("spx_engine_set_profile", c_int, [c_void_p, c_int32]),
     ("spx_engine_stats", c_int, [c_void_p, POINTER(CommStats)]),
     ("spx_debug_naive_gemm", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     ("spx_debug_naive_attention", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,

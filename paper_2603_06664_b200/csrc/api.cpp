@@ -683,6 +683,14 @@ spx_status spx_engine_generate_block(spx_engine* engine, int64_t block,
     });
 }
 
+spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
+                                            const void* const* noise_dev, void* const* out_dev) {
+    return guarded([&] {
+        require(engine && noise_dev && out_dev, SPX_ERR_CONFIG, "null argument");
+        engine->e->generate_block_device(block, noise_dev, out_dev);
+    });
+}
+
 spx_status spx_engine_generate(spx_engine* engine, uint16_t* out_host) {
     return guarded([&] {
         require(engine && out_host, SPX_ERR_CONFIG, "null argument");
@@ -708,6 +716,13 @@ spx_status spx_engine_reset_stage_times(spx_engine* engine) {
     return guarded([&] {
         require_ptr(engine, "engine");
         engine->e->reset_stage_times();
+    });
+}
+
+spx_status spx_engine_set_profile(spx_engine* engine, int32_t on) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->set_profile(on != 0);
     });
 }
 

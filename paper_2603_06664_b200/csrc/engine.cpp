@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <thread>
 
 #include "common.hpp"
@@ -526,12 +527,27 @@ void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, v
     run_layer(layer, start_frame, qv, ov);
 }
 
-void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host) {
+void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_step) {
     require(block >= 0 && block < cfg_.num_blocks, SPX_ERR_RANGE, "block out of range");
     const int64_t start = cfg_.force_start_frame_zero ? 0 : block * F_;
     begin_block(block);
-    const size_t block_elems = static_cast<size_t>(L_ * C_);
     for (int64_t step = 0; step < cfg_.denoise_steps; ++step) {
+        load_step(step);  // fresh noise into x[0] of every local rank (steps do not chain)
+        for (int64_t l = 0; l < cfg_.layers; ++l) {
+            std::vector<const GemmPlan*> qv, ov;
+            for (RankState& rs : ranks_) {
+                qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
+                ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
+            }
+            run_layer(l, start, qv, ov);
+        }
+    }
+}
+
+void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host) {
+    const size_t block_elems = static_cast<size_t>(L_ * C_);
+    const size_t slice_bytes = static_cast<size_t>(Lp_ * C_) * sizeof(bf16);
+    run_block(block, [&](int64_t step) {
         const uint16_t* src = nullptr;
         if (noise_host) {
             src = noise_host + static_cast<size_t>(step) * block_elems;
@@ -552,26 +568,36 @@ void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t*
         for (RankState& rs : ranks_) {
             SPX_CUDA(cudaSetDevice(rs.device));
             SPX_CUDA(cudaMemcpyAsync(rs.x[0], src + static_cast<size_t>(rs.rank * Lp_ * C_),
-                                     static_cast<size_t>(Lp_ * C_) * sizeof(bf16),
-                                     cudaMemcpyHostToDevice, rs.stream));
+                                     slice_bytes, cudaMemcpyHostToDevice, rs.stream));
         }
-        for (int64_t l = 0; l < cfg_.layers; ++l) {
-            std::vector<const GemmPlan*> qv, ov;
-            for (RankState& rs : ranks_) {
-                qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
-                ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
-            }
-            run_layer(l, start, qv, ov);
-        }
-    }
+    });
     const int fin = static_cast<int>(cfg_.layers % 2);
     for (RankState& rs : ranks_) {
         SPX_CUDA(cudaSetDevice(rs.device));
         SPX_CUDA(cudaMemcpyAsync(out_host + static_cast<size_t>(rs.local) * Lp_ * C_, rs.x[fin],
-                                 static_cast<size_t>(Lp_ * C_) * sizeof(bf16),
-                                 cudaMemcpyDeviceToHost, rs.stream));
+                                 slice_bytes, cudaMemcpyDeviceToHost, rs.stream));
     }
     synchronize();
+}
+
+void Engine::generate_block_device(int64_t block, const void* const* noise_dev,
+                                   void* const* out_dev) {
+    const size_t slice_bytes = static_cast<size_t>(Lp_ * C_) * sizeof(bf16);
+    run_block(block, [&](int64_t step) {
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            SPX_CUDA(cudaMemcpyAsync(rs.x[0],
+                                     static_cast<const uint8_t*>(noise_dev[rs.local]) +
+                                         static_cast<size_t>(step) * slice_bytes,
+                                     slice_bytes, cudaMemcpyDeviceToDevice, rs.stream));
+        }
+    });
+    const int fin = static_cast<int>(cfg_.layers % 2);
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        SPX_CUDA(cudaMemcpyAsync(out_dev[rs.local], rs.x[fin], slice_bytes,
+                                 cudaMemcpyDeviceToDevice, rs.stream));
+    }
 }
 
 void Engine::generate(uint16_t* out_host) {

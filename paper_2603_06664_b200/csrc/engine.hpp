@@ -21,6 +21,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <vector>
@@ -86,14 +87,19 @@ class Engine {
     void layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,
                         void* const* y);
     void generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host);
+    // device-resident variant (no host copies, no synchronisation): noise_dev[local] holds
+    // (steps, L/P, C) bf16, out_dev[local] receives (L/P, C)
+    void generate_block_device(int64_t block, const void* const* noise_dev, void* const* out_dev);
     void generate(uint16_t* out_host);
     void synchronize();
     void stage_times(double out_ms[6], int64_t* calls);
     void reset_stage_times();
+    void set_profile(bool on) { cfg_.profile = on ? 1 : 0; }
     spx_comm_stats stats() const { return world_->stats(); }
 
   private:
     void allocate();
+    void run_block(int64_t block, const std::function<void(int64_t)>& load_step);
     void build_plans();
     void run_layer(int64_t layer, int64_t start_frame, const std::vector<const GemmPlan*>& qkv,
                    const std::vector<const GemmPlan*>& oproj);

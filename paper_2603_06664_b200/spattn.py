@@ -1,0 +1,539 @@
+"""Python mirror of the reference operator API (namespace spattn, proj/include/spattn/*.hpp)
+over the B200 C ABI (include/spx.h, libspx.so).
+
+Same names, argument meaning and error classes as the reference, so a caller -- and the
+parity tests -- read like proj/tests. Differences forced by the device:
+  * tensors are torch CUDA bf16 tensors in the reference's (B, S, H, D) layout;
+  * the reference calls collectives per rank inside CommWorld::run threads; here one call
+    moves the buffers of every rank of a LOCAL world (lists indexed by rank);
+  * KvCache lives on the device and attention reads it in place (KvCache.attention).
+torch is used only to own device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (AlignmentError, CollectiveError, ConfigError, EmptyCacheError, PartitionError,  # noqa: F401
+                   RangeError, ShapeError, SpxError, UnsupportedError, check, i64_array, lib, ptr_array)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def _bf16(t):
+    torch = _torch()
+    if not (t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous()):
+        raise ShapeError("expected a contiguous CUDA bf16 tensor")
+    return t
+
+
+class Axis(enum.IntEnum):
+    """Axis (proj/include/spattn/tensor.hpp:16)."""
+
+    Batch = 0
+    Seq = 1
+    Heads = 2
+    HeadDim = 3
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """GridSpec (rope.hpp:13-21): F frames of H_g x W_g tokens, row-major (t, h, w)."""
+
+    frames: int
+    height: int
+    width: int
+
+    def tokens_per_frame(self) -> int:
+        return self.height * self.width
+
+    def seq_len(self) -> int:
+        return self.frames * self.height * self.width
+
+    def as_array(self):
+        return i64_array([self.frames, self.height, self.width])
+
+
+@dataclass(frozen=True)
+class BandSplit:
+    """BandSplit (rope.hpp:35-44)."""
+
+    temporal: int
+    height: int
+    width: int
+
+    def total(self) -> int:
+        return self.temporal + self.height + self.width
+
+    @staticmethod
+    def defaults_for(head_dim: int) -> "BandSplit":
+        out = i64_array([0, 0, 0])
+        check(lib().spx_band_split_defaults(head_dim, out))
+        return BandSplit(*out)
+
+
+class RopeFrequencyTable:
+    """RopeFrequencyTable (rope.hpp:52-88): fp64 on the host, fp32 copies per device."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().spx_rope_table_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        out = i64_array([0] * 7)
+        check(lib().spx_rope_table_info(self._h, out))
+        return list(out)
+
+    def max_frames(self):
+        return self._info()[0]
+
+    def max_height(self):
+        return self._info()[1]
+
+    def max_width(self):
+        return self._info()[2]
+
+    def split(self) -> BandSplit:
+        return BandSplit(*self._info()[3:6])
+
+    def _at(self, band, pos, pair):
+        c = ctypes.c_double()
+        s = ctypes.c_double()
+        check(lib().spx_rope_table_at(self._h, int(band), pos, pair, ctypes.byref(c), ctypes.byref(s)))
+        return c.value, s.value
+
+    def cos_at(self, band, pos, pair):
+        return self._at(band, pos, pair)[0]
+
+    def sin_at(self, band, pos, pair):
+        return self._at(band, pos, pair)[1]
+
+
+def precompute_frequencies(max_frames, max_h, max_w, head_dim, base=10000.0,
+                           split: Optional[BandSplit] = None) -> RopeFrequencyTable:
+    """precompute_frequencies (rope.hpp:90-99, rope.cpp:21-64)."""
+    h = ctypes.c_void_p()
+    sp = i64_array([split.temporal, split.height, split.width]) if split else None
+    check(lib().spx_rope_table_create(max_frames, max_h, max_w, head_dim, base, sp, ctypes.byref(h)))
+    return RopeFrequencyTable(h)
+
+
+def global_time_index(i_local, rank, local_len, grid_hw, start_frame) -> int:
+    """global_time_index (rope.cpp:66-70)."""
+    return int(lib().spx_global_time_index(i_local, rank, local_len, grid_hw, start_frame))
+
+
+def rope_positions(grid: GridSpec, start_frame, rank, world_size):
+    """(t, h, w) int32 tensors of rank `rank`'s local rows, from the device index path."""
+    torch = _torch()
+    n = grid.seq_len() // world_size if world_size > 0 else 0
+    t = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    h = torch.empty_like(t)
+    w = torch.empty_like(t)
+    check(lib().spx_rope_positions(grid.as_array(), start_frame, rank, world_size, t.data_ptr(),
+                                   h.data_ptr(), w.data_ptr(), _stream()))
+    return t[:n], h[:n], w[:n]
+
+
+def apply_rope_causal_local(x_local, grid: GridSpec, table: RopeFrequencyTable, start_frame, rank,
+                            world_size, norm_weight=None, norm_eps=1e-6, out=None):
+    """apply_rope_causal_local (rope.hpp:121-123): x_local (B, L/P, H, D) bf16 -> rotated."""
+    x = _bf16(x_local)
+    B, S, H, D = x.shape
+    y = _torch().empty_like(x) if out is None else out
+    nw = _bf16(norm_weight).data_ptr() if norm_weight is not None else None
+    check(lib().spx_rope_apply_causal_local(table._h, x.data_ptr(), y.data_ptr(), B, S, H, D,
+                                            grid.as_array(), start_frame, rank, world_size, nw,
+                                            norm_eps, _stream()))
+    return y
+
+
+def apply_rope_global(x, grid: GridSpec, table: RopeFrequencyTable, start_frame, out=None):
+    """apply_rope_global (rope.hpp:113-114)."""
+    x = _bf16(x)
+    B, S, H, D = x.shape
+    y = _torch().empty_like(x) if out is None else out
+    check(lib().spx_rope_apply_global(table._h, x.data_ptr(), y.data_ptr(), B, S, H, D,
+                                      grid.as_array(), start_frame, _stream()))
+    return y
+
+
+def project_tokens(x, w):
+    """project_tokens (sp_attention.hpp:34): y[b,s] = W x[b,s]; W (H*D, H*D) bf16 [out][in]."""
+    x = _bf16(x)
+    w = _bf16(w)
+    B, S, H, D = x.shape
+    if w.shape[1] != H * D:
+        raise ShapeError(f"projection is {w.shape[0]}x{w.shape[1]}, tokens have H*D = {H * D}")
+    y = _torch().empty(B, S, w.shape[0] // D, D, dtype=x.dtype, device=x.device)
+    check(lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(), B * S, H * D, w.shape[0],
+                                   _stream()))
+    return y
+
+
+def scaled_dot_product_attention(q, k, v):
+    """scaled_dot_product_attention (tensor.hpp:99): no mask, scale 1/sqrt(D)."""
+    q, k, v = _bf16(q), _bf16(k), _bf16(v)
+    if k.shape != v.shape:
+        raise ShapeError(f"k/v shape mismatch: {tuple(k.shape)} vs {tuple(v.shape)}")
+    B, Sq, H, D = q.shape
+    if k.shape[0] != B or k.shape[2] != H or k.shape[3] != D:
+        raise ShapeError("q/kv mismatch on batch, heads or head_dim")
+    o = _torch().empty_like(q)
+    check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Sq, k.shape[1], H,
+                              D, _stream()))
+    return o
+
+
+class KvCache:
+    """KvCache (kv_cache.hpp:16-50) as a device ring of frame slots."""
+
+    def __init__(self, tokens_per_frame, window_frames=None, heads=1, head_dim=2, capacity_frames=0,
+                 device=0):
+        self._h = ctypes.c_void_p()
+        self.heads, self.head_dim = heads, head_dim
+        self._tpf = tokens_per_frame
+        check(lib().spx_kv_ring_create(device, tokens_per_frame, -1 if window_frames is None else window_frames,
+                                       capacity_frames, heads, head_dim, ctypes.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().spx_kv_ring_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        out = i64_array([0] * 4)
+        check(lib().spx_kv_ring_info(self._h, out))
+        return list(out)
+
+    def update(self, block_index, k_block, v_block):
+        k, v = _bf16(k_block), _bf16(v_block)
+        if k.shape != v.shape:
+            raise ShapeError("k/v block shape mismatch")
+        if k.shape[2] != self.heads or k.shape[3] != self.head_dim:
+            raise ShapeError("block shape incompatible with cached frames")
+        check(lib().spx_kv_ring_update(self._h, block_index, k.data_ptr(), v.data_ptr(), k.shape[1], _stream()))
+
+    def read(self):
+        torch = _torch()
+        n = self.seq_len()
+        k = torch.empty(1, max(n, 1), self.heads, self.head_dim, dtype=torch.bfloat16, device="cuda")
+        v = torch.empty_like(k)
+        check(lib().spx_kv_ring_read(self._h, k.data_ptr(), v.data_ptr(), _stream()))
+        return k, v
+
+    def attention(self, q):
+        q = _bf16(q)
+        o = _torch().empty_like(q)
+        check(lib().spx_kv_ring_attention(self._h, q.data_ptr(), o.data_ptr(), q.shape[1], _stream()))
+        return o
+
+    def cached_frames(self):
+        return self._info()[0]
+
+    def seq_len(self):
+        return self._info()[1]
+
+    def empty(self):
+        return self.cached_frames() == 0
+
+    def oldest_block_index(self):
+        info = self._info()
+        if info[0] == 0:
+            raise EmptyCacheError("oldest_block_index() on an empty cache")
+        return info[2]
+
+    def capacity_frames(self):
+        return self._info()[3]
+
+
+class CommStats(dict):
+    pass
+
+
+class CommWorld:
+    """CommWorld (collectives.hpp:39-113): LOCAL transport, every rank in this process.
+
+    devices: per-rank CUDA device ids (default: all ranks share the current device)."""
+
+    def __init__(self, world_size, devices: Optional[Sequence[int]] = None, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+        else:
+            self._h = ctypes.c_void_p()
+            devs = (ctypes.c_int * world_size)(*devices) if devices else None
+            check(lib().spx_world_create_local(world_size, devs, ctypes.byref(self._h)))
+        self._world_size = self.info()[0]
+
+    @classmethod
+    def nccl(cls, rank, world_size, unique_id: bytes, device):
+        h = ctypes.c_void_p()
+        uid = (ctypes.c_uint8 * 128)(*unique_id)
+        check(lib().spx_world_create_nccl(rank, world_size, uid, device, ctypes.byref(h)))
+        return cls(world_size, _handle=h)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        uid = (ctypes.c_uint8 * 128)()
+        check(lib().spx_nccl_get_unique_id(uid))
+        return bytes(uid)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().spx_world_destroy(self._h)
+            self._h = None
+
+    def info(self):
+        out = (ctypes.c_int32 * 4)()
+        check(lib().spx_world_info(self._h, out))
+        return list(out)
+
+    def world_size(self):
+        return self._world_size
+
+    def stats(self) -> dict:
+        s = _lib.CommStats()
+        check(lib().spx_world_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        check(lib().spx_world_reset_stats(self._h))
+
+    def synchronize(self):
+        check(lib().spx_world_synchronize(self._h))
+
+    def _sync_in(self):
+        _torch().cuda.synchronize()
+
+    @staticmethod
+    def _raw(t):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ShapeError("expected contiguous CUDA tensors")
+        return t.data_ptr()
+
+    def all_to_all(self, xs: List, scatter_dim: Axis, gather_dim: Axis):
+        """all_to_all (collectives.cpp:203-235) for every rank: xs[r] is rank r's tensor."""
+        torch = _torch()
+        P = self._world_size
+        shape = list(xs[0].shape)
+        out_shape = list(shape)
+        if shape[scatter_dim] % P:
+            raise PartitionError(f"all_to_all scatter extent {shape[scatter_dim]} not divisible by world size {P}")
+        out_shape[scatter_dim] //= P
+        out_shape[gather_dim] *= P
+        outs = [torch.empty(out_shape, dtype=x.dtype, device=x.device) for x in xs]
+        self._sync_in()
+        check(lib().spx_all_to_all(self._h, ptr_array([self._raw(x) for x in xs]),
+                                   ptr_array([o.data_ptr() for o in outs]), i64_array(shape),
+                                   xs[0].element_size(), int(scatter_dim), int(gather_dim)))
+        self.synchronize()
+        return outs
+
+    def fused_all_to_all(self, qs, ks, vs, scatter_dim=Axis.Heads, gather_dim=Axis.Seq):
+        """fused_all_to_all (collectives.cpp:237-276): one invocation, one round."""
+        torch = _torch()
+        P = self._world_size
+        shape = list(qs[0].shape)
+        if shape[scatter_dim] % P:
+            raise PartitionError(f"fused_all_to_all scatter extent {shape[scatter_dim]} not divisible by world size {P}")
+        out_shape = list(shape)
+        out_shape[scatter_dim] //= P
+        out_shape[gather_dim] *= P
+        outs = [[torch.empty(out_shape, dtype=t.dtype, device=t.device) for t in ts] for ts in (qs, ks, vs)]
+        self._sync_in()
+        arrs = [ptr_array([self._raw(t) for t in ts]) for ts in (qs, ks, vs)]
+        oarrs = [ptr_array([t.data_ptr() for t in ts]) for ts in outs]
+        check(lib().spx_fused_all_to_all(self._h, *arrs, *oarrs, i64_array(shape), qs[0].element_size(),
+                                         int(scatter_dim), int(gather_dim)))
+        self.synchronize()
+        return outs
+
+    def all_gather(self, xs, dim: Axis):
+        """all_gather (collectives.cpp:180-201)."""
+        torch = _torch()
+        P = self._world_size
+        shape = list(xs[0].shape)
+        out_shape = list(shape)
+        out_shape[dim] *= P
+        outs = [torch.empty(out_shape, dtype=x.dtype, device=x.device) for x in xs]
+        self._sync_in()
+        check(lib().spx_all_gather(self._h, ptr_array([self._raw(x) for x in xs]),
+                                   ptr_array([o.data_ptr() for o in outs]), i64_array(shape),
+                                   xs[0].element_size(), int(dim)))
+        self.synchronize()
+        return outs
+
+
+@dataclass
+class GenerationConfig:
+    """GenerationConfig (generator.hpp:14-42) with the device knobs of spx_engine_config."""
+
+    grid_per_block: GridSpec = field(default_factory=lambda: GridSpec(3, 4, 4))
+    num_blocks: int = 5
+    layers: int = 4
+    denoise_steps: int = 2
+    batch: int = 1
+    heads: int = 8
+    head_dim: int = 16
+    world_size: int = 1
+    seed: int = 0
+    window_frames: Optional[int] = None
+    rope_base: float = 10000.0
+    band_split: Optional[BandSplit] = None
+    force_start_frame_zero: bool = False
+    qk_norm: bool = False
+    norm_eps: float = 1e-6
+    profile: bool = False
+
+    def block_len(self):
+        return self.grid_per_block.seq_len()
+
+    def local_len(self):
+        return self.block_len() // self.world_size
+
+    def total_calls(self):
+        return self.num_blocks * self.denoise_steps * self.layers
+
+    def to_c(self) -> _lib.EngineConfig:
+        c = _lib.EngineConfig()
+        lib().spx_engine_config_defaults(ctypes.byref(c))
+        g = self.grid_per_block
+        c.frames, c.grid_h, c.grid_w = g.frames, g.height, g.width
+        c.num_blocks, c.layers, c.denoise_steps = self.num_blocks, self.layers, self.denoise_steps
+        c.batch, c.heads, c.head_dim = self.batch, self.heads, self.head_dim
+        c.window_frames = -1 if self.window_frames is None else self.window_frames
+        c.rope_base = self.rope_base
+        if self.band_split is not None:
+            c.band_split[0], c.band_split[1], c.band_split[2] = (self.band_split.temporal, self.band_split.height,
+                                                                 self.band_split.width)
+        c.seed = self.seed
+        c.force_start_frame_zero = int(self.force_start_frame_zero)
+        c.qk_norm = int(self.qk_norm)
+        c.norm_eps = self.norm_eps
+        c.profile = int(self.profile)
+        return c
+
+    def validate(self):
+        """GenerationConfig::validate (generator.cpp:7-38) + device constraints."""
+        c = self.to_c()
+        check(lib().spx_engine_config_validate(ctypes.byref(c), self.world_size))
+
+
+STAGES = ("qkv", "rope", "gather_or_fused", "cache", "attention", "output_exchange")
+
+
+class Engine:
+    """The optimized Causal-RoPE SP schedule + generator on device (spx_engine)."""
+
+    def __init__(self, cfg: GenerationConfig, world: Optional[CommWorld] = None, seed_weights=True):
+        self.cfg = cfg
+        self.world = world if world is not None else CommWorld(cfg.world_size)
+        self._c = cfg.to_c()
+        self._h = ctypes.c_void_p()
+        check(lib().spx_engine_create(self.world._h, ctypes.byref(self._c), ctypes.byref(self._h)))
+        info = i64_array([0] * 8)
+        check(lib().spx_engine_info(self._h, info))
+        (self.head_groups, self.query_splits, self.block_len, self.local_len, self.heads_per_group,
+         self.query_rows, self.capacity_frames, self.model_dim) = list(info)
+        self.local_ranks = self.world.info()[1]
+        if seed_weights:
+            check(lib().spx_engine_seed_weights(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().spx_engine_destroy(self._h)
+            self._h = None
+
+    def set_layer_weights(self, layer, wq, wk, wv, wo):
+        """host weights (dim, dim) [out][in]; float arrays are rounded to bf16 (RNE)."""
+        self.set_layer_weights_bits(layer, *[float_to_bf16_bits(w) for w in (wq, wk, wv, wo)])
+
+    def set_layer_weights_bits(self, layer, wq, wk, wv, wo):
+        arrs = [np.ascontiguousarray(w, dtype=np.uint16) for w in (wq, wk, wv, wo)]
+        check(lib().spx_engine_set_layer_weights(self._h, layer, *[a.ctypes.data for a in arrs]))
+
+    def set_norm_weights_bits(self, layer, wq, wk):
+        a = np.ascontiguousarray(wq, dtype=np.uint16)
+        b = np.ascontiguousarray(wk, dtype=np.uint16)
+        check(lib().spx_engine_set_norm_weights(self._h, layer, a.ctypes.data, b.ctypes.data))
+
+    def begin_block(self, block_index):
+        check(lib().spx_engine_begin_block(self._h, block_index))
+
+    def optimized_sp_self_attention(self, layer, block_index, start_frame, x_locals):
+        """one optimized_sp_self_attention call (sp_attention.hpp:118-130) on every rank."""
+        torch = _torch()
+        ys = [torch.empty_like(x) for x in x_locals]
+        torch.cuda.synchronize()
+        check(lib().spx_engine_layer(self._h, layer, block_index, start_frame,
+                                     ptr_array([_bf16(x).data_ptr() for x in x_locals]),
+                                     ptr_array([y.data_ptr() for y in ys])))
+        check(lib().spx_engine_synchronize(self._h))
+        return ys
+
+    def generate_block(self, block, noise_bits: Optional[np.ndarray] = None) -> np.ndarray:
+        """bf16 bits (rows_local * local_ranks, H, D) of the block output."""
+        rows = self.local_len * self.local_ranks
+        out = np.empty((rows, self.cfg.heads, self.cfg.head_dim), dtype=np.uint16)
+        nz = None
+        if noise_bits is not None:
+            nz = np.ascontiguousarray(noise_bits, dtype=np.uint16)
+        check(lib().spx_engine_generate_block(self._h, block, nz.ctypes.data if nz is not None else None,
+                                              out.ctypes.data))
+        return out
+
+    def generate(self) -> np.ndarray:
+        rows = self.local_len * self.local_ranks
+        out = np.empty((self.cfg.num_blocks, rows, self.cfg.heads, self.cfg.head_dim), dtype=np.uint16)
+        check(lib().spx_engine_generate(self._h, out.ctypes.data))
+        return out
+
+    def stage_times(self):
+        ms = (ctypes.c_double * 6)()
+        calls = ctypes.c_int64()
+        check(lib().spx_engine_stage_times(self._h, ms, ctypes.byref(calls)))
+        return dict(zip(STAGES, list(ms))), calls.value
+
+    def reset_stage_times(self):
+        check(lib().spx_engine_reset_stage_times(self._h))
+
+    def stats(self) -> dict:
+        s = _lib.CommStats()
+        check(lib().spx_engine_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+
+def bf16_bits_to_float(bits: np.ndarray) -> np.ndarray:
+    b = np.asarray(bits, dtype=np.uint16)
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def float_to_bf16_bits(x) -> np.ndarray:
+    d = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    out = np.empty(d.size, dtype=np.uint16)
+    check(lib().spx_f64_to_bf16(d.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), d.size))
+    return out.reshape(np.shape(x))
+
+
+def generate(cfg: GenerationConfig) -> np.ndarray:
+    """generate(cfg) (generator.hpp:65): block outputs as float64 (bf16 values), (blocks, L, H, D)."""
+    eng = Engine(cfg)
+    return bf16_bits_to_float(eng.generate())
