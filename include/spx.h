@@ -190,6 +190,19 @@ spx_status spx_fused_all_to_all(spx_world* world, void* const* q_in, void* const
 spx_status spx_all_gather(spx_world* world, void* const* in, void* const* out,
                           const int64_t shape[4], int32_t elem_bytes, int32_t axis);
 
+/* Partition of P ranks over H heads and a block of L tokens: out = G (head groups),
+ * S (query splits), L/P, L/S, H/G. Ulysses (S = 1) whenever H % P == 0. */
+spx_status spx_partition(int32_t world_size, int64_t heads, int64_t block_len, int64_t head_dim,
+                         int64_t out[5]);
+/* The cross-rank transfers one rank posts in one exchange round (which = 0: q/k/v exchange
+ * replacing fused_all_to_all, collectives.cpp:237-276; which = 1: output all_to_all,
+ * collectives.cpp:203-235), in posting order. Row i of out (6 int64): peer, is_send,
+ * buffer id (0 q_send, 1 k_send, 2 v_send, 3 o_send, 4 q_recv, 5 ring_k, 6 ring_v, 7 o_recv),
+ * element offset, element count, 0. The NCCL transport executes exactly this list. */
+spx_status spx_exchange_plan(int32_t which, int32_t rank, int32_t world_size, int64_t heads,
+                             int64_t block_len, int64_t head_dim, int64_t block_base_row,
+                             int64_t* out, int64_t max_entries, int64_t* n_entries);
+
 /* ---------------------------------------------------------------------------------------
  * Engine: the optimized Causal-RoPE SP schedule (sp_self_attention_engine, all flags on:
  * proj/src/sp_attention.cpp:197-313) and the block-wise AR driver (generate:

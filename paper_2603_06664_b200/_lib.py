@@ -139,6 +139,9 @@ _SIGS = [
                                                                            c_int32, c_int32]),
     ("spx_all_gather", c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_int64),
                                c_int32, c_int32]),
+    ("spx_partition", c_int, [c_int32, c_int64, c_int64, c_int64, POINTER(c_int64)]),
+    ("spx_exchange_plan", c_int, [c_int32, c_int32, c_int32, c_int64, c_int64, c_int64, c_int64,
+                                  POINTER(c_int64), c_int64, POINTER(c_int64)]),
     ("spx_engine_config_defaults", None, [POINTER(EngineConfig)]),
     ("spx_engine_config_validate", c_int, [POINTER(EngineConfig), c_int32]),
     ("spx_engine_create", c_int, [c_void_p, POINTER(EngineConfig), POINTER(c_void_p)]),

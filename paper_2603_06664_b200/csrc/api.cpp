@@ -11,6 +11,7 @@
 #include "../../include/spx.h"
 #include "common.hpp"
 #include "engine.hpp"
+#include "exchange_plan.hpp"
 #include "host_rng.hpp"
 #include "kernels.hpp"
 #include "kv_ring.hpp"
@@ -584,6 +585,44 @@ spx_status spx_all_gather(spx_world* world, void* const* in, void* const* out,
         require_ptr(world, "world");
         require(in && out && shape, SPX_ERR_CONFIG, "null argument");
         world->w->all_gather(in, out, shape, elem_bytes, axis);
+    });
+}
+
+spx_status spx_partition(int32_t world_size, int64_t heads, int64_t block_len, int64_t head_dim,
+                         int64_t out[5]) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        require(heads >= 1 && head_dim >= 1, SPX_ERR_SHAPE, "bad head shape");
+        const Partition p = Partition::make(world_size, heads, block_len, head_dim);
+        out[0] = p.G;
+        out[1] = p.S;
+        out[2] = p.Lp;
+        out[3] = p.Lq;
+        out[4] = p.Hl;
+    });
+}
+
+spx_status spx_exchange_plan(int32_t which, int32_t rank, int32_t world_size, int64_t heads,
+                             int64_t block_len, int64_t head_dim, int64_t block_base_row,
+                             int64_t* out, int64_t max_entries, int64_t* n_entries) {
+    return guarded([&] {
+        require(out && n_entries, SPX_ERR_CONFIG, "null argument");
+        require(rank >= 0 && rank < world_size, SPX_ERR_COLLECTIVE, "rank out of range");
+        const Partition p = Partition::make(world_size, heads, block_len, head_dim);
+        const std::vector<Transfer> plan =
+            which == 0 ? plan_qkv_exchange(p, rank, block_base_row) : plan_out_exchange(p, rank);
+        require(static_cast<int64_t>(plan.size()) <= max_entries, SPX_ERR_RANGE,
+                "plan has more entries than the output holds");
+        for (size_t i = 0; i < plan.size(); ++i) {
+            int64_t* r = out + 6 * i;
+            r[0] = plan[i].peer;
+            r[1] = plan[i].is_send;
+            r[2] = plan[i].buf;
+            r[3] = plan[i].offset;
+            r[4] = plan[i].elems;
+            r[5] = 0;
+        }
+        *n_entries = static_cast<int64_t>(plan.size());
     });
 }
 

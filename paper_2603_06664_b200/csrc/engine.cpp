@@ -88,6 +88,7 @@ Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_
     Lp_ = L_ / P_;
     Lq_ = L_ / S_;
     Hl_ = H_ / G_;
+    part_ = Partition::make(P_, H_, L_, D_);
     cap_frames_ = cfg.window_frames < 0 ? cfg.num_blocks * F_
                                         : ceil_div(cfg.window_frames, F_) * F_;
     frames_ = FrameRing(cap_frames_, cfg.window_frames);
@@ -377,8 +378,6 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
     const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
     const int nl = static_cast<int>(ranks_.size());
     const int64_t slab = Lp_ * Hl_ * D_;
-    const size_t slab_bytes = static_cast<size_t>(slab) * sizeof(bf16);
-    const int64_t row_elems = Hl_ * D_;
 
     StageEvents* prof = nullptr;
     if (cfg_.profile) {
@@ -416,34 +415,13 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
                     SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(lj)].ev_k3, 0));
         }
     } else if (P_ > 1) {
+        // one NCCL group == one round: the plan's sends and receives (exchange_plan.cpp)
         RankState& rs = ranks_[0];
         SPX_CUDA(cudaSetDevice(rs.device));
-        KvRingStorage& ring = rs.rings[static_cast<size_t>(layer)];
-        world_->group_start();
-        for (int64_t g = 0; g < G_; ++g) {
-            const int d = static_cast<int>(rs.p * G_ + g);
-            if (d != rs.rank) world_->send(rs.q_send + g * slab, slab_bytes, d, rs.stream);
-        }
-        for (int d = 0; d < P_; ++d) {
-            if (d == rs.rank) continue;
-            const int64_t gd = d % G_;
-            world_->send(rs.k_send + gd * slab, slab_bytes, d, rs.stream);
-            world_->send(rs.v_send + gd * slab, slab_bytes, d, rs.stream);
-        }
-        for (int64_t c = 0; c < G_; ++c) {
-            const int i = static_cast<int>(rs.p * G_ + c);
-            if (i != rs.rank) world_->recv(rs.q_recv + c * slab, slab_bytes, i, rs.stream);
-        }
-        for (int i = 0; i < P_; ++i) {
-            if (i == rs.rank) continue;
-            const int64_t row0 = block_base_row_ + static_cast<int64_t>(i) * Lp_;
-            world_->recv(ring.k + row0 * row_elems, slab_bytes, i, rs.stream);
-            world_->recv(ring.v + row0 * row_elems, slab_bytes, i, rs.stream);
-        }
-        world_->group_end();
+        run_plan(rs, layer, plan_qkv_exchange(part_, rs.rank, block_base_row_));
     }
     // ledger: one fused exchange (q: G-1 peers, k/v: P-1 peers per source) ...
-    world_->add_stats(0, 0, 1, P_ * ((G_ - 1) + 2 * (P_ - 1)) * slab, 1);
+    world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
 
     // K6 attention, output rows stored straight into their source's o_recv slab
     for (int li = 0; li < nl; ++li) {
@@ -479,19 +457,10 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
     } else if (P_ > 1) {
         RankState& rs = ranks_[0];
         SPX_CUDA(cudaSetDevice(rs.device));
-        world_->group_start();
-        for (int64_t c = 0; c < G_; ++c) {
-            const int i = static_cast<int>(rs.p * G_ + c);
-            if (i != rs.rank) world_->send(rs.o_send + c * slab, slab_bytes, i, rs.stream);
-        }
-        for (int64_t c = 0; c < G_; ++c) {
-            const int j = static_cast<int>(rs.p * G_ + c);
-            if (j != rs.rank) world_->recv(rs.o_recv + (j % G_) * slab, slab_bytes, j, rs.stream);
-        }
-        world_->group_end();
+        run_plan(rs, layer, plan_out_exchange(part_, rs.rank));
     }
     // ... and one output all-to-all (G-1 peers per rank)
-    world_->add_stats(0, 1, 0, P_ * (G_ - 1) * slab, 1);
+    world_->add_stats(0, 1, 0, out_exchange_elements(part_), 1);
 
     // K8 output projection
     for (int li = 0; li < nl; ++li) {
@@ -500,6 +469,23 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         gemm_run(*oproj[static_cast<size_t>(li)], rs.stream);
         mark(li, 6);
     }
+}
+
+void Engine::run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>& plan) {
+    KvRingStorage& ring = rs.rings[static_cast<size_t>(layer)];
+    bf16* bases[8] = {rs.q_send, rs.k_send, rs.v_send, rs.o_send, rs.q_recv, ring.k, ring.v,
+                      rs.o_recv};
+    world_->group_start();
+    for (const Transfer& t : plan) {
+        bf16* p = bases[t.buf] + t.offset;
+        const size_t bytes = static_cast<size_t>(t.elems) * sizeof(bf16);
+        if (t.is_send) {
+            world_->send(p, bytes, t.peer, rs.stream);
+        } else {
+            world_->recv(p, bytes, t.peer, rs.stream);
+        }
+    }
+    world_->group_end();
 }
 
 void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,

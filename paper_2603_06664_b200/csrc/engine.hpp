@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/spx.h"
+#include "exchange_plan.hpp"
 #include "kernels.hpp"
 #include "kv_ring.hpp"
 #include "rope_table.hpp"
@@ -104,6 +105,7 @@ class Engine {
     void run_layer(int64_t layer, int64_t start_frame, const std::vector<const GemmPlan*>& qkv,
                    const std::vector<const GemmPlan*>& oproj);
     void harvest_events();
+    void run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>& plan);
     RopeLaunch rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const;
     int local_of(int rank) const;
 
@@ -112,6 +114,7 @@ class Engine {
     // geometry
     int64_t F_, Hg_, Wg_, HW_, L_, H_, D_, C_, P_, G_, S_, Lp_, Lq_, Hl_;
     int64_t cap_frames_ = 0;
+    Partition part_{};
     std::unique_ptr<RopeTable> table_;
     std::map<int, DeviceWeights> weights_;
     std::vector<RankState> ranks_;  // local ranks
