@@ -309,6 +309,371 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// =========================================================================================
+// v2: one 128-row query tile per CTA, its KV range split between two softmax warpgroups
+// (slot 0: first half of the kv tiles, slot 1: second half) that ping-pong against the
+// single MMA thread, P written back into TMEM over its S (TS-MMA: A operand from TMEM),
+// K/V tiles streamed through one 6-deep smem ring in exact MMA consumption order, and the
+// two partial (O, m, l) merged in-CTA at the end (TMEM is CTA-wide: each warpgroup reads
+// both O accumulators for its half of the head dim).
+//
+//   warp 0      TMA producer            warp 1   MMA issuer (one thread)
+//   warp 2      TMEM allocator          warp 3   idle
+//   warps 4-7   softmax slot 0          warps 8-11 softmax slot 1
+//   TMEM: S0 | S1 | O0 | O1 (128 columns each); P_i (bf16 pairs) over S_i columns 0..63
+// =========================================================================================
+constexpr int kThreadsV2 = 384;
+constexpr int kSlotsV2 = 5;
+
+template <int D>
+struct SmemV2 {
+    static constexpr uint32_t kChunks = D / 64;
+    static constexpr uint32_t kTileBytes = kBKV * D * 2;
+    static constexpr uint32_t kSlots = D == 128 ? kSlotsV2 : 2 * kSlotsV2;
+    static constexpr uint32_t kOffQ = 0;
+    static constexpr uint32_t kOffRing = kOffQ + kBQ * D * 2;
+    static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
+    static constexpr uint32_t kNumBars = 1 + 2 * kSlots + 6;
+    static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
+    static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
+};
+
+__device__ __forceinline__ void setmaxnreg_dec56() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+}
+__device__ __forceinline__ void setmaxnreg_inc224() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+
+// 2^x on the FMA pipe (offloads part of the exponentials from MUFU): round-to-nearest split,
+// degree-3 minimax for 2^f on [-1/2, 1/2] (max rel. error 8.4e-5 << bf16's 2^-9)
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -127.0f);
+    const float t = x + 12582912.0f;
+    const int ji = __float_as_int(t) - 0x4B400000;
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(0.0553458875f, f, 0.24260599f);
+    p = fmaf(p, f, 0.69322751f);
+    p = fmaf(p, f, 0.999927776f);
+    return __int_as_float(__float_as_int(p) + (ji << 23));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreadsV2, 1)
+    attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap map_q,
+                       const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
+    using L = SmemV2<D>;
+    constexpr uint32_t kSlots = L::kSlots;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sQ = smem + L::kOffQ;
+    uint8_t* ring = smem + L::kOffRing;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+    uint64_t* q_full = bars;
+    uint64_t* slot_full = bars + 1;
+    uint64_t* slot_empty = slot_full + kSlots;
+    uint64_t* s_full = slot_empty + kSlots;  // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* pv_done = p_full + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+    float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
+    float* st_l = st_m + 256;                                     // [2][128]
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int q_tile = blockIdx.x;
+    const int head = blockIdx.y;
+    const int n_total = p.total_tiles;
+    const int n0 = (n_total + 1) / 2;
+    const int n1 = n_total - n0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_q);
+        tma_prefetch_desc(&map_k);
+        tma_prefetch_desc(&map_v);
+        mbar_init(q_full, 1);
+        for (uint32_t s = 0; s < kSlots; ++s) {
+            mbar_init(&slot_full[s], 1);
+            mbar_init(&slot_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&pv_done[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 4) {
+        setmaxnreg_dec56();
+        if (warp == 0 && lane == 0) {
+            // ---------------- TMA producer: the MMA consumption order ----------------
+            mbar_arrive_expect_tx(q_full, kBQ * D * 2);
+#pragma unroll
+            for (int c = 0; c < (int)L::kChunks; ++c)
+                tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
+            uint32_t t = 0;
+            auto load = [&](bool is_v, int g) {
+                const uint32_t slot = t % kSlots;
+                const uint32_t ph = (t / kSlots) & 1;
+                mbar_wait(&slot_empty[slot], ph ^ 1);
+                mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
+                int row, valid;
+                kv_tile_coords(p, g, row, valid);
+                uint8_t* dst = ring + slot * L::kTileBytes;
+#pragma unroll
+                for (int c = 0; c < (int)L::kChunks; ++c)
+                    tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
+                                c * 64, head, row);
+                ++t;
+            };
+            load(false, 0);
+            if (n1 > 0) load(false, n0);
+            for (int j = 0; j < n0; ++j) {
+                load(true, j);
+                if (j + 1 < n0) load(false, j + 1);
+                if (j < n1) {
+                    load(true, n0 + j);
+                    if (j + 1 < n1) load(false, n0 + j + 1);
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
+            const uint32_t q_addr = smem_u32(sQ);
+            const uint32_t ring_addr = smem_u32(ring);
+            uint32_t t = 0;
+            auto take = [&]() {
+                const uint32_t slot = t % kSlots;
+                mbar_wait(&slot_full[slot], (t / kSlots) & 1);
+                tc_fence_after();
+                ++t;
+                return slot;
+            };
+            auto issue_s = [&](int i) {
+                const uint32_t slot = take();
+                const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                    umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
+                                 make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[i]);
+                umma_commit(&slot_empty[slot]);
+            };
+            auto issue_pv = [&](int i, int j) {
+                const uint32_t slot = take();
+                mbar_wait(&p_full[i], j & 1);
+                tc_fence_after();
+                const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kBKV / 16; ++kk) {
+                    umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                                 make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                 idesc_o, (j | kk) != 0);
+                }
+                umma_commit(&pv_done[i]);
+                umma_commit(&slot_empty[slot]);
+            };
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            issue_s(0);
+            if (n1 > 0) issue_s(1);
+            for (int j = 0; j < n0; ++j) {
+                issue_pv(0, j);
+                if (j + 1 < n0) issue_s(0);
+                if (j < n1) {
+                    issue_pv(1, j);
+                    if (j + 1 < n1) issue_s(1);
+                }
+            }
+        }
+    } else {
+        setmaxnreg_inc224();
+        // ---------------- softmax warpgroups ----------------
+        const int i = (warp - 4) / 4;           // slot
+        const int q = warp % 4;                 // TMEM lane quarter
+        const int r = q * 32 + lane;            // query row in the tile == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const uint32_t t_s = tmem_base + i * 128 + lane_off;
+        const uint32_t t_o = tmem_base + 256 + i * 128 + lane_off;
+        const int n = i == 0 ? n0 : n1;
+        const int g0 = i == 0 ? 0 : n0;
+        const float scale = p.scale_log2;
+        float m_run = -INFINITY;
+        float l_run = 0.0f;
+        for (int j = 0; j < n; ++j) {
+            int row, valid;
+            kv_tile_coords(p, g0 + j, row, valid);
+            mbar_wait(&s_full[i], j & 1);
+            tc_fence_after();
+            uint32_t u[kBKV];
+#pragma unroll
+            for (int c = 0; c < kBKV / 32; ++c)
+                tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+            tmem_ld_wait();
+            float mx = -INFINITY;
+            if (valid == kBKV) {
+#pragma unroll
+                for (int c = 0; c < kBKV; ++c) mx = fmaxf(mx, __uint_as_float(u[c]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < kBKV; ++c)
+                    if (c < valid) mx = fmaxf(mx, __uint_as_float(u[c]));
+            }
+            const float m_new = fmaxf(m_run, mx * scale);
+            if (j == 0) {
+                m_run = m_new;
+            } else if (__any_sync(0xffffffffu, m_new > m_run + kRescaleThreshold)) {
+                mbar_wait(&pv_done[i], (j - 1) & 1);
+                tc_fence_after();
+                const float alpha = ex2_approx(m_run - m_new);
+#pragma unroll 1
+                for (int c = 0; c < D / 32; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(t_o + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tmem_st32(t_o + c * 32, o);
+                }
+                tmem_st_wait();
+                l_run *= alpha;
+                m_run = m_new;
+            }
+            const float neg_m = -m_run;
+            float lsum0 = 0.0f, lsum1 = 0.0f;
+            uint32_t pk[kBKV / 2];
+#pragma unroll
+            for (int e = 0; e < kBKV / 2; ++e) {
+                const float x0 = fmaf(__uint_as_float(u[2 * e]), scale, neg_m);
+                const float x1 = fmaf(__uint_as_float(u[2 * e + 1]), scale, neg_m);
+                float p0, p1;
+                if ((e & 7) >= 6) {  // 1/4 of the exponentials on the FMA pipe
+                    p0 = ex2_poly(x0);
+                    p1 = ex2_poly(x1);
+                } else {
+                    p0 = ex2_approx(x0);
+                    p1 = ex2_approx(x1);
+                }
+                if (valid != kBKV) {
+                    if (2 * e >= valid) p0 = 0.0f;
+                    if (2 * e + 1 >= valid) p1 = 0.0f;
+                }
+                lsum0 += p0;
+                lsum1 += p1;
+                pk[e] = pack_bf16x2(p0, p1);
+            }
+            l_run += lsum0 + lsum1;
+#pragma unroll
+            for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_s + c * 16, &pk[c * 16]);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[i]);
+        }
+        if (n > 0) {
+            mbar_wait(&pv_done[i], (n - 1) & 1);
+            tc_fence_after();
+        }
+        st_m[i * 128 + r] = m_run;
+        st_l[i * 128 + r] = l_run;
+        tc_fence_before();
+        named_bar_sync(1, 256);
+        tc_fence_after();
+        // merge the two partial softmaxes; warpgroup i stores head-dim columns [i D/2, (i+1) D/2)
+        const int qi = q_tile * kBQ + r;
+        const float m0 = st_m[r], l0 = st_l[r];
+        const float m1 = n1 > 0 ? st_m[128 + r] : -INFINITY;
+        const float l1 = n1 > 0 ? st_l[128 + r] : 0.0f;
+        const float mm = fmaxf(m0, m1);
+        const float a0 = ex2_approx(m0 - mm);
+        const float a1 = n1 > 0 ? ex2_approx(m1 - mm) : 0.0f;
+        const float inv = 1.0f / (l0 * a0 + l1 * a1);
+        const float w0 = a0 * inv, w1 = a1 * inv;
+        bf16* dst = nullptr;
+        if (qi < p.sq) {
+            const int chunk = qi / p.rows_per_chunk;
+            dst = p.out_base[chunk] +
+                  static_cast<int64_t>(qi - chunk * p.rows_per_chunk) * p.out_row_stride +
+                  static_cast<int64_t>(head) * D;
+        }
+        const uint32_t t_o0 = tmem_base + 256 + lane_off;
+        const uint32_t t_o1 = tmem_base + 384 + lane_off;
+#pragma unroll 1
+        for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+            uint32_t o0[32], o1[32];
+            tmem_ld32(t_o0 + c * 32, o0);
+            if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
+            tmem_ld_wait();
+            if (dst) {
+                float f[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    f[e] = __uint_as_float(o0[e]) * w0 + (n1 > 0 ? __uint_as_float(o1[e]) * w1 : 0.0f);
+                uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    d4[v] = make_uint4(pack_bf16x2(f[8 * v + 0], f[8 * v + 1]),
+                                       pack_bf16x2(f[8 * v + 2], f[8 * v + 3]),
+                                       pack_bf16x2(f[8 * v + 4], f[8 * v + 5]),
+                                       pack_bf16x2(f[8 * v + 6], f[8 * v + 7]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+template <int D>
+void attn_v2_set_attr() {
+    static bool done[64] = {};
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 63]) {
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v2_kernel<D>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(SmemV2<D>::kBytes)));
+        done[dev & 63] = true;
+    }
+}
+
 template <int D>
 void attn_set_attr() {
     static bool done[64] = {};
@@ -389,13 +754,27 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     p.out_batch_stride = o.out_batch_stride;
     dim3 grid(static_cast<unsigned>(ceil_div(o.sq, kBQ)), static_cast<unsigned>(o.heads),
               static_cast<unsigned>(o.batch));
-    if (o.head_dim == 128) {
-        attn_set_attr<128>();
-        attn_fwd_kernel<128><<<grid, kThreads, AttnSmem<128>::kBytes, stream>>>(
+    static const bool use_v1 = [] {
+        const char* e = std::getenv("SPX_ATTN_KERNEL");
+        return e && std::string(e) == "v1";
+    }();
+    if (use_v1) {
+        if (o.head_dim == 128) {
+            attn_set_attr<128>();
+            attn_fwd_kernel<128><<<grid, kThreads, AttnSmem<128>::kBytes, stream>>>(
+                plan.map_q, plan.map_k, plan.map_v, p);
+        } else {
+            attn_set_attr<64>();
+            attn_fwd_kernel<64><<<grid, kThreads, AttnSmem<64>::kBytes, stream>>>(
+                plan.map_q, plan.map_k, plan.map_v, p);
+        }
+    } else if (o.head_dim == 128) {
+        attn_v2_set_attr<128>();
+        attn_fwd_v2_kernel<128><<<grid, kThreadsV2, SmemV2<128>::kBytes, stream>>>(
             plan.map_q, plan.map_k, plan.map_v, p);
     } else {
-        attn_set_attr<64>();
-        attn_fwd_kernel<64><<<grid, kThreads, AttnSmem<64>::kBytes, stream>>>(
+        attn_v2_set_attr<64>();
+        attn_fwd_v2_kernel<64><<<grid, kThreadsV2, SmemV2<64>::kBytes, stream>>>(
             plan.map_q, plan.map_k, plan.map_v, p);
     }
     SPX_CUDA_LAUNCH();
