@@ -306,7 +306,7 @@ def main():
                    "l2": "inputs larger than L2: 566 MB of weights + 58 MB KV ring stream per chunk"},
         "e2e": {"value": e2e_fps, "unit": "latent frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "first_frame_latency_ms": e2e_s / args.steps * 1e3},
-        "roofline": {"kernel": "attn_fwd_kernel<128>", "bound": "tensor", "achieved": achieved,
+        "roofline": {"kernel": "attn_fwd_v2_kernel<128>", "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "frac_of_burst_peak": achieved / peaks["bf16_tflops"],
                      "peak_source": peak_src + " sustained bf16",
