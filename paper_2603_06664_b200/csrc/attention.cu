@@ -372,7 +372,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 // 2^x on the FMA pipe (offloads part of the exponentials from MUFU): round-to-nearest split,
 // degree-3 minimax for 2^f on [-1/2, 1/2] (max rel. error 8.4e-5 << bf16's 2^-9)
 __device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -127.0f);
+    x = fmaxf(x, -126.0f);  // keeps the exponent add >= 0 (no sign/NaN wrap)
     const float t = x + 12582912.0f;
     const int ji = __float_as_int(t) - 0x4B400000;
     const float f = x - (t - 12582912.0f);
@@ -380,6 +380,57 @@ __device__ __forceinline__ float ex2_poly(float x) {
     p = fmaf(p, f, 0.69322751f);
     p = fmaf(p, f, 0.999927776f);
     return __int_as_float(__float_as_int(p) + (ji << 23));
+}
+
+// ---- packed f32x2 arithmetic (FFMA2 / FADD2: two lanes per issue slot on sm_100) ----
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5}; mov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// ex2_poly on a pair with packed arithmetic: 2 clamps + 3 FADD2 + 3 FFMA2 + 2 IMAD per pair.
+// bits(t) = 0x4B400000 + round(x); the constant's low 9 bits are zero, so
+// bits(t) << 23 == round(x) << 23 (mod 2^32) and the exponent add is one IMAD.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    constexpr float kC = 12582912.0f;  // 1.5 * 2^23
+    x.x = fmaxf(x.x, -126.0f);
+    x.y = fmaxf(x.y, -126.0f);
+    const float2 t = fadd2(x, make_float2(kC, kC));
+    const float2 f = fsub2(x, fsub2(t, make_float2(kC, kC)));
+    float2 p = ffma2(make_float2(0.0553458875f, 0.0553458875f), f,
+                     make_float2(0.24260599f, 0.24260599f));
+    p = ffma2(p, f, make_float2(0.69322751f, 0.69322751f));
+    p = ffma2(p, f, make_float2(0.999927776f, 0.999927776f));
+    return make_float2(
+        __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 template <int D>
@@ -545,15 +596,21 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             for (int c = 0; c < kBKV / 32; ++c)
                 tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
             tmem_ld_wait();
-            float mx = -INFINITY;
-            if (valid == kBKV) {
-#pragma unroll
-                for (int c = 0; c < kBKV; ++c) mx = fmaxf(mx, __uint_as_float(u[c]));
-            } else {
+            if (valid < kBKV) {  // ragged tail tile only: masked logits -> -inf (exp -> 0)
 #pragma unroll
                 for (int c = 0; c < kBKV; ++c)
-                    if (c < valid) mx = fmaxf(mx, __uint_as_float(u[c]));
+                    if (c >= valid) u[c] = 0xff800000u;
             }
+            // row max: four independent 3-input max chains
+            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < kBKV; c += 8) {
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4)
+                    mq[k4] = fmax3f(mq[k4], __uint_as_float(u[c + 2 * k4]),
+                                    __uint_as_float(u[c + 2 * k4 + 1]));
+            }
+            const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
             const float m_new = fmaxf(m_run, mx * scale);
             if (j == 0) {
                 m_run = m_new;
@@ -574,30 +631,30 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 l_run *= alpha;
                 m_run = m_new;
             }
-            const float neg_m = -m_run;
-            float lsum0 = 0.0f, lsum1 = 0.0f;
+            const float2 sc2 = make_float2(scale, scale);
+            const float2 nm2 = make_float2(-m_run, -m_run);
+            float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
             uint32_t pk[kBKV / 2];
 #pragma unroll
             for (int e = 0; e < kBKV / 2; ++e) {
-                const float x0 = fmaf(__uint_as_float(u[2 * e]), scale, neg_m);
-                const float x1 = fmaf(__uint_as_float(u[2 * e + 1]), scale, neg_m);
-                float p0, p1;
+                const float2 x = ffma2(
+                    make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2,
+                    nm2);
+                float2 pr;
                 if ((e & 7) >= 6) {  // 1/4 of the exponentials on the FMA pipe
-                    p0 = ex2_poly(x0);
-                    p1 = ex2_poly(x1);
+                    pr = ex2_poly2(x);
                 } else {
-                    p0 = ex2_approx(x0);
-                    p1 = ex2_approx(x1);
+                    pr.x = ex2_approx(x.x);
+                    pr.y = ex2_approx(x.y);
                 }
-                if (valid != kBKV) {
-                    if (2 * e >= valid) p0 = 0.0f;
-                    if (2 * e + 1 >= valid) p1 = 0.0f;
-                }
-                lsum0 += p0;
-                lsum1 += p1;
-                pk[e] = pack_bf16x2(p0, p1);
+                ls[e & 3] = fadd2(ls[e & 3], pr);
+                pk[e] = pack_bf16x2(pr.x, pr.y);
             }
-            l_run += lsum0 + lsum1;
+            {
+                const float2 s01 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+                l_run += s01.x + s01.y;
+            }
 #pragma unroll
             for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_s + c * 16, &pk[c * 16]);
             tmem_st_wait();

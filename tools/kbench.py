@@ -1,0 +1,103 @@
+"""Kernel microbenchmarks through the C ABI (CUDA events on the launching stream, warm,
+inputs resident in HBM). Prints one line per case: time, achieved rate, fraction of peak.
+
+usage: python tools/kbench.py [attn|gemm|rope|all] [iters]
+"""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2603_06664_b200._lib import check, lib  # noqa: E402
+
+PEAK_TF = 1590.0   # fallback burst bf16 (B200_PROFILING.md) unless MEASURED_PEAKS.json
+PEAK_GBS = 6650.0
+try:
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "MEASURED_PEAKS.json")) as f:
+        _p = json.load(f)
+        PEAK_TF = float(_p.get("bf16_tflops", PEAK_TF))
+        PEAK_GBS = float(_p.get("hbm_gbs", PEAK_GBS))
+except Exception:
+    pass
+
+
+def timeit(fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def attn(iters):
+    s = torch.cuda.current_stream().cuda_stream
+    for sq, skv, H in [(4680, 4680, 12), (4680, 32760, 12), (2340, 4680, 6), (1170, 4680, 3),
+                       (2340, 4680, 3), (4680, 14040, 12)]:
+        D = 128
+        q = (torch.randn(1, sq, H, D, device="cuda") * 0.5).to(torch.bfloat16)
+        k = (torch.randn(1, skv, H, D, device="cuda") * 0.5).to(torch.bfloat16)
+        v = torch.randn(1, skv, H, D, device="cuda").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        ms = timeit(lambda: check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                      o.data_ptr(), 1, sq, skv, H, D, s)), iters)
+        tf = 4.0 * sq * skv * H * D / (ms * 1e-3) / 1e12
+        print(json.dumps({"kernel": "attention", "sq": sq, "skv": skv, "heads": H, "ms": round(ms, 4),
+                          "tflops": round(tf, 1), "frac_peak": round(tf / PEAK_TF, 3)}), flush=True)
+
+
+def gemm(iters):
+    s = torch.cuda.current_stream().cuda_stream
+    for M, K, N in [(4680, 1536, 4608), (4680, 1536, 1536), (2340, 1536, 4608), (1170, 1536, 4608),
+                    (585, 1536, 4608), (8192, 8192, 8192)]:
+        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+        y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ms = timeit(lambda: check(lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                                           M, K, N, s)), iters)
+        tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
+        ref_ms = timeit(lambda: torch.matmul(x, w.t()), iters)
+        print(json.dumps({"kernel": "gemm", "M": M, "K": K, "N": N, "ms": round(ms, 4),
+                          "tflops": round(tf, 1), "frac_peak": round(tf / PEAK_TF, 3),
+                          "torch_ms": round(ref_ms, 4)}), flush=True)
+
+
+def rope(iters):
+    s = torch.cuda.current_stream().cuda_stream
+    tab = ctypes.c_void_p()
+    split = (ctypes.c_int64 * 3)(22, 21, 21)
+    check(lib().spx_rope_table_create(240, 30, 52, 128, 10000.0, split, ctypes.byref(tab)))
+    grid = (ctypes.c_int64 * 3)(3, 30, 52)
+    for P, norm in [(1, False), (1, True), (8, False)]:
+        Lp, H, D = 4680 // P, 12, 128
+        x = torch.randn(Lp, H, D, device="cuda").to(torch.bfloat16)
+        y = torch.empty_like(x)
+        nw = torch.ones(H * D, device="cuda", dtype=torch.bfloat16)
+        for start in (0, 18):
+            ms = timeit(lambda: check(lib().spx_rope_apply_causal_local(
+                tab, x.data_ptr(), y.data_ptr(), 1, Lp, H, D, grid, start, 0, P,
+                nw.data_ptr() if norm else None, 1e-6, s)), iters)
+            gbs = 2 * x.numel() * 2 / (ms * 1e-3) / 1e9
+            print(json.dumps({"kernel": "rope_single", "P": P, "norm": norm, "start": start,
+                              "ms": round(ms, 5), "GBs": round(gbs, 1),
+                              "frac_peak": round(gbs / PEAK_GBS, 3)}), flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    lib()
+    if which in ("attn", "all"):
+        attn(iters)
+    if which in ("gemm", "all"):
+        gemm(iters)
+    if which in ("rope", "all"):
+        rope(iters)

@@ -26,3 +26,19 @@ rows.sort(key=lambda r: -int(r["Warp Stall Sampling (All Samples)"] or 0))
 for r in rows[:top]:
     s = int(r["Warp Stall Sampling (All Samples)"] or 0)
     print(f"{s/tot:6.1%} {r['Address'][-5:]} {r['Source'].strip()[:90]}")
+
+# stall-reason totals (all samples), overall and excluding the top-2 wait instructions
+cols = [c for c in rows[0].keys() if c.startswith("stall_") and "Not Issued" not in c]
+def agg(rs):
+    t = collections.Counter()
+    for r in rs:
+        for c in cols:
+            t[c] += int(r[c] or 0)
+    s = sum(t.values()) or 1
+    return ", ".join(f"{k[6:]} {v/s:.0%}" for k, v in t.most_common(10) if v)
+print("stalls (all):", agg(rows))
+if len(sys.argv) > 4:
+    lo, hi = int(sys.argv[3], 16), int(sys.argv[4], 16)
+    sel = [r for r in rows if lo <= int(r["Address"], 16) % (1 << 20) <= hi]
+    n = sum(int(r["Warp Stall Sampling (All Samples)"] or 0) for r in sel)
+    print(f"range {sys.argv[3]}-{sys.argv[4]}: {n} samples ({n/tot:.1%});", agg(sel))
