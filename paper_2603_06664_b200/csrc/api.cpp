@@ -1,6 +1,8 @@
 // api.cpp -- the extern "C" boundary (include/spx.h). Each entry validates like the reference
 // function it replaces, converts spx::Error into a status code, and launches on the caller's
 // stream. No exception crosses this file.
+#include <map>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -327,6 +329,40 @@ spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tok
     });
 }
 
+namespace {
+// one attention launch with stream-ordered scratch for the split-KV partials
+void attention_oneshot(spx::AttnOperands a, cudaStream_t st) {
+    using namespace spx;
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    const int sms = device_sm_count(dev);
+    const size_t ws = attn_workspace_bytes(a, attn_max_splits(a, sms));
+    if (ws > 0) {
+        // cached per (device, stream): the kernel re-arms its own counters, so the buffer
+        // is zeroed only when it is (re)allocated; growth waits for the stream first
+        static std::mutex mu;
+        static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+        std::lock_guard<std::mutex> lock(mu);
+        auto& slot = cache[{dev, st}];
+        if (slot.second < ws) {
+            if (slot.first) {
+                SPX_CUDA(cudaStreamSynchronize(st));
+                SPX_CUDA(cudaFree(slot.first));
+            }
+            slot = {nullptr, 0};
+            SPX_CUDA(cudaMalloc(&slot.first, ws));
+            SPX_CUDA(cudaMemset(slot.first, 0, ws));
+            slot.second = ws;
+        }
+        a.workspace = slot.first;
+        a.workspace_bytes = slot.second;
+    }
+    AttnPlan plan;
+    attn_plan(&plan, a, sms);
+    attn_run(plan, st);
+}
+}  // namespace
+
 spx_status spx_attention(const void* q, const void* k, const void* v, void* o, int64_t batch,
                          int64_t sq, int64_t skv, int64_t heads, int64_t head_dim, void* stream) {
     return guarded([&] {
@@ -349,9 +385,7 @@ spx_status spx_attention(const void* q, const void* k, const void* v, void* o, i
         a.out_base[0] = static_cast<bf16*>(o);
         a.rows_per_chunk = static_cast<int>(sq);
         a.out_row_stride = heads * head_dim;
-        AttnPlan plan;
-        attn_plan(&plan, a);
-        attn_run(plan, as_stream(stream));
+        attention_oneshot(a, as_stream(stream));
     });
 }
 
@@ -474,9 +508,7 @@ spx_status spx_kv_ring_attention(const spx_kv_ring* ring, const void* q, void* o
         a.out_base[0] = static_cast<bf16*>(o);
         a.rows_per_chunk = static_cast<int>(sq);
         a.out_row_stride = ring->st.row_elems();
-        AttnPlan plan;
-        attn_plan(&plan, a);
-        attn_run(plan, as_stream(stream));
+        attention_oneshot(a, as_stream(stream));
     });
 }
 

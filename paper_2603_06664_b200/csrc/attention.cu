@@ -15,6 +15,8 @@
 //               rescaling (only when the running max grows by > 2^8), P_j written to smem
 //               (bf16, SWIZZLE_128B K-major) for the PV MMA; finally O / l -> bf16, stored
 //               straight into the output-exchange destination slab of that row.
+#include <algorithm>
+
 #include "common.hpp"
 #include "kernels.hpp"
 #include "sm100.cuh"
@@ -42,6 +44,13 @@ struct AttnParams {
     int rows_per_chunk;
     int64_t out_row_stride;
     int64_t out_batch_stride;
+    // split-KV (v2 kernel): gridDim.z CTAs per (query tile, head)
+    int splits;
+    int heads;
+    int q_tiles;
+    int* counters;   // [q_tiles][heads], zero between launches
+    float* ws_lse;   // [splits][q_tiles * 128][heads]
+    float* ws_o;     // [splits][q_tiles * 128][heads][D]
 };
 
 template <int D>
@@ -460,9 +469,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int lane = threadIdx.x % 32;
     const int q_tile = blockIdx.x;
     const int head = blockIdx.y;
-    const int n_total = p.total_tiles;
+    const int split = blockIdx.z;
+    // this CTA's share [tb, tb + n_total) of the kv tiles, halved between the warpgroups
+    const int tb = static_cast<int>((static_cast<int64_t>(split) * p.total_tiles) / p.splits);
+    const int n_total =
+        static_cast<int>((static_cast<int64_t>(split + 1) * p.total_tiles) / p.splits) - tb;
     const int n0 = (n_total + 1) / 2;
     const int n1 = n_total - n0;
+    __shared__ int s_last;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_q);
@@ -501,7 +515,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 mbar_wait(&slot_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
                 int row, valid;
-                kv_tile_coords(p, g, row, valid);
+                kv_tile_coords(p, tb + g, row, valid);
                 uint8_t* dst = ring + slot * L::kTileBytes;
 #pragma unroll
                 for (int c = 0; c < (int)L::kChunks; ++c)
@@ -582,7 +596,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const uint32_t t_s = tmem_base + i * 128 + lane_off;
         const uint32_t t_o = tmem_base + 256 + i * 128 + lane_off;
         const int n = i == 0 ? n0 : n1;
-        const int g0 = i == 0 ? 0 : n0;
+        const int g0 = tb + (i == 0 ? 0 : n0);
         const float scale = p.scale_log2;
         float m_run = -INFINITY;
         float l_run = 0.0f;
@@ -689,24 +703,98 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         const uint32_t t_o0 = tmem_base + 256 + lane_off;
         const uint32_t t_o1 = tmem_base + 384 + lane_off;
+        if (p.splits == 1) {
 #pragma unroll 1
-        for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
-            uint32_t o0[32], o1[32];
-            tmem_ld32(t_o0 + c * 32, o0);
-            if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
-            tmem_ld_wait();
-            if (dst) {
-                float f[32];
+            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+                uint32_t o0[32], o1[32];
+                tmem_ld32(t_o0 + c * 32, o0);
+                if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
+                tmem_ld_wait();
+                if (dst) {
+                    float f[32];
 #pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    f[e] = __uint_as_float(o0[e]) * w0 + (n1 > 0 ? __uint_as_float(o1[e]) * w1 : 0.0f);
-                uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+                    for (int e = 0; e < 32; ++e)
+                        f[e] = __uint_as_float(o0[e]) * w0 +
+                               (n1 > 0 ? __uint_as_float(o1[e]) * w1 : 0.0f);
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    d4[v] = make_uint4(pack_bf16x2(f[8 * v + 0], f[8 * v + 1]),
-                                       pack_bf16x2(f[8 * v + 2], f[8 * v + 3]),
-                                       pack_bf16x2(f[8 * v + 4], f[8 * v + 5]),
-                                       pack_bf16x2(f[8 * v + 6], f[8 * v + 7]));
+                    for (int v = 0; v < 4; ++v)
+                        d4[v] = make_uint4(pack_bf16x2(f[8 * v + 0], f[8 * v + 1]),
+                                           pack_bf16x2(f[8 * v + 2], f[8 * v + 3]),
+                                           pack_bf16x2(f[8 * v + 4], f[8 * v + 5]),
+                                           pack_bf16x2(f[8 * v + 6], f[8 * v + 7]));
+                }
+            }
+        } else {
+            // ---- split-KV: normalised fp32 partial + lse to the workspace ----
+            const int64_t prow = static_cast<int64_t>(q_tile) * kBQ + r;
+            const int64_t rows_all = static_cast<int64_t>(p.q_tiles) * kBQ;
+            float* wo = p.ws_o + ((split * rows_all + prow) * p.heads + head) * D;
+#pragma unroll 1
+            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+                uint32_t o0[32], o1[32];
+                tmem_ld32(t_o0 + c * 32, o0);
+                if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
+                tmem_ld_wait();
+                float4* w4 = reinterpret_cast<float4*>(wo + c * 32);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    float f[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        f[e] = __uint_as_float(o0[4 * v + e]) * w0 +
+                               (n1 > 0 ? __uint_as_float(o1[4 * v + e]) * w1 : 0.0f);
+                    __stcg(w4 + v, make_float4(f[0], f[1], f[2], f[3]));
+                }
+            }
+            if (i == 0)
+                __stcg(p.ws_lse + (split * rows_all + prow) * p.heads + head,
+                       mm + __log2f(l0 * a0 + l1 * a1));
+            __threadfence();
+            named_bar_sync(1, 256);
+            if (threadIdx.x == 128) {
+                int* ctr = p.counters + q_tile * p.heads + head;
+                const int prev = atomicAdd(ctr, 1);
+                s_last = prev == p.splits - 1;
+                if (s_last) *ctr = 0;  // every split has arrived: re-arm for the next launch
+            }
+            named_bar_sync(1, 256);
+            if (s_last) {
+                __threadfence();
+                // merge: row r, head-dim half i, over all splits (lse-weighted)
+                float lse_max = -INFINITY;
+                for (int z = 0; z < p.splits; ++z)
+                    lse_max = fmaxf(lse_max,
+                                    __ldcg(p.ws_lse + (z * rows_all + prow) * p.heads + head));
+                float wsum = 0.0f;
+                float acc[D / 2];
+#pragma unroll
+                for (int e = 0; e < D / 2; ++e) acc[e] = 0.0f;
+                for (int z = 0; z < p.splits; ++z) {
+                    const float wz = ex2_approx(
+                        __ldcg(p.ws_lse + (z * rows_all + prow) * p.heads + head) - lse_max);
+                    wsum += wz;
+                    const float4* src = reinterpret_cast<const float4*>(
+                        p.ws_o + ((z * rows_all + prow) * p.heads + head) * D + i * (D / 2));
+#pragma unroll
+                    for (int v = 0; v < D / 8; ++v) {
+                        const float4 t = __ldcg(src + v);
+                        acc[4 * v + 0] = fmaf(wz, t.x, acc[4 * v + 0]);
+                        acc[4 * v + 1] = fmaf(wz, t.y, acc[4 * v + 1]);
+                        acc[4 * v + 2] = fmaf(wz, t.z, acc[4 * v + 2]);
+                        acc[4 * v + 3] = fmaf(wz, t.w, acc[4 * v + 3]);
+                    }
+                }
+                if (dst) {
+                    const float inv_w = 1.0f / wsum;
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + i * (D / 2));
+#pragma unroll
+                    for (int v = 0; v < D / 16; ++v)
+                        d4[v] = make_uint4(pack_bf16x2(acc[8 * v + 0] * inv_w, acc[8 * v + 1] * inv_w),
+                                           pack_bf16x2(acc[8 * v + 2] * inv_w, acc[8 * v + 3] * inv_w),
+                                           pack_bf16x2(acc[8 * v + 4] * inv_w, acc[8 * v + 5] * inv_w),
+                                           pack_bf16x2(acc[8 * v + 6] * inv_w, acc[8 * v + 7] * inv_w));
+                }
             }
         }
     }
@@ -746,7 +834,30 @@ void attn_set_attr() {
 
 }  // namespace
 
-void attn_plan(AttnPlan* plan, const AttnOperands& ops) {
+int attn_max_splits(const AttnOperands& ops, int sm_count) {
+    static const int forced = [] {  // tuning override: SPX_ATTN_SPLITS=<1..8>
+        const char* e = std::getenv("SPX_ATTN_SPLITS");
+        return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
+    }();
+    if (forced) return forced;
+    // Split only while the doubled grid still fits in one wave: the partials cost a
+    // fp32 round trip through L2 and a merge, which only pays when SMs would idle
+    // (measured: 1170x4680x3 s=2 0.043 ms vs s=1 0.047; 4680x4680x12 s=2 0.209 vs 0.127).
+    const int64_t n = ceil_div(static_cast<int64_t>(ops.sq), kBQ) * ops.heads * ops.batch;
+    int best = 1;
+    while (best < 8 && n * 2 * best <= sm_count) best *= 2;
+    return best;
+}
+
+size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits) {
+    if (max_splits <= 1) return 0;
+    const size_t rows = static_cast<size_t>(ceil_div(static_cast<int64_t>(ops.sq), kBQ)) * kBQ;
+    const size_t ctr = (rows / kBQ * ops.heads * sizeof(int) + 255) / 256 * 256;
+    const size_t lse = (max_splits * rows * ops.heads * sizeof(float) + 255) / 256 * 256;
+    return ctr + lse + max_splits * rows * ops.heads * ops.head_dim * sizeof(float);
+}
+
+void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count) {
     require(ops.head_dim == 64 || ops.head_dim == 128, SPX_ERR_UNSUPPORTED,
             "attention: head_dim must be 64 or 128 (got " + std::to_string(ops.head_dim) + ")");
     require(ops.batch == 1, SPX_ERR_UNSUPPORTED, "attention kernel: batch must be 1");
@@ -777,6 +888,10 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops) {
                 SPX_ERR_ALIGNMENT, err);
     }
     attn_set_segments(plan, ops.seg_start, ops.seg_len, ops.num_segs);
+    plan->max_splits = ops.batch == 1 ? attn_max_splits(ops, sm_count) : 1;
+    if (plan->max_splits > 1 &&
+        (ops.workspace == nullptr || ops.workspace_bytes < attn_workspace_bytes(ops, plan->max_splits)))
+        plan->max_splits = 1;  // no (or too small a) workspace: one CTA per tile
 }
 
 void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs) {
@@ -809,6 +924,19 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     p.rows_per_chunk = o.rows_per_chunk;
     p.out_row_stride = o.out_row_stride;
     p.out_batch_stride = o.out_batch_stride;
+    // kv splits: as planned, but every CTA keeps >= 2 kv tiles (one per softmax warpgroup)
+    p.splits = std::max(1, std::min(plan.max_splits, p.total_tiles / 2));
+    p.heads = o.heads;
+    p.q_tiles = static_cast<int>(ceil_div(o.sq, kBQ));
+    if (p.splits > 1) {
+        const size_t rows = static_cast<size_t>(p.q_tiles) * kBQ;
+        uint8_t* ws = static_cast<uint8_t*>(o.workspace);
+        const size_t ctr = (rows / kBQ * o.heads * sizeof(int) + 255) / 256 * 256;
+        const size_t lse = (plan.max_splits * rows * o.heads * sizeof(float) + 255) / 256 * 256;
+        p.counters = reinterpret_cast<int*>(ws);
+        p.ws_lse = reinterpret_cast<float*>(ws + ctr);
+        p.ws_o = reinterpret_cast<float*>(ws + ctr + lse);
+    }
     dim3 grid(static_cast<unsigned>(ceil_div(o.sq, kBQ)), static_cast<unsigned>(o.heads),
               static_cast<unsigned>(o.batch));
     static const bool use_v1 = [] {
@@ -826,10 +954,12 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 plan.map_q, plan.map_k, plan.map_v, p);
         }
     } else if (o.head_dim == 128) {
+        grid.z = static_cast<unsigned>(p.splits);
         attn_v2_set_attr<128>();
         attn_fwd_v2_kernel<128><<<grid, kThreadsV2, SmemV2<128>::kBytes, stream>>>(
             plan.map_q, plan.map_k, plan.map_v, p);
     } else {
+        grid.z = static_cast<unsigned>(p.splits);
         attn_v2_set_attr<64>();
         attn_fwd_v2_kernel<64><<<grid, kThreadsV2, SmemV2<64>::kBytes, stream>>>(
             plan.map_q, plan.map_k, plan.map_v, p);

@@ -236,7 +236,20 @@ void Engine::build_plans() {
             a.num_segs = 1;
             a.rows_per_chunk = static_cast<int>(Lp_);
             a.out_row_stride = Hl_ * D_;
-            attn_plan(&rs.attn_plan[l], a);
+            if (l == 0) {  // one split-KV workspace per rank (layers run in stream order)
+                const size_t ws = attn_workspace_bytes(a, attn_max_splits(a, sms));
+                if (ws > 0) {
+                    void* ptr = nullptr;
+                    SPX_CUDA(cudaMalloc(&ptr, ws));
+                    SPX_CUDA(cudaMemset(ptr, 0, ws));
+                    rs.allocations.push_back(ptr);
+                    rs.attn_ws = ptr;
+                    rs.attn_ws_bytes = ws;
+                }
+            }
+            a.workspace = rs.attn_ws;
+            a.workspace_bytes = rs.attn_ws_bytes;
+            attn_plan(&rs.attn_plan[l], a, sms);
         }
     }
 }

@@ -61,6 +61,8 @@ struct RankState {
     std::vector<GemmPlan> qkv_plan;   // per layer, A = x[layer % 2]
     std::vector<GemmPlan> o_plan;     // per layer, out = x[(layer + 1) % 2]
     std::vector<AttnPlan> attn_plan;  // per layer
+    void* attn_ws = nullptr;          // split-KV workspace (shared by the layers)
+    size_t attn_ws_bytes = 0;
     cudaEvent_t ev_k3 = nullptr;
     cudaEvent_t ev_attn = nullptr;
     std::vector<void*> allocations;

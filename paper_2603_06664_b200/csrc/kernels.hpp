@@ -68,6 +68,12 @@ struct AttnOperands {
     int rows_per_chunk = 0;
     int64_t out_row_stride = 0;
     int64_t out_batch_stride = 0;
+    // split-KV workspace (zero-initialised once; see attn_workspace_bytes). When the grid of
+    // (query tiles x heads) under-fills the SMs, the kv range is split over up to
+    // max_splits CTAs per tile, each writing a normalised fp32 partial + its log-sum-exp; the
+    // last CTA of a tile to finish merges them (no extra launch).
+    void* workspace = nullptr;
+    size_t workspace_bytes = 0;
 };
 
 struct AttnPlan {
@@ -75,9 +81,14 @@ struct AttnPlan {
     CUtensorMap map_k;
     CUtensorMap map_v;
     AttnOperands ops;
+    int max_splits = 1;
 };
 
-void attn_plan(AttnPlan* plan, const AttnOperands& ops);
+// kv splits the planner uses for this (query rows, heads) shape on sm_count SMs
+int attn_max_splits(const AttnOperands& ops, int sm_count);
+// workspace bytes for that many splits (0 when max_splits == 1)
+size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits);
+void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count);
 void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs);
 void attn_run(const AttnPlan& plan, cudaStream_t stream);
 

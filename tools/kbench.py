@@ -25,44 +25,59 @@ except Exception:
     pass
 
 
+_STREAM = None
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
 def timeit(fn, iters):
+    """device time per call: `iters` calls captured in one CUDA graph (host launch cost out)"""
+    st = torch.cuda.current_stream()
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for _ in range(iters):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        fn()
-    e1.record()
+    e0.record(st)
+    g.replay()
+    e1.record(st)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters
 
 
+ATTN_SHAPES = [(4680, 4680, 12), (4680, 32760, 12), (2340, 4680, 6), (1170, 4680, 3),
+               (2340, 4680, 3), (4680, 14040, 12)]
+
+
 def attn(iters):
-    s = torch.cuda.current_stream().cuda_stream
-    for sq, skv, H in [(4680, 4680, 12), (4680, 32760, 12), (2340, 4680, 6), (1170, 4680, 3),
-                       (2340, 4680, 3), (4680, 14040, 12)]:
+    for sq, skv, H in ATTN_SHAPES:
         D = 128
         q = (torch.randn(1, sq, H, D, device="cuda") * 0.5).to(torch.bfloat16)
         k = (torch.randn(1, skv, H, D, device="cuda") * 0.5).to(torch.bfloat16)
         v = torch.randn(1, skv, H, D, device="cuda").to(torch.bfloat16)
         o = torch.empty_like(q)
         ms = timeit(lambda: check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                                      o.data_ptr(), 1, sq, skv, H, D, s)), iters)
+                                                      o.data_ptr(), 1, sq, skv, H, D, stream_handle())), iters)
         tf = 4.0 * sq * skv * H * D / (ms * 1e-3) / 1e12
         print(json.dumps({"kernel": "attention", "sq": sq, "skv": skv, "heads": H, "ms": round(ms, 4),
                           "tflops": round(tf, 1), "frac_peak": round(tf / PEAK_TF, 3)}), flush=True)
 
 
 def gemm(iters):
-    s = torch.cuda.current_stream().cuda_stream
     for M, K, N in [(4680, 1536, 4608), (4680, 1536, 1536), (2340, 1536, 4608), (1170, 1536, 4608),
                     (585, 1536, 4608), (8192, 8192, 8192)]:
         x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
         y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         ms = timeit(lambda: check(lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(),
-                                                           M, K, N, s)), iters)
+                                                           M, K, N, stream_handle())), iters)
         tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
         ref_ms = timeit(lambda: torch.matmul(x, w.t()), iters)
         print(json.dumps({"kernel": "gemm", "M": M, "K": K, "N": N, "ms": round(ms, 4),
@@ -71,7 +86,6 @@ def gemm(iters):
 
 
 def rope(iters):
-    s = torch.cuda.current_stream().cuda_stream
     tab = ctypes.c_void_p()
     split = (ctypes.c_int64 * 3)(22, 21, 21)
     check(lib().spx_rope_table_create(240, 30, 52, 128, 10000.0, split, ctypes.byref(tab)))
@@ -84,7 +98,7 @@ def rope(iters):
         for start in (0, 18):
             ms = timeit(lambda: check(lib().spx_rope_apply_causal_local(
                 tab, x.data_ptr(), y.data_ptr(), 1, Lp, H, D, grid, start, 0, P,
-                nw.data_ptr() if norm else None, 1e-6, s)), iters)
+                nw.data_ptr() if norm else None, 1e-6, stream_handle())), iters)
             gbs = 2 * x.numel() * 2 / (ms * 1e-3) / 1e9
             print(json.dumps({"kernel": "rope_single", "P": P, "norm": norm, "start": start,
                               "ms": round(ms, 5), "GBs": round(gbs, 1),
@@ -93,8 +107,13 @@ def rope(iters):
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which.startswith("attn:"):  # attn:SQxSKVxH
+        ATTN_SHAPES[:] = [tuple(int(v) for v in which[5:].split("x"))]
+        which = "attn"
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     lib()
+    _side = torch.cuda.Stream()  # graph capture needs a non-default stream
+    torch.cuda.set_stream(_side)
     if which in ("attn", "all"):
         attn(iters)
     if which in ("gemm", "all"):
