@@ -11,6 +11,8 @@
 //   warps 4..7  : epilogue, tcgen05.ld -> (gate, residual) -> bf16 -> global
 //
 // The smem ring is 4 stages of (A 16 KB + B BN*128 B), SWIZZLE_128B everywhere.
+#include <cstdlib>
+
 #include "common.hpp"
 #include "kernels.hpp"
 #include "sm100.cuh"
@@ -41,6 +43,38 @@ struct GemmParams {
 template <int BN>
 constexpr size_t gemm_smem_bytes() {
     return 1024 + static_cast<size_t>(kStages) * (kBM * kBK * 2 + BN * kBK * 2) + 256;
+}
+
+// one 32-column slice of an accumulator row -> (gate, residual) -> bf16 -> global
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0,
+                                               const uint32_t (&r)[32]) {
+    if (row >= p.M || col0 >= p.N) return;
+    float f[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+    if (p.epi_mode == 1) {
+        const uint4* res = reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint4 rv = res[q];
+            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 rr = unpack_bf16x2(rw[e]);
+                const int j = q * 8 + e * 2;
+                f[j] = rr.x + p.gate[col0 + j] * f[j];
+                f[j + 1] = rr.y + p.gate[col0 + j + 1] * f[j + 1];
+            }
+        }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(row) * p.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]),
+                            pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                            pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]),
+                            pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+    }
 }
 
 template <int BN>
@@ -155,36 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t r[32];
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
-                const int col0 = n0 + c * 32;
-                if (row < p.M && col0 < p.N) {
-                    float f[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
-                    if (p.epi_mode == 1) {
-                        const uint4* res =
-                            reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint4 rv = res[q];
-                            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                float2 rr = unpack_bf16x2(rw[e]);
-                                const int j = q * 8 + e * 2;
-                                f[j] = rr.x + p.gate[col0 + j] * f[j];
-                                f[j + 1] = rr.y + p.gate[col0 + j + 1] * f[j + 1];
-                            }
-                        }
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + row * p.ldo + col0);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]),
-                                            pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
-                                            pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]),
-                                            pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
-                    }
-                }
+                epilogue_chunk(p, row, n0 + c * 32, r);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
@@ -194,6 +199,176 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
+    }
+}
+
+// =========================================================================================
+// CTA-pair variant (cta_group::2): a 2-CTA cluster owns a 256 x BN output tile. CTA c loads
+// its own 128 rows of A and its half (BN/2 rows) of B into its own smem; the leader's single
+// MMA thread issues M=256 x N=BN x K=16 pair MMAs that read both CTAs' smem, so each SM
+// streams half the B operand it would for a 128 x BN tile (operand bytes per MMA cycle
+// halve, the L2 -> SM limit of the 1-CTA kernel). Accumulators: 128 lanes x BN columns in
+// each CTA's TMEM, double-buffered; each CTA's epilogue drains its own rows.
+//   full[s]   leader only, 1 arrival + 2 x stage bytes (both CTAs' TMA count on it)
+//   empty[s]  both CTAs, released by the leader's multicast commit
+//   tfull[a]  both CTAs, multicast commit after the tile's last k-block
+//   tempty[a] leader only, 2 x 128 epilogue arrivals (the peer's arrive remotely)
+// =========================================================================================
+constexpr int kPairStages = 6;
+
+template <int BN>
+constexpr size_t gemm_pair_smem_bytes() {
+    return 1024 + static_cast<size_t>(kPairStages) * (128 * kBK * 2 + (BN / 2) * kBK * 2) + 256;
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                             const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    constexpr uint32_t kABytes = 128 * kBK * 2;
+    constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
+    constexpr uint32_t kTmemCols = 2 * BN;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kPairStages * kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kPairStages * kBBytes);
+    uint64_t* empty = full + kPairStages;
+    uint64_t* tfull = empty + kPairStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int cta = static_cast<int>(cluster_ctarank());
+    const bool leader = cta == 0;
+    const int pair = blockIdx.x / 2;
+    const int npairs = gridDim.x / 2;
+    const int num_tiles = p.num_m_tiles * p.num_n_tiles;  // m tiles of 256 rows
+    const int num_kt = p.K / kBK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_a);
+        tma_prefetch_desc(&map_b);
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int m0 = (tile % p.num_m_tiles) * 256 + cta * 128;
+                const int n0 = (tile / p.num_m_tiles) * BN + cta * (BN / 2);
+                for (int kt = 0; kt < num_kt; ++kt) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kABytes + kBBytes));
+                    const int k0 = kt * kBK;
+                    tma_load_3d_pair(sA + stage * kABytes, &map_a, &full[stage], k0 % p.k_inner, m0,
+                                     k0 / p.k_inner);
+                    tma_load_2d_pair(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
+                    if (++stage == kPairStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            // drain: every multicast release of this CTA's stages has landed before exit
+            for (int s = 0; s < kPairStages; ++s) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (++stage == kPairStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = make_idesc_bf16(256, BN, false, false);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kt = 0; kt < num_kt; ++kt) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * kABytes);
+                    const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        umma_bf16_ss_pair(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
+                                          make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                                          (kt | k) != 0);
+                    }
+                    umma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == kPairStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_pair(&tfull[acc], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4;
+        int it = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            const int m0 = (tile % p.num_m_tiles) * 256 + cta * 128;
+            const int n0 = (tile / p.num_m_tiles) * BN;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int row = m0 + ew * 32 + lane;
+            const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(t_row + c * 32, r);
+                tmem_ld_wait();
+                epilogue_chunk(p, row, n0 + c * 32, r);
+            }
+            tc_fence_before();
+            mbar_arrive_leader(&tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair<kTmemCols>(tmem_base);
+    }
+}
+
+template <int BN>
+void set_pair_smem_attr() {
+    static bool done[64] = {};
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 63]) {
+        SPX_CUDA(cudaFuncSetAttribute(gemm_bf16_tn_pair_kernel<BN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(gemm_pair_smem_bytes<BN>())));
+        done[dev & 63] = true;
     }
 }
 
@@ -221,34 +396,57 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
     require((reinterpret_cast<uintptr_t>(ops.out) & 15) == 0 && ops.out_row_stride % 8 == 0,
             SPX_ERR_ALIGNMENT, "gemm: output must be 16-byte aligned");
     plan->ops = ops;
-    // BN: 256 unless 128 gives a better wave quantisation over the SMs
-    const int64_t mt = ceil_div(ops.M, kBM);
-    auto waste = [&](int bn) {
-        const int64_t tiles = mt * ceil_div(ops.N, bn);
-        const int64_t waves = ceil_div(tiles, sm_count);
-        return static_cast<double>(waves * sm_count * bn) / static_cast<double>(tiles * bn) *
-               (ops.N % bn == 0 ? 1.0 : 1.0 + static_cast<double>(bn - ops.N % bn) / ops.N);
-    };
-    plan->bn = (ops.N % 256 == 0 && waste(256) <= waste(128) * 1.05) ? 256 : 128;
+    // Variant: modelled time = waves x per-SM tile work / efficiency, over
+    //   pair (cta_group::2) 256 x {256, 128} tiles and single-CTA 128 x {256, 128} tiles.
+    // The single-CTA kernels stream 1.5-2x the operand bytes per MMA cycle (L2 -> SM bound).
+    struct Cand { bool pair; int bn; double eff; };
+    // efficiencies measured on B200 (tools/kbench.py gemm, K = 1536): pair-256 1358 TFLOP/s
+    // at 4680x4608, pair-128 908, single-256 1237, single-128 1077
+    static const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.65}, {false, 256, 0.88},
+                                 {false, 128, 0.72}};
+    static const int forced = [] {  // tuning override: SPX_GEMM_VARIANT=0..3 (index above)
+        const char* e = std::getenv("SPX_GEMM_VARIANT");
+        return e ? std::atoi(e) : -1;
+    }();
+    double best = 1e30;
+    for (int ci = 0; ci < 4; ++ci) {
+        const Cand& c = cands[ci];
+        if (ops.N % 32 != 0) continue;
+        const int64_t bm = c.pair ? 256 : 128;
+        const int64_t tiles = ceil_div(static_cast<int64_t>(ops.M), bm) * ceil_div(ops.N, c.bn);
+        const int64_t slots = c.pair ? sm_count / 2 : sm_count;
+        const double t = static_cast<double>(ceil_div(tiles, slots)) * 128.0 * c.bn / c.eff;
+        if ((forced < 0 && t < best) || forced == ci) {
+            best = forced == ci ? -1.0 : t;
+            plan->pair = c.pair;
+            plan->bn = c.bn;
+        }
+    }
+    const int bm = plan->pair ? 256 : 128;
     char err[256];
     {
         const uint64_t dims[3] = {static_cast<uint64_t>(ops.k_inner), static_cast<uint64_t>(ops.M),
                                   static_cast<uint64_t>(ops.groups)};
         const uint64_t strides[2] = {static_cast<uint64_t>(ops.a_row_stride) * 2,
                                      static_cast<uint64_t>(ops.a_group_stride) * 2};
-        const uint32_t box[3] = {kBK, kBM, 1};
+        const uint32_t box[3] = {kBK, 128, 1};
         require(make_tma_map_bf16(&plan->map_a, ops.a, 3, dims, strides, box, err, sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
     }
     {
         const uint64_t dims[2] = {static_cast<uint64_t>(ops.K), static_cast<uint64_t>(ops.N)};
         const uint64_t strides[1] = {static_cast<uint64_t>(ops.b_row_stride) * 2};
-        const uint32_t box[2] = {kBK, static_cast<uint32_t>(plan->bn)};
+        const uint32_t box[2] = {kBK, static_cast<uint32_t>(plan->pair ? plan->bn / 2 : plan->bn)};
         require(make_tma_map_bf16(&plan->map_b, ops.b, 2, dims, strides, box, err, sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
     }
-    const int64_t tiles = mt * ceil_div(ops.N, plan->bn);
-    plan->grid = static_cast<int>(tiles < sm_count ? tiles : sm_count);
+    const int64_t tiles = ceil_div(static_cast<int64_t>(ops.M), bm) * ceil_div(ops.N, plan->bn);
+    if (plan->pair) {
+        const int64_t pairs = sm_count / 2;
+        plan->grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+    } else {
+        plan->grid = static_cast<int>(tiles < sm_count ? tiles : sm_count);
+    }
 }
 
 void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
@@ -258,7 +456,7 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
     p.N = o.N;
     p.K = o.K;
     p.k_inner = o.k_inner;
-    p.num_m_tiles = static_cast<int>(ceil_div(o.M, kBM));
+    p.num_m_tiles = static_cast<int>(ceil_div(o.M, plan.pair ? 256 : kBM));
     p.num_n_tiles = static_cast<int>(ceil_div(o.N, plan.bn));
     p.out = o.out;
     p.ldo = o.out_row_stride;
@@ -266,7 +464,15 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
     p.residual = o.residual;
     p.ldr = o.residual_row_stride;
     p.gate = o.gate;
-    if (plan.bn == 256) {
+    if (plan.pair && plan.bn == 256) {
+        set_pair_smem_attr<256>();
+        gemm_bf16_tn_pair_kernel<256><<<plan.grid, kThreads, gemm_pair_smem_bytes<256>(), stream>>>(
+            plan.map_a, plan.map_b, p);
+    } else if (plan.pair) {
+        set_pair_smem_attr<128>();
+        gemm_bf16_tn_pair_kernel<128><<<plan.grid, kThreads, gemm_pair_smem_bytes<128>(), stream>>>(
+            plan.map_a, plan.map_b, p);
+    } else if (plan.bn == 256) {
         set_smem_attr<256>();
         gemm_bf16_tn_kernel<256><<<plan.grid, kThreads, gemm_smem_bytes<256>(), stream>>>(
             plan.map_a, plan.map_b, p);

@@ -39,6 +39,7 @@ struct GemmPlan {
     CUtensorMap map_b;
     GemmOperands ops;
     int bn = 256;
+    bool pair = false;  // cta_group::2 CTA-pair kernel (256-row tiles)
     int grid = 0;
 };
 
