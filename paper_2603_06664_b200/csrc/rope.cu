@@ -34,8 +34,7 @@ __device__ __forceinline__ void rope_position(int64_t i_local, int64_t row_offse
     w = ig % grid_w;
 }
 
-__device__ __forceinline__ float2 band_cs(const RopeLaunch& l, int j, int64_t t, int64_t h,
-                                          int64_t w) {
+__device__ __forceinline__ float2 band_cs(const RopeLaunch& l, int j, int t, int h, int w) {
     if (j < l.pairs[0]) return __ldg(&l.tab[0][t * l.pairs[0] + j]);
     j -= l.pairs[0];
     if (j < l.pairs[1]) return __ldg(&l.tab[1][h * l.pairs[1] + j]);
@@ -69,72 +68,91 @@ __device__ __forceinline__ uint4 rotate_vec(uint4 x, const float2 (&cs)[4], floa
     return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
+// NV = 16-byte vectors per lane per tensor (C / 256, rounded up). Every load of the row
+// (q, k and v: 3 NV vectors per lane) is issued before any math, so each warp keeps
+// 3 x NV x 512 B in flight; the position math is 32-bit.
+template <int NV>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     rope_norm_pack_kernel(const RopeLaunch l) {
     const int lane = threadIdx.x % 32;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + threadIdx.x / 32;
+    const int row = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
     if (row >= l.rows) return;
     const int C = l.heads * l.head_dim;
     const int nvec = C / 8;
     const int hpg = l.heads / l.groups;
-    const int64_t i_local = row % l.rows_per_batch;
-    int64_t t, h, w;
-    rope_position(i_local, l.row_offset, l.hw, l.grid_w, l.start_frame, t, h, w);
+    const uint4* src = reinterpret_cast<const uint4*>(l.in + static_cast<int64_t>(row) * l.in_row_stride);
 
-    // this lane's four pairs (identical for all of its vectors because D | 256)
+    uint4 xq[NV], xk[NV], xv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int v = lane + 32 * i;
+        if (v < nvec) {
+            xq[i] = __ldg(src + v);
+            if (l.has_kv) {
+                xk[i] = __ldg(src + nvec + v);
+                xv[i] = __ldg(src + 2 * nvec + v);
+            }
+        }
+    }
+
+    // (t, h, w) of this row (rope.cpp:97-101), 32-bit
+    const int i_local = row % static_cast<int>(l.rows_per_batch);
+    const int ig = static_cast<int>(l.row_offset) + i_local;
+    const int hw = static_cast<int>(l.hw), gw = static_cast<int>(l.grid_w);
+    const int tq = ig / hw;
+    const int t = static_cast<int>(l.start_frame) + tq;
+    const int rem = ig - tq * hw;
+    const int h = rem / gw;
+    const int w = rem - h * gw;
+    // this lane's four rotation pairs (identical for all of its vectors because D | 256)
     const int e0 = (8 * lane) % l.head_dim;
     float2 cs[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) cs[e] = band_cs(l, e0 / 2 + e, t, h, w);
 
-    const uint4* src = reinterpret_cast<const uint4*>(l.in + row * l.in_row_stride);
-    const int ntensor = l.has_kv ? 3 : 1;
-#pragma unroll 1
-    for (int which = 0; which < ntensor; ++which) {
-        const uint4* s = src + which * nvec;
-        uint4 x[kMaxVecPerLane];
-        float ss = 0.0f;
+    float scale_q = 1.0f, scale_k = 1.0f;
+    if (l.norm) {  // QK-RMSNorm over the C channels (Wan mode; no reference counterpart)
+        float sq = 0.0f, sk = 0.0f;
 #pragma unroll
-        for (int i = 0; i < kMaxVecPerLane; ++i) {
-            const int v = lane + 32 * i;
-            if (v < nvec) {
-                x[i] = s[v];
-                if (l.norm && which < 2) {
-                    const uint32_t q[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+        for (int i = 0; i < NV; ++i) {
+            if (lane + 32 * i < nvec) {
+                const uint32_t a[4] = {xq[i].x, xq[i].y, xq[i].z, xq[i].w};
+                const uint32_t b[4] = {xk[i].x, xk[i].y, xk[i].z, xk[i].w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = unpack_bf16x2(q[e]);
-                        ss += f.x * f.x + f.y * f.y;
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    const float2 fa = unpack_bf16x2(a[e]);
+                    const float2 fb = unpack_bf16x2(b[e]);
+                    sq = fmaf(fa.x, fa.x, fmaf(fa.y, fa.y, sq));
+                    sk = fmaf(fb.x, fb.x, fmaf(fb.y, fb.y, sk));
                 }
             }
         }
-        float scale = 1.0f;
-        const uint4* nw_base = nullptr;
-        if (l.norm && which < 2) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            scale = rsqrtf(ss / static_cast<float>(C) + l.norm_eps);
-            nw_base = reinterpret_cast<const uint4*>(which == 0 ? l.norm_w_q : l.norm_w_k);
+        for (int o = 16; o > 0; o >>= 1) {
+            sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            sk += __shfl_xor_sync(0xffffffffu, sk, o);
         }
+        scale_q = rsqrtf(sq / static_cast<float>(C) + l.norm_eps);
+        scale_k = rsqrtf(sk / static_cast<float>(C) + l.norm_eps);
+    }
+    const uint4* nwq = l.norm ? reinterpret_cast<const uint4*>(l.norm_w_q) : nullptr;
+    const uint4* nwk = l.norm ? reinterpret_cast<const uint4*>(l.norm_w_k) : nullptr;
+
 #pragma unroll
-        for (int i = 0; i < kMaxVecPerLane; ++i) {
-            const int v = lane + 32 * i;
-            if (v >= nvec) continue;
-            const int head = (8 * v) / l.head_dim;
-            const int g = head / hpg;
-            const int64_t off = row * l.dst_row_stride + (head - g * hpg) * l.head_dim + e0;
-            if (which == 2) {
-                for (int c = 0; c < l.dst.copies; ++c)
-                    *reinterpret_cast<uint4*>(l.dst.v[g][c] + off) = x[i];
-            } else {
-                const uint4 y = rotate_vec(x[i], cs, scale, nw_base ? nw_base + v : nullptr);
-                if (which == 0) {
-                    *reinterpret_cast<uint4*>(l.dst.q[g] + off) = y;
-                } else {
-                    for (int c = 0; c < l.dst.copies; ++c)
-                        *reinterpret_cast<uint4*>(l.dst.k[g][c] + off) = y;
-                }
+    for (int i = 0; i < NV; ++i) {
+        const int v = lane + 32 * i;
+        if (v >= nvec) continue;
+        const int head = (8 * v) / l.head_dim;
+        const int g = head / hpg;
+        const int64_t off = static_cast<int64_t>(row) * l.dst_row_stride +
+                            (head - g * hpg) * l.head_dim + e0;
+        *reinterpret_cast<uint4*>(l.dst.q[g] + off) =
+            rotate_vec(xq[i], cs, scale_q, nwq ? nwq + v : nullptr);
+        if (l.has_kv) {
+            const uint4 yk = rotate_vec(xk[i], cs, scale_k, nwk ? nwk + v : nullptr);
+            for (int c = 0; c < l.dst.copies; ++c) {
+                *reinterpret_cast<uint4*>(l.dst.k[g][c] + off) = yk;
+                *reinterpret_cast<uint4*>(l.dst.v[g][c] + off) = xv[i];
             }
         }
     }
@@ -164,8 +182,19 @@ void rope_run(const RopeLaunch& l, cudaStream_t stream) {
             "rope kernel: heads must split into <= 8 groups");
     require(l.dst.copies >= 1 && l.dst.copies <= 8, SPX_ERR_CONFIG, "rope kernel: 1-8 kv copies");
     if (l.rows == 0) return;
+    require(l.rows < (int64_t(1) << 31) && l.row_offset + l.rows_per_batch < (int64_t(1) << 31),
+            SPX_ERR_RANGE, "rope kernel: row indices must fit in 32 bits");
     const unsigned blocks = static_cast<unsigned>(ceil_div(l.rows, kWarpsPerBlock));
-    rope_norm_pack_kernel<<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l);
+    switch ((C / 8 + 31) / 32) {
+        case 1: rope_norm_pack_kernel<1><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 2: rope_norm_pack_kernel<2><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 3: rope_norm_pack_kernel<3><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 4: rope_norm_pack_kernel<4><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 5: rope_norm_pack_kernel<5><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 6: rope_norm_pack_kernel<6><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        case 7: rope_norm_pack_kernel<7><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+        default: rope_norm_pack_kernel<8><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
+    }
     SPX_CUDA_LAUNCH();
     count_launch();
 }
