@@ -51,6 +51,7 @@ struct AttnParams {
     int* counters;   // [q_tiles][heads], zero between launches
     float* ws_lse;   // [splits][q_tiles * 128][heads]
     float* ws_o;     // [splits][q_tiles * 128][heads][D]
+    int experiment;  // profiling only (SPX_ATTN_EXPERIMENT): 1 skip softmax math, 2 no MUFU
 };
 
 template <int D>
@@ -334,11 +335,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kThreadsV2 = 384;
 constexpr int kSlotsV2 = 5;
 
-template <int D>
+template <int D, bool kPair = false>
 struct SmemV2 {
     static constexpr uint32_t kChunks = D / 64;
-    static constexpr uint32_t kTileBytes = kBKV * D * 2;
-    static constexpr uint32_t kSlots = D == 128 ? kSlotsV2 : 2 * kSlotsV2;
+    // pair: each CTA holds half of every K tile (64 kv rows x D) and half of every V tile
+    // (128 kv rows x D/2), so a ring slot is half as large and the ring twice as deep
+    static constexpr uint32_t kTileBytes = kPair ? kBKV * D : kBKV * D * 2;
+    static constexpr uint32_t kSlots = (D == 128 ? kSlotsV2 : 2 * kSlotsV2) * (kPair ? 2 : 1);
     static constexpr uint32_t kOffQ = 0;
     static constexpr uint32_t kOffRing = kOffQ + kBQ * D * 2;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
@@ -442,12 +445,21 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
         __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int D>
+// kPair (D = 128 only; opt-in, see attn_run): a 2-CTA cluster = two adjacent query tiles of one head. The leader's
+// MMA thread issues M = 256 pair MMAs: S = Q K^T with each CTA supplying its own 128 query
+// rows and half of the K tile's 128 kv rows; O += P V with P read from each CTA's TMEM and
+// each CTA supplying half of V's head-dim columns. Per SM the K/V fill traffic and the SMEM
+// operand reads of the MMAs halve. Barriers that collect both CTAs (q_full, slot_full,
+// p_full) live in the leader; commits multicast to both CTAs.
+template <int D, bool kPair>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    using L = SmemV2<D>;
+    using L = SmemV2<D, kPair>;
+    static_assert(!kPair || D == 128, "pair attention is D = 128 only");
+    const int cta = kPair ? static_cast<int>(cluster_ctarank()) : 0;
+    const bool leader = cta == 0;
     constexpr uint32_t kSlots = L::kSlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -489,14 +501,22 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 128);
+            mbar_init(&p_full[i], kPair ? 256 : 128);
             mbar_init(&pv_done[i], 1);
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    if (warp == 2) {
+        if constexpr (kPair)
+            tmem_alloc_pair<512>(tmem_slot);
+        else
+            tmem_alloc<512>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair)
+        cluster_sync_all();
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -504,23 +524,39 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         setmaxnreg_dec56();
         if (warp == 0 && lane == 0) {
             // ---------------- TMA producer: the MMA consumption order ----------------
-            mbar_arrive_expect_tx(q_full, kBQ * D * 2);
+            if (leader) mbar_arrive_expect_tx(q_full, (kPair ? 2 : 1) * kBQ * D * 2);
 #pragma unroll
-            for (int c = 0; c < (int)L::kChunks; ++c)
-                tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
+            for (int c = 0; c < (int)L::kChunks; ++c) {
+                if constexpr (kPair)
+                    tma_load_3d_pair(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head,
+                                     q_tile * kBQ);
+                else
+                    tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
+            }
             uint32_t t = 0;
             auto load = [&](bool is_v, int g) {
                 const uint32_t slot = t % kSlots;
                 const uint32_t ph = (t / kSlots) & 1;
                 mbar_wait(&slot_empty[slot], ph ^ 1);
-                mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
+                if (leader)
+                    mbar_arrive_expect_tx(&slot_full[slot], (kPair ? 2 : 1) * L::kTileBytes);
                 int row, valid;
                 kv_tile_coords(p, tb + g, row, valid);
                 uint8_t* dst = ring + slot * L::kTileBytes;
+                if constexpr (kPair) {
+                    if (is_v)  // V half: all 128 kv rows, head-dim columns [64 cta, 64 cta + 64)
+                        tma_load_3d_pair(dst, &map_v, &slot_full[slot], cta * 64, head, row);
+                    else       // K half: kv rows [64 cta, 64 cta + 64), all head-dim columns
 #pragma unroll
-                for (int c = 0; c < (int)L::kChunks; ++c)
-                    tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
-                                c * 64, head, row);
+                        for (int c = 0; c < 2; ++c)
+                            tma_load_3d_pair(dst + c * (64 * 128), &map_k, &slot_full[slot],
+                                             c * 64, head, row + cta * 64);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < (int)L::kChunks; ++c)
+                        tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k,
+                                    &slot_full[slot], c * 64, head, row);
+                }
                 ++t;
             };
             load(false, 0);
@@ -533,10 +569,22 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     if (j + 1 < n1) load(false, n0 + j + 1);
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+            if constexpr (kPair) {  // drain: the leader's multicast releases have all landed
+                for (uint32_t k = 0; k < kSlots; ++k, ++t)
+                    mbar_wait(&slot_empty[t % kSlots], ((t / kSlots) & 1) ^ 1);
+            }
+        } else if (warp == 1 && lane == 0 && leader) {
             // ---------------- MMA issuer ----------------
-            constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
-            constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
+            constexpr uint32_t kM = kPair ? 2 * kBQ : kBQ;
+            constexpr uint32_t idesc_s = make_idesc_bf16(kM, kBKV, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(kM, D, false, true);
+            constexpr uint32_t kKChunk = kPair ? 64 * 128 : kBKV * 128;  // K chunk stride
+            auto commit = [&](uint64_t* bar) {
+                if constexpr (kPair)
+                    umma_commit_pair(bar, 0x3);
+                else
+                    umma_commit(bar);
+            };
             const uint32_t q_addr = smem_u32(sQ);
             const uint32_t ring_addr = smem_u32(ring);
             uint32_t t = 0;
@@ -552,26 +600,40 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
-                                 make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                    const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                    const uint32_t koff = (kk >> 2) * kKChunk + (kk & 3) * 32;
+                    if constexpr (kPair)
+                        umma_bf16_ss_pair(tmem_base + i * 128,
+                                          make_desc_sw128(q_addr + qoff, 16, 1024),
+                                          make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
+                    else
+                        umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + qoff, 16, 1024),
+                                     make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
                 }
-                umma_commit(&s_full[i]);
-                umma_commit(&slot_empty[slot]);
+                commit(&s_full[i]);
+                commit(&slot_empty[slot]);
             };
             auto issue_pv = [&](int i, int j) {
                 const uint32_t slot = take();
-                mbar_wait(&p_full[i], j & 1);
+                if constexpr (kPair)
+                    mbar_wait_cluster(&p_full[i], j & 1);
+                else
+                    mbar_wait(&p_full[i], j & 1);
                 tc_fence_after();
                 const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
 #pragma unroll
                 for (int kk = 0; kk < kBKV / 16; ++kk) {
-                    umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
-                                 make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                 idesc_o, (j | kk) != 0);
+                    if constexpr (kPair)
+                        umma_bf16_ts_pair(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                                          make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                          idesc_o, (j | kk) != 0);
+                    else
+                        umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                                     make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                     idesc_o, (j | kk) != 0);
                 }
-                umma_commit(&pv_done[i]);
-                umma_commit(&slot_empty[slot]);
+                commit(&pv_done[i]);
+                commit(&slot_empty[slot]);
             };
             mbar_wait(q_full, 0);
             tc_fence_after();
@@ -605,6 +667,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             kv_tile_coords(p, g0 + j, row, valid);
             mbar_wait(&s_full[i], j & 1);
             tc_fence_after();
+            if (p.experiment == 1) {  // profiling: MMA/TMA/barrier skeleton only
+                tc_fence_before();
+                if constexpr (kPair)
+                    mbar_arrive_leader(&p_full[i]);
+                else
+                    mbar_arrive(&p_full[i]);
+                continue;
+            }
             uint32_t u[kBKV];
 #pragma unroll
             for (int c = 0; c < kBKV / 32; ++c)
@@ -659,8 +729,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 if ((e & 7) >= 6) {  // 1/4 of the exponentials on the FMA pipe
                     pr = ex2_poly2(x);
                 } else {
-                    pr.x = ex2_approx(x.x);
-                    pr.y = ex2_approx(x.y);
+                    if (p.experiment == 2) {  // profiling: no MUFU
+                        pr.x = fmaf(x.x, 0.03125f, 1.0f);
+                        pr.y = fmaf(x.y, 0.03125f, 1.0f);
+                    } else {
+                        pr.x = ex2_approx(x.x);
+                        pr.y = ex2_approx(x.y);
+                    }
                 }
                 ls[e & 3] = fadd2(ls[e & 3], pr);
                 pk[e] = pack_bf16x2(pr.x, pr.y);
@@ -673,7 +748,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_s + c * 16, &pk[c * 16]);
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_full[i]);
+            if constexpr (kPair)
+                mbar_arrive_leader(&p_full[i]);
+            else
+                mbar_arrive(&p_full[i]);
         }
         if (n > 0) {
             mbar_wait(&pv_done[i], (n - 1) & 1);
@@ -799,23 +877,48 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair)
+        cluster_sync_all();
+    else
+        __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if constexpr (kPair)
+            tmem_dealloc_pair<512>(tmem_base);
+        else
+            tmem_dealloc<512>(tmem_base);
     }
 }
 
-template <int D>
-void attn_v2_set_attr() {
+template <int D, bool kPair>
+void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
     static bool done[64] = {};
     int dev = 0;
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v2_kernel<D>,
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v2_kernel<D, kPair>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(SmemV2<D>::kBytes)));
+                                      static_cast<int>(SmemV2<D, kPair>::kBytes)));
         done[dev & 63] = true;
+    }
+    if constexpr (kPair) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kThreadsV2);
+        cfg.dynamicSmemBytes = SmemV2<D, kPair>::kBytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kPair>, plan.map_q, plan.map_k_pair,
+                                    plan.map_v, p));
+    } else {
+        attn_fwd_v2_kernel<D, kPair><<<grid, kThreadsV2, SmemV2<D, kPair>::kBytes, stream>>>(
+            plan.map_q, plan.map_k, plan.map_v, p);
     }
 }
 
@@ -851,7 +954,8 @@ int attn_max_splits(const AttnOperands& ops, int sm_count) {
 
 size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits) {
     if (max_splits <= 1) return 0;
-    const size_t rows = static_cast<size_t>(ceil_div(static_cast<int64_t>(ops.sq), kBQ)) * kBQ;
+    const size_t tiles = static_cast<size_t>((ceil_div(static_cast<int64_t>(ops.sq), kBQ) + 1) & ~1);
+    const size_t rows = tiles * kBQ;  // query tiles padded to whole CTA pairs
     const size_t ctr = (rows / kBQ * ops.heads * sizeof(int) + 255) / 256 * 256;
     const size_t lse = (max_splits * rows * ops.heads * sizeof(float) + 255) / 256 * 256;
     return ctr + lse + max_splits * rows * ops.heads * ops.head_dim * sizeof(float);
@@ -883,6 +987,10 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count) {
         const uint64_t strides[2] = {static_cast<uint64_t>(ops.head_dim) * 2,
                                      static_cast<uint64_t>(ops.heads) * ops.head_dim * 2};
         require(make_tma_map_bf16(&plan->map_k, ops.k, 3, dims, strides, box, err, sizeof(err)),
+                SPX_ERR_ALIGNMENT, err);
+        const uint32_t box_half[3] = {64, 1, 64};
+        require(make_tma_map_bf16(&plan->map_k_pair, ops.k, 3, dims, strides, box_half, err,
+                                  sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
         require(make_tma_map_bf16(&plan->map_v, ops.v, 3, dims, strides, box, err, sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
@@ -920,6 +1028,11 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     p.seg_tiles0 = static_cast<int>(ceil_div(o.seg_len[0], kBKV));
     p.total_tiles = p.seg_tiles0 + static_cast<int>(ceil_div(o.seg_len[1], kBKV));
     p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(o.head_dim));
+    static const int experiment = [] {
+        const char* e = std::getenv("SPX_ATTN_EXPERIMENT");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.experiment = experiment;
     for (int i = 0; i < 8; ++i) p.out_base[i] = o.out_base[i];
     p.rows_per_chunk = o.rows_per_chunk;
     p.out_row_stride = o.out_row_stride;
@@ -927,7 +1040,7 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     // kv splits: as planned, but every CTA keeps >= 2 kv tiles (one per softmax warpgroup)
     p.splits = std::max(1, std::min(plan.max_splits, p.total_tiles / 2));
     p.heads = o.heads;
-    p.q_tiles = static_cast<int>(ceil_div(o.sq, kBQ));
+    p.q_tiles = static_cast<int>((ceil_div(o.sq, kBQ) + 1) & ~1);  // workspace stride (pairs)
     if (p.splits > 1) {
         const size_t rows = static_cast<size_t>(p.q_tiles) * kBQ;
         uint8_t* ws = static_cast<uint8_t*>(o.workspace);
@@ -943,6 +1056,14 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         const char* e = std::getenv("SPX_ATTN_KERNEL");
         return e && std::string(e) == "v1";
     }();
+    // CTA-pair variant (SPX_ATTN_KERNEL=pair, D = 128): correct, but measured slower on B200
+    // (4680x4680x12: 0.225 ms vs 0.135 ms single-CTA; the no-softmax skeleton 0.99 vs 0.68 ms
+    // at 32760 keys): every S -> P -> PV hand-off crosses SMs twice (remote p_full arrive,
+    // multicast commit) and with two S buffers in TMEM that latency is exposed.
+    static const bool use_v2 = [] {
+        const char* e = std::getenv("SPX_ATTN_KERNEL");
+        return !(e && std::string(e) == "pair");
+    }();
     if (use_v1) {
         if (o.head_dim == 128) {
             attn_set_attr<128>();
@@ -953,16 +1074,16 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             attn_fwd_kernel<64><<<grid, kThreads, AttnSmem<64>::kBytes, stream>>>(
                 plan.map_q, plan.map_k, plan.map_v, p);
         }
+    } else if (o.head_dim == 128 && !use_v2) {
+        grid.x = (grid.x + 1) & ~1u;  // whole CTA pairs; the padding tile's rows are all >= sq
+        grid.z = static_cast<unsigned>(p.splits);
+        attn_v2_launch<128, true>(grid, plan, p, stream);
     } else if (o.head_dim == 128) {
         grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_set_attr<128>();
-        attn_fwd_v2_kernel<128><<<grid, kThreadsV2, SmemV2<128>::kBytes, stream>>>(
-            plan.map_q, plan.map_k, plan.map_v, p);
+        attn_v2_launch<128, false>(grid, plan, p, stream);
     } else {
         grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_set_attr<64>();
-        attn_fwd_v2_kernel<64><<<grid, kThreadsV2, SmemV2<64>::kBytes, stream>>>(
-            plan.map_q, plan.map_k, plan.map_v, p);
+        attn_v2_launch<64, false>(grid, plan, p, stream);
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -305,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
                 const int acc = it & 1;
                 const uint32_t aphase = (it >> 1) & 1;
-                mbar_wait(&tempty[acc], aphase ^ 1);
+                mbar_wait_cluster(&tempty[acc], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {

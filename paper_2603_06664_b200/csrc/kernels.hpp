@@ -80,6 +80,7 @@ struct AttnOperands {
 struct AttnPlan {
     CUtensorMap map_q;
     CUtensorMap map_k;
+    CUtensorMap map_k_pair;  // 64-row boxes: each CTA of a pair loads half of a K tile
     CUtensorMap map_v;
     AttnOperands ops;
     int max_splits = 1;
