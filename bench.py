@@ -154,6 +154,8 @@ def main():
     ap.add_argument("--impl", default="spx", choices=["spx", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no timing line)")
+    ap.add_argument("--no-fuse-rope", action="store_true",
+                    help="standalone K3 RoPE/pack kernel instead of the QKV GEMM epilogue")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -184,7 +186,8 @@ def main():
     L, C = F * Hg * Wg, H * D
     cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(F, Hg, Wg), num_blocks=1,
                                   layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H, head_dim=D,
-                                  world_size=world_size, seed=0, profile=False)
+                                  world_size=world_size, seed=0, profile=False,
+                                  fuse_rope_epilogue=not args.no_fuse_rope)
     eng = spattn.Engine(cfg, world=world)  # seeded random-init weights (reference init, bf16)
     Lp = eng.local_len
     steps = WAN["steps"]

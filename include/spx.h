@@ -234,6 +234,8 @@ typedef struct spx_engine_config {
     int32_t qk_norm;                  /* 0 = reference semantics; 1 = Wan QK-RMSNorm */
     float norm_eps;
     int32_t profile;                  /* 1: CUDA-event stage timing on every call */
+    int32_t fuse_rope_epilogue;       /* 1 (default): Causal-RoPE + pack in the QKV GEMM
+                                         epilogue when qk_norm = 0; 0: standalone K3 kernel */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */

@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kThreadsV2 = 384;
 constexpr int kSlotsV2 = 5;
 
-template <int D, bool kPair = false>
+template <int D, int kMode = 0>
 struct SmemV2 {
+    static constexpr bool kPair = kMode == 1;
     static constexpr uint32_t kChunks = D / 64;
     // pair: each CTA holds half of every K tile (64 kv rows x D) and half of every V tile
     // (128 kv rows x D/2), so a ring slot is half as large and the ring twice as deep
@@ -451,15 +452,25 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // each CTA supplying half of V's head-dim columns. Per SM the K/V fill traffic and the SMEM
 // operand reads of the MMAs halve. Barriers that collect both CTAs (q_full, slot_full,
 // p_full) live in the leader; commits multicast to both CTAs.
-template <int D, bool kPair>
+//
+// kMode 2 (kMcast, D = 128): a 2-CTA cluster = two adjacent query tiles of one head with
+// private MMA/softmax pipelines; only the K/V stream is shared. Each CTA's producer loads
+// half of every K/V tile (64 kv rows) with .multicast::cluster into BOTH CTAs' ring slot,
+// so every K/V byte leaves L2 once per 256 query rows (the single-CTA kernel is bounded by
+// the ~11 TB/s L2 -> SM TMA stream: 1430 TFLOP/s with the softmax switched off). A slot is
+// refilled only when both CTAs' MMAs have released it (multicast commits, count 2).
+template <int D, int kMode>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    using L = SmemV2<D, kPair>;
-    static_assert(!kPair || D == 128, "pair attention is D = 128 only");
-    const int cta = kPair ? static_cast<int>(cluster_ctarank()) : 0;
-    const bool leader = cta == 0;
+    constexpr bool kPair = kMode == 1;
+    constexpr bool kMcast = kMode == 2;
+    constexpr bool kCluster = kPair || kMcast;
+    using L = SmemV2<D, kMode>;
+    static_assert(!kCluster || D == 128, "clustered attention is D = 128 only");
+    const int cta = kCluster ? static_cast<int>(cluster_ctarank()) : 0;
+    const bool leader = !kPair || cta == 0;
     constexpr uint32_t kSlots = L::kSlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -497,7 +508,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         mbar_init(q_full, 1);
         for (uint32_t s = 0; s < kSlots; ++s) {
             mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_empty[s], 1);
+            mbar_init(&slot_empty[s], kMcast ? 2 : 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
@@ -513,7 +524,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tmem_alloc<512>(tmem_slot);
     }
     tc_fence_before();
-    if constexpr (kPair)
+    if constexpr (kCluster)
         cluster_sync_all();
     else
         __syncthreads();
@@ -543,7 +554,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 int row, valid;
                 kv_tile_coords(p, tb + g, row, valid);
                 uint8_t* dst = ring + slot * L::kTileBytes;
-                if constexpr (kPair) {
+                if constexpr (kMcast) {  // my 64 kv rows of the tile -> both CTAs' slot
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        tma_load_3d_mcast(dst + c * (kBKV * 128) + cta * (64 * 128),
+                                          is_v ? &map_v : &map_k, &slot_full[slot], c * 64, head,
+                                          row + cta * 64, 0x3);
+                } else if constexpr (kPair) {
                     if (is_v)  // V half: all 128 kv rows, head-dim columns [64 cta, 64 cta + 64)
                         tma_load_3d_pair(dst, &map_v, &slot_full[slot], cta * 64, head, row);
                     else       // K half: kv rows [64 cta, 64 cta + 64), all head-dim columns
@@ -569,7 +586,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     if (j + 1 < n1) load(false, n0 + j + 1);
                 }
             }
-            if constexpr (kPair) {  // drain: the leader's multicast releases have all landed
+            if constexpr (kCluster) {  // drain: every multicast release has landed
                 for (uint32_t k = 0; k < kSlots; ++k, ++t)
                     mbar_wait(&slot_empty[t % kSlots], ((t / kSlots) & 1) ^ 1);
             }
@@ -584,6 +601,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     umma_commit_pair(bar, 0x3);
                 else
                     umma_commit(bar);
+            };
+            auto release = [&](uint64_t* bar) {  // a ring slot: both CTAs' producers refill it
+                if constexpr (kMcast)
+                    umma_commit_mcast(bar, 0x3);
+                else
+                    commit(bar);
             };
             const uint32_t q_addr = smem_u32(sQ);
             const uint32_t ring_addr = smem_u32(ring);
@@ -611,13 +634,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                      make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
                 }
                 commit(&s_full[i]);
-                commit(&slot_empty[slot]);
+                release(&slot_empty[slot]);
             };
             auto issue_pv = [&](int i, int j) {
                 const uint32_t slot = take();
                 if constexpr (kPair)
                     mbar_wait_cluster(&p_full[i], j & 1);
-                else
+                else if (p.experiment != 3)  // 3: profiling, MMA stream without softmax
                     mbar_wait(&p_full[i], j & 1);
                 tc_fence_after();
                 const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
@@ -633,7 +656,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                      idesc_o, (j | kk) != 0);
                 }
                 commit(&pv_done[i]);
-                commit(&slot_empty[slot]);
+                release(&slot_empty[slot]);
             };
             mbar_wait(q_full, 0);
             tc_fence_after();
@@ -662,7 +685,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const float scale = p.scale_log2;
         float m_run = -INFINITY;
         float l_run = 0.0f;
-        for (int j = 0; j < n; ++j) {
+        for (int j = 0; j < (p.experiment == 3 ? 0 : n); ++j) {
             int row, valid;
             kv_tile_coords(p, g0 + j, row, valid);
             mbar_wait(&s_full[i], j & 1);
@@ -877,7 +900,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
     }
     tc_fence_before();
-    if constexpr (kPair)
+    if constexpr (kCluster)
         cluster_sync_all();
     else
         __syncthreads();
@@ -890,22 +913,22 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
 }
 
-template <int D, bool kPair>
+template <int D, int kMode>
 void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
     static bool done[64] = {};
     int dev = 0;
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v2_kernel<D, kPair>,
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v2_kernel<D, kMode>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(SmemV2<D, kPair>::kBytes)));
+                                      static_cast<int>(SmemV2<D, kMode>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kPair) {
+    if constexpr (kMode != 0) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kThreadsV2);
-        cfg.dynamicSmemBytes = SmemV2<D, kPair>::kBytes;
+        cfg.dynamicSmemBytes = SmemV2<D, kMode>::kBytes;
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -914,10 +937,11 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kPair>, plan.map_q, plan.map_k_pair,
-                                    plan.map_v, p));
+        // pair and multicast modes both load 64-row K boxes; multicast also 64-row V boxes
+        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q,
+                                    plan.map_k_pair, kMode == 2 ? plan.map_v_half : plan.map_v, p));
     } else {
-        attn_fwd_v2_kernel<D, kPair><<<grid, kThreadsV2, SmemV2<D, kPair>::kBytes, stream>>>(
+        attn_fwd_v2_kernel<D, kMode><<<grid, kThreadsV2, SmemV2<D, kMode>::kBytes, stream>>>(
             plan.map_q, plan.map_k, plan.map_v, p);
     }
 }
@@ -994,6 +1018,9 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count) {
                 SPX_ERR_ALIGNMENT, err);
         require(make_tma_map_bf16(&plan->map_v, ops.v, 3, dims, strides, box, err, sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
+        require(make_tma_map_bf16(&plan->map_v_half, ops.v, 3, dims, strides, box_half, err,
+                                  sizeof(err)),
+                SPX_ERR_ALIGNMENT, err);
     }
     attn_set_segments(plan, ops.seg_start, ops.seg_len, ops.num_segs);
     plan->max_splits = ops.batch == 1 ? attn_max_splits(ops, sm_count) : 1;
@@ -1056,13 +1083,16 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         const char* e = std::getenv("SPX_ATTN_KERNEL");
         return e && std::string(e) == "v1";
     }();
-    // CTA-pair variant (SPX_ATTN_KERNEL=pair, D = 128): correct, but measured slower on B200
-    // (4680x4680x12: 0.225 ms vs 0.135 ms single-CTA; the no-softmax skeleton 0.99 vs 0.68 ms
-    // at 32760 keys): every S -> P -> PV hand-off crosses SMs twice (remote p_full arrive,
-    // multicast commit) and with two S buffers in TMEM that latency is exposed.
-    static const bool use_v2 = [] {
+    // D = 128 kernel: 0 single CTA (default); opt-in, both measured slower on B200:
+    //   1 CTA-pair MMAs (SPX_ATTN_KERNEL=pair): 4680x4680x12 0.225 vs 0.135 ms -- every
+    //     S -> P -> PV hand-off crosses SMs with only two S buffers to hide it;
+    //   2 K/V multicast across a CTA pair (SPX_ATTN_KERNEL=mcast): 0.182 ms, and 0.87 vs
+    //     0.66 ms for the bare MMA stream at 32760 keys -- the ring fill is not the limit.
+    static const int mode128 = [] {
         const char* e = std::getenv("SPX_ATTN_KERNEL");
-        return !(e && std::string(e) == "pair");
+        if (e && std::string(e) == "pair") return 1;
+        if (e && std::string(e) == "mcast") return 2;
+        return 0;
     }();
     if (use_v1) {
         if (o.head_dim == 128) {
@@ -1074,16 +1104,19 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             attn_fwd_kernel<64><<<grid, kThreads, AttnSmem<64>::kBytes, stream>>>(
                 plan.map_q, plan.map_k, plan.map_v, p);
         }
-    } else if (o.head_dim == 128 && !use_v2) {
+    } else if (o.head_dim == 128 && mode128 != 0) {
         grid.x = (grid.x + 1) & ~1u;  // whole CTA pairs; the padding tile's rows are all >= sq
         grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_launch<128, true>(grid, plan, p, stream);
+        if (mode128 == 1)
+            attn_v2_launch<128, 1>(grid, plan, p, stream);
+        else
+            attn_v2_launch<128, 2>(grid, plan, p, stream);
     } else if (o.head_dim == 128) {
         grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_launch<128, false>(grid, plan, p, stream);
+        attn_v2_launch<128, 0>(grid, plan, p, stream);
     } else {
         grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_launch<64, false>(grid, plan, p, stream);
+        attn_v2_launch<64, 0>(grid, plan, p, stream);
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -413,9 +413,17 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         RankState& rs = ranks_[static_cast<size_t>(li)];
         SPX_CUDA(cudaSetDevice(rs.device));
         mark(li, 0);
-        gemm_run(*qkv[static_cast<size_t>(li)], rs.stream);
-        mark(li, 1);
-        rope_run(rope_launch(rs, layer, start_frame), rs.stream);
+        const RopeLaunch rl = rope_launch(rs, layer, start_frame);
+        const GemmPlan& qp = *qkv[static_cast<size_t>(li)];
+        if (cfg_.fuse_rope_epilogue && gemm_rope_fusable(qp, rl)) {
+            // K2+K3 in one kernel: RoPE + pack in the QKV GEMM epilogue (no qkv round trip)
+            gemm_run(qp, rs.stream, &rl);
+            mark(li, 1);
+        } else {
+            gemm_run(qp, rs.stream);
+            mark(li, 1);
+            rope_run(rl, rs.stream);
+        }
         mark(li, 2);
         if (local) SPX_CUDA(cudaEventRecord(rs.ev_k3, rs.stream));
     }

@@ -8,13 +8,15 @@
 //   warp 1      : single-thread tcgen05.mma issuer, M=128 x N=BN x K=16 per instruction,
 //                 fp32 accumulator double-buffered in TMEM (2 x BN columns)
 //   warp 2      : TMEM allocator
-//   warps 4..7  : epilogue, tcgen05.ld -> (gate, residual) -> bf16 -> global
+//   warps 4..11 : epilogue (two warps per TMEM lane quarter, half the columns each),
+//                 tcgen05.ld -> (gate, residual | RoPE + pack) -> bf16 -> global
 //
 // The smem ring is 4 stages of (A 16 KB + B BN*128 B), SWIZZLE_128B everywhere.
 #include <cstdlib>
 
 #include "common.hpp"
 #include "kernels.hpp"
+#include "rope_device.cuh"
 #include "sm100.cuh"
 #include "tma.hpp"
 
@@ -27,7 +29,12 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kStages = 4;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;  // warps 4..11: two per TMEM lane quarter, splitting the columns
+// epi_mode 2 stages the rank's slice of the RoPE band tables in smem: T rows of the frames
+// its tokens span, all H rows, all W rows (the scattered per-row table reads from L1/L2 cost
+// more than the whole mainloop: 0.111 vs 0.054 ms for the Wan QKV GEMM)
+constexpr int kRopeSmemPairs = 2048;
 
 struct GemmParams {
     int M, N, K, k_inner;
@@ -38,20 +45,127 @@ struct GemmParams {
     const bf16* residual;
     int64_t ldr;
     const float* gate;
+    RopeLaunch rope;  // epi_mode 2
+    int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation
 };
 
 template <int BN>
 constexpr size_t gemm_smem_bytes() {
-    return 1024 + static_cast<size_t>(kStages) * (kBM * kBK * 2 + BN * kBK * 2) + 256;
+    return 1024 + static_cast<size_t>(kStages) * (kBM * kBK * 2 + BN * kBK * 2) + 256 +
+           kRopeSmemPairs * 8;
 }
 
-// one 32-column slice of an accumulator row -> (gate, residual) -> bf16 -> global
+
+// ---- RoPE band tables staged in smem (epi_mode 2) ----
+struct RopeSmem {
+    int t_lo, n_t;  // frames [t_lo, t_lo + n_t) of the T band
+    int off_h, off_w;
+};
+
+__host__ __device__ inline RopeSmem rope_smem_layout(const RopeLaunch& l) {
+    RopeSmem r;
+    const int64_t first = l.row_offset, last = l.row_offset + l.rows_per_batch - 1;
+    r.t_lo = static_cast<int>(l.start_frame + first / l.hw);
+    r.n_t = static_cast<int>(last / l.hw - first / l.hw + 1);
+    r.off_h = r.n_t * l.pairs[0];
+    r.off_w = r.off_h + static_cast<int>(l.hw / l.grid_w) * l.pairs[1];
+    return r;
+}
+
+__host__ __device__ inline int rope_smem_pairs(const RopeLaunch& l) {
+    const RopeSmem r = rope_smem_layout(l);
+    return r.off_w + static_cast<int>(l.grid_w) * l.pairs[2];
+}
+
+// every thread of the CTA: copy the slice (before the CTA-wide barrier that follows setup)
+__device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, float2* st) {
+    const RopeSmem r = rope_smem_layout(l);
+    const int nt = r.n_t * l.pairs[0];
+    const int total = rope_smem_pairs(l);
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        float2 v;
+        if (i < nt)
+            v = __ldg(&l.tab[0][r.t_lo * l.pairs[0] + i]);
+        else if (i < r.off_w)
+            v = __ldg(&l.tab[1][i - r.off_h]);
+        else
+            v = __ldg(&l.tab[2][i - r.off_w]);
+        st[i] = v;
+    }
+}
+
+// a token row's three band rows in the staged tables (computed once per row per tile)
+struct RopeRow {
+    const float2* t;  // T band row of its frame
+    const float2* h;  // H band row
+    const float2* w;  // W band row
+    bool valid;
+};
+
+__device__ __forceinline__ RopeRow rope_row(const RopeLaunch& l, const RopeSmem& r,
+                                            const float2* st, int row) {
+    int t, h, w;
+    rope_thw(l, row, t, h, w);
+    return {st + (t - r.t_lo) * l.pairs[0], st + r.off_h + h * l.pairs[1],
+            st + r.off_w + w * l.pairs[2], true};
+}
+
+// epi_mode 2: a 32-column slice of one head of q, k or v for token `row` at (t, h, w):
+// q/k pairs (2j, 2j+1) rotate in fp32 (rope.cpp:106-126) before the single bf16 rounding,
+// then the slice is stored into its head group's q slab / every KV-ring copy (the pack of
+// the fused all-to-all, as K3 does)
+__device__ __forceinline__ void rope_pack_chunk(const RopeLaunch& l, const RopeRow& rr, int row,
+                                                int col0, float (&f)[32]) {
+    const int C = l.heads * l.head_dim;
+    const int which = col0 / C;
+    const int c = col0 - which * C;
+    const int head = c / l.head_dim;
+    const int d0 = c - head * l.head_dim;
+    const int hpg = l.heads / l.groups;
+    const int g = head / hpg;
+    const int64_t off =
+        static_cast<int64_t>(row) * l.dst_row_stride + (head - g * hpg) * l.head_dim + d0;
+    if (which < 2 && rr.valid) {
+        const int p0 = l.pairs[0], p01 = l.pairs[0] + l.pairs[1];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int j = d0 / 2 + e;  // warp-uniform band selection
+            const float2 cs = j < p0 ? rr.t[j] : (j < p01 ? rr.h[j - p0] : rr.w[j - p01]);
+            const float a = f[2 * e], b = f[2 * e + 1];
+            f[2 * e] = a * cs.x - b * cs.y;
+            f[2 * e + 1] = a * cs.y + b * cs.x;
+        }
+    }
+    uint4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        v[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                          pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+    if (which == 0) {
+        uint4* d = reinterpret_cast<uint4*>(l.dst.q[g] + off);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d[q] = v[q];
+    } else {
+        for (int cp = 0; cp < l.dst.copies; ++cp) {
+            uint4* d = reinterpret_cast<uint4*>((which == 1 ? l.dst.k[g][cp] : l.dst.v[g][cp]) + off);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = v[q];
+        }
+    }
+}
+
+// one 32-column slice of an accumulator row -> (gate, residual | rope + pack) -> bf16 -> global
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0,
-                                               const uint32_t (&r)[32]) {
+                                               const uint32_t (&r)[32],
+                                               const RopeRow& rr = RopeRow{}) {
     if (row >= p.M || col0 >= p.N) return;
     float f[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+    if (p.epi_mode == 2) {
+        rope_pack_chunk(p.rope, rr, row, col0, f);
+        return;
+    }
     if (p.epi_mode == 1) {
         const uint4* res = reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
 #pragma unroll
@@ -94,6 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float2* s_rope = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(full) + 256);
+    const RopeSmem rope_l = p.epi_mode == 2 ? rope_smem_layout(p.rope) : RopeSmem{};
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -109,11 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], kEpiWarps * 32);
         }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+    if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -173,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        const int ew = warp % 4;         // TMEM lane quarter this warp may access
+        const int half = (warp - 4) / 4;  // which half of the tile's columns
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int acc = it & 1;
@@ -184,12 +302,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int row = m0 + ew * 32 + lane;
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+            RopeRow rr{};
+            if (p.epi_mode == 2 && row < p.M) rr = rope_row(p.rope, rope_l, s_rope, row);
+            if (p.experiment == 1) rr.valid = false;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
                 uint32_t r[32];
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
-                epilogue_chunk(p, row, n0 + c * 32, r);
+                epilogue_chunk(p, row, n0 + c * 32, r, rr);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
@@ -218,7 +339,8 @@ constexpr int kPairStages = 6;
 
 template <int BN>
 constexpr size_t gemm_pair_smem_bytes() {
-    return 1024 + static_cast<size_t>(kPairStages) * (128 * kBK * 2 + (BN / 2) * kBK * 2) + 256;
+    return 1024 + static_cast<size_t>(kPairStages) * (128 * kBK * 2 + (BN / 2) * kBK * 2) + 256 +
+           kRopeSmemPairs * 8;
 }
 
 template <int BN>
@@ -238,6 +360,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + kPairStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float2* s_rope = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(full) + 256);
+    const RopeSmem rope_l = p.epi_mode == 2 ? rope_smem_layout(p.rope) : RopeSmem{};
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -257,11 +381,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * 128);
+            mbar_init(&tempty[a], 2 * kEpiWarps * 32);
         }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
@@ -329,7 +454,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int ew = warp - 4;
+        const int ew = warp % 4;
+        const int half = (warp - 4) / 4;
         int it = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
             const int acc = it & 1;
@@ -340,12 +466,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int row = m0 + ew * 32 + lane;
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+            RopeRow rr{};
+            if (p.epi_mode == 2 && row < p.M) rr = rope_row(p.rope, rope_l, s_rope, row);
+            if (p.experiment == 1) rr.valid = false;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
                 uint32_t r[32];
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
-                epilogue_chunk(p, row, n0 + c * 32, r);
+                epilogue_chunk(p, row, n0 + c * 32, r, rr);
             }
             tc_fence_before();
             mbar_arrive_leader(&tempty[acc]);
@@ -449,7 +578,15 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
     }
 }
 
-void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
+bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope) {
+    const int C = rope.heads * rope.head_dim;
+    return rope.norm == 0 && rope.has_kv == 1 && rope.head_dim % 32 == 0 && C % plan.bn == 0 &&
+           rope_smem_pairs(rope) <= kRopeSmemPairs &&
+           plan.ops.N == 3 * C && plan.ops.M == rope.rows && plan.ops.groups == 1 &&
+           rope.rows < (int64_t(1) << 31) && rope.row_offset + rope.rows_per_batch < (int64_t(1) << 31);
+}
+
+void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope) {
     const GemmOperands& o = plan.ops;
     GemmParams p{};
     p.M = o.M;
@@ -464,6 +601,17 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream) {
     p.residual = o.residual;
     p.ldr = o.residual_row_stride;
     p.gate = o.gate;
+    if (rope) {
+        require(gemm_rope_fusable(plan, *rope), SPX_ERR_UNSUPPORTED,
+                "gemm: rope epilogue needs 3C outputs, C % BN == 0, D % 32 == 0, no QK-norm");
+        p.epi_mode = 2;
+        p.rope = *rope;
+    }
+    static const int experiment = [] {
+        const char* e = std::getenv("SPX_GEMM_EXPERIMENT");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.experiment = experiment;
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         gemm_bf16_tn_pair_kernel<256><<<plan.grid, kThreads, gemm_pair_smem_bytes<256>(), stream>>>(

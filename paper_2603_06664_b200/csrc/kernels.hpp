@@ -28,6 +28,7 @@ struct GemmOperands {
     int64_t out_row_stride = 0;
     int M = 0, N = 0, K = 0;
     // epilogue: 0 -> out = acc ; 1 -> out = residual + gate[col] * acc (adaLN gate + residual)
+    //           2 -> Causal-RoPE rotate-and-pack (set by gemm_run's rope argument)
     int epi_mode = 0;
     const bf16* residual = nullptr;
     int64_t residual_row_stride = 0;
@@ -43,8 +44,13 @@ struct GemmPlan {
     int grid = 0;
 };
 
+struct RopeLaunch;
 void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count);
-void gemm_run(const GemmPlan& plan, cudaStream_t stream);
+// rope != nullptr (QKV projection only): the epilogue applies Causal-RoPE to the q and k
+// columns of the fp32 accumulator and stores q / k / v straight into rope->dst (the K3
+// rotate-and-pack without its qkv round trip); requires gemm_rope_fusable()
+void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope = nullptr);
+bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope);
 
 // ---------------------------------------------------------------------------------------
 // K6: chunk-causal flash attention, tcgen05/TMEM, TMA-fed.
@@ -82,6 +88,7 @@ struct AttnPlan {
     CUtensorMap map_k;
     CUtensorMap map_k_pair;  // 64-row boxes: each CTA of a pair loads half of a K tile
     CUtensorMap map_v;
+    CUtensorMap map_v_half;  // 64-row boxes (K/V multicast mode)
     AttnOperands ops;
     int max_splits = 1;
 };

@@ -14,6 +14,7 @@
 // all-to-all's pack step), for every query-split copy of k/v.
 #include "common.hpp"
 #include "kernels.hpp"
+#include "rope_device.cuh"
 #include "sm100.cuh"
 
 namespace spx {
@@ -32,14 +33,6 @@ __device__ __forceinline__ void rope_position(int64_t i_local, int64_t row_offse
     t = start_frame + ig / hw;
     h = (ig % hw) / grid_w;
     w = ig % grid_w;
-}
-
-__device__ __forceinline__ float2 band_cs(const RopeLaunch& l, int j, int t, int h, int w) {
-    if (j < l.pairs[0]) return __ldg(&l.tab[0][t * l.pairs[0] + j]);
-    j -= l.pairs[0];
-    if (j < l.pairs[1]) return __ldg(&l.tab[1][h * l.pairs[1] + j]);
-    j -= l.pairs[1];
-    return __ldg(&l.tab[2][w * l.pairs[2] + j]);
 }
 
 __device__ __forceinline__ uint4 rotate_vec(uint4 x, const float2 (&cs)[4], float scale,
@@ -96,14 +89,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
 
     // (t, h, w) of this row (rope.cpp:97-101), 32-bit
-    const int i_local = row % static_cast<int>(l.rows_per_batch);
-    const int ig = static_cast<int>(l.row_offset) + i_local;
-    const int hw = static_cast<int>(l.hw), gw = static_cast<int>(l.grid_w);
-    const int tq = ig / hw;
-    const int t = static_cast<int>(l.start_frame) + tq;
-    const int rem = ig - tq * hw;
-    const int h = rem / gw;
-    const int w = rem - h * gw;
+    int t, h, w;
+    rope_thw(l, row, t, h, w);
     // this lane's four rotation pairs (identical for all of its vectors because D | 256)
     const int e0 = (8 * lane) % l.head_dim;
     float2 cs[4];

@@ -1,0 +1,35 @@
+// rope_device.cuh -- Causal-RoPE device helpers shared by K3 (rope.cu) and the QKV GEMM's
+// fused rotate-and-pack epilogue (gemm.cu).
+//
+// Reference: rotate_rows (proj/src/rope.cpp:78-131): local row i of rank r has global
+// position i_g = row_offset + i, frame t = start_frame + i_g / (H_g W_g),
+// h = (i_g mod H_g W_g) / W_g, w = i_g mod W_g (rope.cpp:97-101); pair j < p_T rotates by
+// T[t], then H[h], then W[w] (rope.cpp:106-126).
+#pragma once
+
+#include "kernels.hpp"
+
+namespace spx {
+
+// (cos, sin) of rotation pair j at position (t, h, w): band tables are [pos][pairs_b]
+__device__ __forceinline__ float2 band_cs(const RopeLaunch& l, int j, int t, int h, int w) {
+    if (j < l.pairs[0]) return __ldg(&l.tab[0][t * l.pairs[0] + j]);
+    j -= l.pairs[0];
+    if (j < l.pairs[1]) return __ldg(&l.tab[1][h * l.pairs[1] + j]);
+    j -= l.pairs[1];
+    return __ldg(&l.tab[2][w * l.pairs[2] + j]);
+}
+
+// (t, h, w) of local token row `row` (32-bit; rope_run checks the range)
+__device__ __forceinline__ void rope_thw(const RopeLaunch& l, int row, int& t, int& h, int& w) {
+    const int i_local = row % static_cast<int>(l.rows_per_batch);
+    const int ig = static_cast<int>(l.row_offset) + i_local;
+    const int hw = static_cast<int>(l.hw), gw = static_cast<int>(l.grid_w);
+    const int tq = ig / hw;
+    t = static_cast<int>(l.start_frame) + tq;
+    const int rem = ig - tq * hw;
+    h = rem / gw;
+    w = rem - h * gw;
+}
+
+}  // namespace spx

@@ -401,6 +401,7 @@ class GenerationConfig:
     qk_norm: bool = False
     norm_eps: float = 1e-6
     profile: bool = False
+    fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
 
     def block_len(self):
         return self.grid_per_block.seq_len()
@@ -428,6 +429,7 @@ class GenerationConfig:
         c.qk_norm = int(self.qk_norm)
         c.norm_eps = self.norm_eps
         c.profile = int(self.profile)
+        c.fuse_rope_epilogue = int(self.fuse_rope_epilogue)
         return c
 
     def validate(self):

@@ -62,11 +62,12 @@ def _engine_with_weights(cfg, w):
     return eng
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_single_layer_well_conditioned_matches_oracle(cuda, world):
+@pytest.mark.parametrize("world,fuse", [(1, True), (2, True), (4, True), (1, False), (4, False)])
+def test_single_layer_well_conditioned_matches_oracle(cuda, world, fuse):
+    """fuse: Causal-RoPE + pack in the QKV GEMM epilogue (default) or the standalone K3."""
     s = spattn()
     kw = dict(TINY, layers=1, num_blocks=2)
-    cfg = cfg_from(kw, steps=1, world=world)
+    cfg = cfg_from(kw, steps=1, world=world, fuse_rope_epilogue=fuse)
     dim = kw["heads"] * kw["head_dim"]
     w = _scaled_weights(dim, 1, 4.0)
     eng = _engine_with_weights(cfg, w)
@@ -79,15 +80,16 @@ def test_single_layer_well_conditioned_matches_oracle(cuda, world):
         assert rel_l2(centered(got[b]), centered(ref[b])) < 1e-2, b
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_sp_ranks_bit_identical_to_p1(cuda, world):
+@pytest.mark.parametrize("world,fuse", [(2, True), (4, True), (8, True), (8, False)])
+def test_sp_ranks_bit_identical_to_p1(cuda, world, fuse):
     """The reference's invariant (test_sp_attention.cpp:116-130): SP output == P=1 output.
     P = 8 with H = 4 runs the head-group x query-split partition (4 x 2)."""
     s = spattn()
     kw = dict(TINY)
     w = _scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 4.0, seed=7)
-    base = s.bf16_bits_to_float(_engine_with_weights(cfg_from(kw, world=1), w).generate())
-    eng = _engine_with_weights(cfg_from(kw, world=world), w)
+    base = s.bf16_bits_to_float(
+        _engine_with_weights(cfg_from(kw, world=1, fuse_rope_epilogue=fuse), w).generate())
+    eng = _engine_with_weights(cfg_from(kw, world=world, fuse_rope_epilogue=fuse), w)
     got = s.bf16_bits_to_float(eng.generate())
     assert np.array_equal(got, base)
 
@@ -266,3 +268,52 @@ def test_errors_map_to_reference_classes(cuda):
     with pytest.raises(s.AlignmentError):
         cache.update(0, torch.zeros(1, 6, 2, 4, device=cuda, dtype=torch.bfloat16),
                      torch.zeros(1, 6, 2, 4, device=cuda, dtype=torch.bfloat16))
+
+
+def _torch_reference_blocks(kw, w, seed=0):
+    """fp32 (GPU, torch) + fp64 RoPE (CPU oracle, exact reference positions) restatement of one
+    layer, one denoise step, over kw["num_blocks"] blocks with an unlimited KV cache: the
+    reference P = 1 path (sp_attention.cpp:317-348) at shapes the CPU oracle is too slow for."""
+    import torch
+
+    F, Hg, Wg, H, D = kw["frames"], kw["grid_h"], kw["grid_w"], kw["heads"], kw["head_dim"]
+    L, C = F * Hg * Wg, H * D
+    Wt = [torch.from_numpy(w[0, m]).cuda().float() for m in range(4)]
+    ks, vs, outs = [], [], []
+    for b in range(kw["num_blocks"]):
+        x = oracle.round_bf16(oracle.block_noise(seed, b, 0, (L, H, D))).reshape(L, C)
+        xt = torch.from_numpy(x).cuda().float()
+        q, k, v = (xt @ Wt[m].t() for m in range(3))
+        q, k = (torch.from_numpy(oracle.rope_causal_local(
+            t.cpu().double().numpy().reshape(L, H, D), (F, Hg, Wg), b * F, 0, 1,
+            max_frames=kw["num_blocks"] * F)).cuda().float() for t in (q, k))
+        ks.append(k)
+        vs.append(v.reshape(L, H, D))
+        kk, vv = torch.cat(ks), torch.cat(vs)
+        o = torch.softmax(torch.einsum("qhd,khd->hqk", q, kk) / math.sqrt(D), dim=-1)
+        o = torch.einsum("hqk,khd->qhd", o, vv).reshape(L, C)
+        outs.append((o @ Wt[3].t()).cpu().double().numpy())
+    return outs
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_rope_epilogue_matches_k3_at_wan_grid(cuda, world):
+    """The QKV GEMM's fused rotate-and-pack epilogue and the standalone K3 kernel, both vs an
+    fp32/fp64 restatement on the Wan 480P grid (3x30x52, H=12, D=128) with rank offsets and
+    a nonzero start frame (block 1): same positions and pack; the fused path rounds to bf16
+    once instead of twice, so it must be at least as close."""
+    s = spattn()
+    kw = dict(frames=3, grid_h=30, grid_w=52, num_blocks=2, layers=1, heads=12, head_dim=128)
+    w = _scaled_weights(kw["heads"] * kw["head_dim"], 1, 4.0, seed=11)
+    ref = _torch_reference_blocks(kw, w)
+    err = {}
+    for fuse in (True, False):
+        eng = _engine_with_weights(cfg_from(kw, steps=1, world=world, fuse_rope_epilogue=fuse), w)
+        got = s.bf16_bits_to_float(eng.generate())
+        err[fuse] = [(rel_l2(got[b].reshape(ref[b].shape), ref[b]),
+                      rel_l2(centered(got[b].reshape(ref[b].shape)), centered(ref[b])))
+                     for b in range(kw["num_blocks"])]
+    for b in range(kw["num_blocks"]):
+        assert err[True][b][0] < 5e-3 and err[False][b][0] < 5e-3, err
+        assert err[True][b][1] < 3e-2 and err[False][b][1] < 3e-2, err
+        assert err[True][b][1] <= 1.1 * err[False][b][1] + 1e-3, err
