@@ -255,20 +255,30 @@ def main():
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # profiling switched on for the timed chunks through a fresh config on the same engine
-    _set_profile(eng, True)
+    # attention launches bracketed by CUDA events on the engine stream (profile level 2: two
+    # events per call around the attention kernel, nothing else)
+    _set_profile(eng, 2)
     ev0.record(stream)
     for _ in range(args.steps):
         chunk_device()
     ev1.record(stream)
     barrier()
     clocks = sampler.stop()
-    _set_profile(eng, False)
+    _set_profile(eng, 0)
     launches = int(lib().spx_launch_count()) - launches0
     dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    stage_ms, calls = eng.stage_times()
+    attn_stage, attn_calls = eng.stage_times()
+    attn_ms = max_over_ranks(attn_stage["attention"] / max(attn_calls, 1))
     ms_per_chunk = dev_ms / args.steps
     fps = F * args.steps / (dev_ms / 1e3)
+
+    # ---- stage split: one more (untimed) chunk with every stage bracketed ----
+    check(lib().spx_engine_reset_stage_times(eng._h))
+    _set_profile(eng, 1)
+    chunk_device()
+    barrier()
+    _set_profile(eng, 0)
+    stage_ms, calls = eng.stage_times()
 
     # ---- e2e through the C ABI from pinned host memory (H2D noise, D2H latents each chunk) ----
     for _ in range(1):
@@ -283,9 +293,15 @@ def main():
     h2d = steps * Lp * C * 2
     d2h = Lp * C * 2
 
-    # ---- roofline of the dominant kernel (attention, chunk 0: S_kv = L) ----
+    # ---- C3: 5 s 480P video = 7 chunks, unlimited KV window (the ring grows to 21 frames) ----
+    video = run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev, out_dev,
+                      barrier, max_over_ranks, stream_ptr)
+
+    # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
     peaks, peak_src = load_peaks()
-    attn_ms = stage_ms["attention"] / max(calls, 1)
+    rope_mb = run_rope_microbench(torch, spattn, lib, check, peaks) if rank == 0 else None
+
+    # ---- roofline of the dominant kernel (attention, chunk 0: S_kv = L) ----
     s_kv = L
     flops = 4.0 * eng.query_rows * s_kv * eng.heads_per_group * D  # QK^T + PV per launch
     achieved = flops / (attn_ms * 1e-3) / 1e12
@@ -315,6 +331,10 @@ def main():
                      "peak_source": peak_src + " sustained bf16",
                      "flops_per_launch": flops, "avg_launch_ms": attn_ms},
         "stage_ms_per_call": {k: v / max(calls, 1) for k, v in stage_ms.items()},
+        "stage_note": "one extra untimed chunk with CUDA events between every stage (K2+K3 are "
+                      "one kernel when the RoPE epilogue is fused: 'rope' is then empty)",
+        "video_5s": video,
+        "rope_microbench": rope_mb,
         "clocks": clocks, "gpu_launches": launches, "ledger": eng.stats(),
     }
 
@@ -342,11 +362,131 @@ def main():
     return 0
 
 
-def _set_profile(eng, on):
-    """toggle per-stage CUDA-event timing on a live engine"""
+def _set_profile(eng, level):
+    """per-stage CUDA-event timing on a live engine: 0 off, 1 every stage, 2 attention only"""
     from paper_2603_06664_b200._lib import check, lib
 
-    check(lib().spx_engine_set_profile(eng._h, 1 if on else 0))
+    check(lib().spx_engine_set_profile(eng._h, int(level)))
+
+
+def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev, out_dev,
+              barrier, max_over_ranks, stream_ptr):
+    """C3: a 5 s 480P video (21 latent frames = 7 chunks, 4 denoise steps, unlimited KV
+    window) on a second engine; per-chunk device times (CUDA events on the engine stream),
+    one untimed warm-up video first. Noise: block 0's draws reused for every chunk (the
+    timing does not depend on the values)."""
+    import torch
+
+    F, Hg, Wg, H, D = WAN["frames"], WAN["grid_h"], WAN["grid_w"], WAN["heads"], WAN["head_dim"]
+    blocks = 7
+    cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(F, Hg, Wg), num_blocks=blocks,
+                                  layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H,
+                                  head_dim=D, world_size=world_size, seed=0, profile=False,
+                                  fuse_rope_epilogue=not args.no_fuse_rope)
+    eng = spattn.Engine(cfg, world=world)
+    sp = ctypes.c_void_p()
+    check(lib().spx_world_stream(world._h, 0, ctypes.byref(sp)))
+    stream = torch.cuda.ExternalStream(sp.value)
+
+    def chunk(b):
+        check(lib().spx_engine_generate_block_device(eng._h, b, ptr_array([noise_dev.data_ptr()]),
+                                                     ptr_array([out_dev.data_ptr()])))
+
+    for b in range(blocks):  # warm-up video
+        chunk(b)
+    barrier()
+    eng.reset_cache()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(blocks + 1)]
+    evs[0].record(stream)
+    for b in range(blocks):
+        chunk(b)
+        evs[b + 1].record(stream)
+    barrier()
+    chunk_ms = [max_over_ranks(evs[b].elapsed_time(evs[b + 1])) for b in range(blocks)]
+    total = sum(chunk_ms)
+    del eng
+    torch.cuda.empty_cache()
+    return {"workload": "C3: 5 s 480P = 7 chunks x 3 latent frames, 30 layers, 4 denoise steps, "
+                        "unlimited KV window (visible frames 3, 6, ..., 21)",
+            "latent_frames_per_s": 3 * blocks / (total / 1e3), "total_ms": total,
+            "first_frame_latency_ms": chunk_ms[0], "chunk_ms": chunk_ms}
+
+
+def run_rope_microbench(torch, spattn, lib, check, peaks):
+    """C4: the fused Causal-RoPE kernel (apply_rope_causal_local through the C ABI, optional
+    QK-RMSNorm) on one rank's q (L/P, 12, 128) bf16 vs the full-sequence control
+    (apply_rope_global over all L rows: what every rank rotates after the Alg. 1 gather).
+    Device time per launch from 50 launches captured in one CUDA graph, each on a different
+    buffer pair (more than 2x L2 in total, so the operands come from HBM); bytes = read +
+    write of the tensor (the roofline is HBM: 2 x rows x C x 2 B per launch)."""
+    F, Hg, Wg, H, D = WAN["frames"], WAN["grid_h"], WAN["grid_w"], WAN["heads"], WAN["head_dim"]
+    L, C = F * Hg * Wg, H * D
+    table = spattn.precompute_frequencies(21, Hg, Wg, D)
+    grid = spattn.GridSpec(F, Hg, Wg)
+    side = torch.cuda.Stream()
+    out = []
+    iters = 50
+
+    def timed(fn):
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(iters):
+                    fn()
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+            g.replay()
+            e1.record(side)
+            torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    nw = torch.ones(C, device="cuda", dtype=torch.bfloat16)
+    l2_bytes = 126 * 2 ** 20
+
+    def buffers(rows):
+        # enough distinct (x, y) pairs that consecutive launches never find their operands
+        # in the 126 MB L2: every launch streams from and to HBM
+        n = int(2 * l2_bytes // (2 * rows * C * 2)) + 2
+        xs = [torch.randn(1, rows, H, D, device="cuda").to(torch.bfloat16) for _ in range(n)]
+        return xs, [torch.empty_like(xs[0]) for _ in range(n)]
+
+    for P in (1, 8):
+        Lp = L // P
+        xs, ys = buffers(Lp)
+        for norm in (False, True):
+            it = [0]
+
+            def fn():
+                i = it[0] % len(xs)
+                it[0] += 1
+                spattn.apply_rope_causal_local(xs[i], grid, table, 18, P - 1, P,
+                                               norm_weight=nw if norm else None, out=ys[i])
+            ms = timed(fn)
+            gbs = 2 * xs[0].numel() * 2 / (ms * 1e-3) / 1e9
+            out.append({"op": "rope_causal_local" + ("+qk_rmsnorm" if norm else ""),
+                        "rows": Lp, "P": P, "start_frame": 18, "ms": ms, "GBs": gbs,
+                        "frac_hbm_peak": gbs / peaks["hbm_gbs"], "l2": "cold (rotating buffers)"})
+        del xs, ys
+    xs, ys = buffers(L)
+    it = [0]
+
+    def fg():
+        i = it[0] % len(xs)
+        it[0] += 1
+        spattn.apply_rope_global(xs[i], grid, table, 18, out=ys[i])
+    ms = timed(fg)
+    gbs = 2 * xs[0].numel() * 2 / (ms * 1e-3) / 1e9
+    out.append({"op": "rope_global (full-sequence control, Alg. 1 per rank)", "rows": L,
+                "start_frame": 18, "ms": ms, "GBs": gbs, "frac_hbm_peak": gbs / peaks["hbm_gbs"],
+                "l2": "cold (rotating buffers)"})
+    del xs, ys
+    torch.cuda.empty_cache()
+    return out
 
 
 if __name__ == "__main__":

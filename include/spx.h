@@ -233,7 +233,8 @@ typedef struct spx_engine_config {
     int32_t force_start_frame_zero;   /* fault injection (generator.hpp:30-32) */
     int32_t qk_norm;                  /* 0 = reference semantics; 1 = Wan QK-RMSNorm */
     float norm_eps;
-    int32_t profile;                  /* 1: CUDA-event stage timing on every call */
+    int32_t profile;                  /* 1: CUDA-event stage timing on every call;
+                                         2: the attention launch only */
     int32_t fuse_rope_epilogue;       /* 1 (default): Causal-RoPE + pack in the QKV GEMM
                                          epilogue when qk_norm = 0; 0: standalone K3 kernel */
 } spx_engine_config;
@@ -259,6 +260,9 @@ spx_status spx_engine_set_norm_weights(spx_engine* engine, int64_t layer, const 
 /* KvCache::update bookkeeping for a block (once per denoise step; every layer's ring gets
  * the same slots) -- generate() calls this itself */
 spx_status spx_engine_begin_block(spx_engine* engine, int64_t block_index);
+/* start a new video: every layer's KV cache empty (a fresh generate() builds new caches,
+ * generator.cpp:69-81); waits for the engine's streams */
+spx_status spx_engine_reset_cache(spx_engine* engine);
 /* one optimized_sp_self_attention call on every local rank: x_local / y_local are device
  * bf16 (1, L/P, H, D), indexed by local rank; y may not alias x */
 spx_status spx_engine_layer(spx_engine* engine, int64_t layer, int64_t block_index,
@@ -281,7 +285,7 @@ spx_status spx_engine_synchronize(spx_engine* engine);
  * (sp_attention.hpp:92-97); calls = number of profiled layer calls */
 spx_status spx_engine_stage_times(spx_engine* engine, double out_ms[6], int64_t* calls);
 spx_status spx_engine_reset_stage_times(spx_engine* engine);
-/* switch the CUDA-event stage timing on (1) / off (0) for subsequent calls */
+/* CUDA-event stage timing for subsequent calls: 0 off, 1 every stage, 2 attention only */
 spx_status spx_engine_set_profile(spx_engine* engine, int32_t on);
 spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
 

@@ -152,6 +152,7 @@ _SIGS = [
     ("spx_engine_set_layer_weights", c_int, [c_void_p, c_int64] + [c_void_p] * 4),
     ("spx_engine_set_norm_weights", c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     ("spx_engine_begin_block", c_int, [c_void_p, c_int64]),
+    ("spx_engine_reset_cache", c_int, [c_void_p]),
     ("spx_engine_layer", c_int, [c_void_p, c_int64, c_int64, c_int64, POINTER(c_void_p),
                                  POINTER(c_void_p)]),
     ("spx_engine_generate_block", c_int, [c_void_p, c_int64, c_void_p, c_void_p]),

@@ -739,6 +739,13 @@ spx_status spx_engine_begin_block(spx_engine* engine, int64_t block_index) {
     });
 }
 
+spx_status spx_engine_reset_cache(spx_engine* engine) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->reset_cache();
+    });
+}
+
 spx_status spx_engine_layer(spx_engine* engine, int64_t layer, int64_t block_index,
                             int64_t start_frame, void* const* x_local, void* const* y_local) {
     return guarded([&] {
@@ -794,7 +801,8 @@ spx_status spx_engine_reset_stage_times(spx_engine* engine) {
 spx_status spx_engine_set_profile(spx_engine* engine, int32_t on) {
     return guarded([&] {
         require_ptr(engine, "engine");
-        engine->e->set_profile(on != 0);
+        require(on >= 0 && on <= 2, SPX_ERR_CONFIG, "profile level must be 0, 1 or 2");
+        engine->e->set_profile(on);
     });
 }
 

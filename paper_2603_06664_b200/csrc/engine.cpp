@@ -314,6 +314,13 @@ void Engine::set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t*
     }
 }
 
+void Engine::reset_cache() {
+    synchronize();
+    frames_ = FrameRing(cap_frames_, cfg_.window_frames);
+    have_block_ = false;
+    current_block_ = -1;
+}
+
 void Engine::begin_block(int64_t block_index) {
     const int64_t first = frames_.update(block_index, F_);
     require(first + F_ <= cap_frames_, SPX_ERR_ALIGNMENT,
@@ -403,9 +410,11 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         pending_events_.push_back(free_events_.back());
         free_events_.pop_back();
         prof = &pending_events_.back();
+        prof->level = cfg_.profile;
     }
     auto mark = [&](int li, int k) {
-        if (prof && li == 0) SPX_CUDA(cudaEventRecord(prof->ev[k], ranks_[0].stream));
+        if (prof && li == 0 && (prof->level == 1 || k == 4 || k == 5))
+            SPX_CUDA(cudaEventRecord(prof->ev[k], ranks_[0].stream));
     };
 
     // K2 + K3 (the fused exchange is carried by K3's stores on the LOCAL transport)
@@ -622,8 +631,9 @@ void Engine::harvest_events() {
     if (pending_events_.empty()) return;
     SPX_CUDA(cudaSetDevice(ranks_[0].device));
     for (StageEvents& se : pending_events_) {
-        SPX_CUDA(cudaEventSynchronize(se.ev[6]));
+        SPX_CUDA(cudaEventSynchronize(se.ev[se.level == 1 ? 6 : 5]));
         for (int k = 0; k < 6; ++k) {
+            if (se.level != 1 && k != 4) continue;
             float ms = 0.0f;
             SPX_CUDA(cudaEventElapsedTime(&ms, se.ev[k], se.ev[k + 1]));
             stage_ms_[k] += ms;

@@ -70,6 +70,7 @@ struct RankState {
 
 struct StageEvents {
     cudaEvent_t ev[7];
+    int level = 1;  // 1: all seven stage marks; 2: the attention bracket (ev[4], ev[5]) only
 };
 
 class Engine {
@@ -87,6 +88,9 @@ class Engine {
                            const uint16_t* wv, const uint16_t* wo);
     void set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk);
     void begin_block(int64_t block_index);
+    // a new video: every layer's KV cache empty again (generate() builds fresh caches,
+    // generator.cpp:69-81); device ring memory is reused as is
+    void reset_cache();
     void layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,
                         void* const* y);
     void generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host);
@@ -97,7 +101,8 @@ class Engine {
     void synchronize();
     void stage_times(double out_ms[6], int64_t* calls);
     void reset_stage_times();
-    void set_profile(bool on) { cfg_.profile = on ? 1 : 0; }
+    // 0 off, 1 every stage (six CUDA-event intervals per call), 2 attention launch only
+    void set_profile(int level) { cfg_.profile = level; }
     spx_comm_stats stats() const { return world_->stats(); }
 
   private:

@@ -64,7 +64,7 @@ __device__ __forceinline__ uint4 rotate_vec(uint4 x, const float2 (&cs)[4], floa
 // NV = 16-byte vectors per lane per tensor (C / 256, rounded up). Every load of the row
 // (q, k and v: 3 NV vectors per lane) is issued before any math, so each warp keeps
 // 3 x NV x 512 B in flight; the position math is 32-bit.
-template <int NV>
+template <int NV, bool KV, bool NORM>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     rope_norm_pack_kernel(const RopeLaunch l) {
     const int lane = threadIdx.x % 32;
@@ -75,13 +75,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const int hpg = l.heads / l.groups;
     const uint4* src = reinterpret_cast<const uint4*>(l.in + static_cast<int64_t>(row) * l.in_row_stride);
 
-    uint4 xq[NV], xk[NV], xv[NV];
+    uint4 xq[NV], xk[KV ? NV : 1], xv[KV ? NV : 1];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int v = lane + 32 * i;
         if (v < nvec) {
             xq[i] = __ldg(src + v);
-            if (l.has_kv) {
+            if constexpr (KV) {
                 xk[i] = __ldg(src + nvec + v);
                 xv[i] = __ldg(src + 2 * nvec + v);
             }
@@ -98,19 +98,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (int e = 0; e < 4; ++e) cs[e] = band_cs(l, e0 / 2 + e, t, h, w);
 
     float scale_q = 1.0f, scale_k = 1.0f;
-    if (l.norm) {  // QK-RMSNorm over the C channels (Wan mode; no reference counterpart)
+    if constexpr (NORM) {  // QK-RMSNorm over the C channels (Wan mode; no reference counterpart)
         float sq = 0.0f, sk = 0.0f;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             if (lane + 32 * i < nvec) {
                 const uint32_t a[4] = {xq[i].x, xq[i].y, xq[i].z, xq[i].w};
-                const uint32_t b[4] = {xk[i].x, xk[i].y, xk[i].z, xk[i].w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const float2 fa = unpack_bf16x2(a[e]);
-                    const float2 fb = unpack_bf16x2(b[e]);
                     sq = fmaf(fa.x, fa.x, fmaf(fa.y, fa.y, sq));
-                    sk = fmaf(fb.x, fb.x, fmaf(fb.y, fb.y, sk));
+                }
+                if constexpr (KV) {
+                    const uint32_t b[4] = {xk[i].x, xk[i].y, xk[i].z, xk[i].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 fb = unpack_bf16x2(b[e]);
+                        sk = fmaf(fb.x, fb.x, fmaf(fb.y, fb.y, sk));
+                    }
                 }
             }
         }
@@ -122,8 +127,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         scale_q = rsqrtf(sq / static_cast<float>(C) + l.norm_eps);
         scale_k = rsqrtf(sk / static_cast<float>(C) + l.norm_eps);
     }
-    const uint4* nwq = l.norm ? reinterpret_cast<const uint4*>(l.norm_w_q) : nullptr;
-    const uint4* nwk = l.norm ? reinterpret_cast<const uint4*>(l.norm_w_k) : nullptr;
+    const uint4* nwq = NORM ? reinterpret_cast<const uint4*>(l.norm_w_q) : nullptr;
+    const uint4* nwk = NORM ? reinterpret_cast<const uint4*>(l.norm_w_k) : nullptr;
 
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                             (head - g * hpg) * l.head_dim + e0;
         *reinterpret_cast<uint4*>(l.dst.q[g] + off) =
             rotate_vec(xq[i], cs, scale_q, nwq ? nwq + v : nullptr);
-        if (l.has_kv) {
+        if constexpr (KV) {
             const uint4 yk = rotate_vec(xk[i], cs, scale_k, nwk ? nwk + v : nullptr);
             for (int c = 0; c < l.dst.copies; ++c) {
                 *reinterpret_cast<uint4*>(l.dst.k[g][c] + off) = yk;
@@ -157,6 +162,32 @@ __global__ void rope_positions_kernel(int64_t rows, int64_t row_offset, int64_t 
     w32[i] = static_cast<int32_t>(w);
 }
 
+template <int NV>
+void launch_rope_nv(const RopeLaunch& l, unsigned blocks, cudaStream_t stream) {
+    const dim3 b(kWarpsPerBlock * 32);
+    if (l.has_kv && l.norm)
+        rope_norm_pack_kernel<NV, true, true><<<blocks, b, 0, stream>>>(l);
+    else if (l.has_kv)
+        rope_norm_pack_kernel<NV, true, false><<<blocks, b, 0, stream>>>(l);
+    else if (l.norm)
+        rope_norm_pack_kernel<NV, false, true><<<blocks, b, 0, stream>>>(l);
+    else
+        rope_norm_pack_kernel<NV, false, false><<<blocks, b, 0, stream>>>(l);
+}
+
+void launch_rope(const RopeLaunch& l, int nv, unsigned blocks, cudaStream_t stream) {
+    switch (nv) {
+        case 1: launch_rope_nv<1>(l, blocks, stream); break;
+        case 2: launch_rope_nv<2>(l, blocks, stream); break;
+        case 3: launch_rope_nv<3>(l, blocks, stream); break;
+        case 4: launch_rope_nv<4>(l, blocks, stream); break;
+        case 5: launch_rope_nv<5>(l, blocks, stream); break;
+        case 6: launch_rope_nv<6>(l, blocks, stream); break;
+        case 7: launch_rope_nv<7>(l, blocks, stream); break;
+        default: launch_rope_nv<8>(l, blocks, stream); break;
+    }
+}
+
 }  // namespace
 
 void rope_run(const RopeLaunch& l, cudaStream_t stream) {
@@ -172,16 +203,7 @@ void rope_run(const RopeLaunch& l, cudaStream_t stream) {
     require(l.rows < (int64_t(1) << 31) && l.row_offset + l.rows_per_batch < (int64_t(1) << 31),
             SPX_ERR_RANGE, "rope kernel: row indices must fit in 32 bits");
     const unsigned blocks = static_cast<unsigned>(ceil_div(l.rows, kWarpsPerBlock));
-    switch ((C / 8 + 31) / 32) {
-        case 1: rope_norm_pack_kernel<1><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 2: rope_norm_pack_kernel<2><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 3: rope_norm_pack_kernel<3><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 4: rope_norm_pack_kernel<4><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 5: rope_norm_pack_kernel<5><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 6: rope_norm_pack_kernel<6><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        case 7: rope_norm_pack_kernel<7><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-        default: rope_norm_pack_kernel<8><<<blocks, kWarpsPerBlock * 32, 0, stream>>>(l); break;
-    }
+    launch_rope(l, (C / 8 + 31) / 32, blocks, stream);
     SPX_CUDA_LAUNCH();
     count_launch();
 }

@@ -479,6 +479,10 @@ class Engine:
     def begin_block(self, block_index):
         check(lib().spx_engine_begin_block(self._h, block_index))
 
+    def reset_cache(self):
+        """a new video: empty KV caches (a fresh generate() builds new ones)."""
+        check(lib().spx_engine_reset_cache(self._h))
+
     def optimized_sp_self_attention(self, layer, block_index, start_frame, x_locals):
         """one optimized_sp_self_attention call (sp_attention.hpp:118-130) on every rank."""
         torch = _torch()
