@@ -5,16 +5,8 @@
 // block causality is structural (the cache only exposes past + current frames). Softmax is
 // order-invariant, so the ring's two chronological segments are visited in storage order.
 //
-// One CTA = one 128-row query tile of one head. Warp roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j through a 2-stage ring
-//   warp 1      single-thread tcgen05.mma issuer:
-//                 S_j = Q K_j^T   (M=128, N=128, K=D; A,B K-major)   -> TMEM S[j%2]
-//                 O  += P_j V_j   (M=128, N=D,  K=128; A K-major smem, B MN-major)  -> TMEM O
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..7  softmax: one thread per query row (TMEM lane), online max with lazy
-//               rescaling (only when the running max grows by > 2^8), P_j written to smem
-//               (bf16, SWIZZLE_128B K-major) for the PV MMA; finally O / l -> bf16, stored
-//               straight into the output-exchange destination slab of that row.
+// The kernel (attn_fwd_v2_kernel below): one CTA = one 128-row query tile of one head, its kv
+// range split between two softmax warpgroups that ping-pong against one MMA thread.
 #include <algorithm>
 
 #include "common.hpp"
@@ -30,7 +22,6 @@ namespace {
 
 constexpr int kBQ = 128;     // query rows per CTA
 constexpr int kBKV = 128;    // kv rows per tile
-constexpr int kThreads = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct AttnParams {
@@ -54,20 +45,6 @@ struct AttnParams {
     int experiment;  // profiling only (SPX_ATTN_EXPERIMENT): 1 skip softmax math, 2 no MUFU
 };
 
-template <int D>
-struct AttnSmem {
-    static constexpr uint32_t kChunks = D / 64;
-    static constexpr uint32_t kTileBytes = kBKV * D * 2;      // one K or V tile
-    static constexpr uint32_t kQBytes = kBQ * D * 2;
-    static constexpr uint32_t kPBytes = kBQ * kBKV * 2;
-    static constexpr uint32_t kOffQ = 0;
-    static constexpr uint32_t kOffK = kOffQ + kQBytes;
-    static constexpr uint32_t kOffV = kOffK + 2 * kTileBytes;
-    static constexpr uint32_t kOffP = kOffV + 2 * kTileBytes;
-    static constexpr uint32_t kOffBar = kOffP + 2 * kPBytes;
-    static constexpr uint32_t kBytes = kOffBar + 256 + 1024;
-};
-
 __device__ __forceinline__ void kv_tile_coords(const AttnParams& p, int j, int& row, int& valid) {
     if (j < p.seg_tiles0) {
         row = p.seg_start[0] + j * kBKV;
@@ -76,246 +53,6 @@ __device__ __forceinline__ void kv_tile_coords(const AttnParams& p, int j, int& 
         const int t = j - p.seg_tiles0;
         row = p.seg_start[1] + t * kBKV;
         valid = min(kBKV, p.seg_len[1] - t * kBKV);
-    }
-}
-
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q,
-                    const __grid_constant__ CUtensorMap map_k,
-                    const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    using L = AttnSmem<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint8_t* sQ = smem + L::kOffQ;
-    uint8_t* sK = smem + L::kOffK;
-    uint8_t* sV = smem + L::kOffV;
-    uint8_t* sP = smem + L::kOffP;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-    uint64_t* bar_q = bars + 0;
-    uint64_t* k_full = bars + 1;     // [2]
-    uint64_t* v_full = bars + 3;     // [2]
-    uint64_t* kv_empty = bars + 5;   // [2]
-    uint64_t* s_full = bars + 7;     // [2]
-    uint64_t* p_full = bars + 9;     // [2]
-    uint64_t* pv_done = bars + 11;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
-
-    const int warp = threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    const int q_tile = blockIdx.x;
-    const int head = blockIdx.y;
-    const int b = blockIdx.z;
-    const int n_tiles = p.total_tiles;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&map_q);
-        tma_prefetch_desc(&map_k);
-        tma_prefetch_desc(&map_v);
-        mbar_init(bar_q, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&k_full[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 128);
-            mbar_init(&pv_done[i], 1);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const uint32_t tmem_s[2] = {tmem_base, tmem_base + 128};
-    const uint32_t tmem_o = tmem_base + 256;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(bar_q, L::kQBytes);
-#pragma unroll
-            for (int c = 0; c < (int)L::kChunks; ++c) {
-                tma_load_3d(sQ + c * (kBQ * 128), &map_q, bar_q, c * 64, head,
-                            b * 0 + q_tile * kBQ + 0);
-            }
-            for (int j = 0; j < n_tiles; ++j) {
-                const int st = j & 1;
-                mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-                int row, valid;
-                kv_tile_coords(p, j, row, valid);
-                mbar_arrive_expect_tx(&k_full[st], L::kTileBytes);
-#pragma unroll
-                for (int c = 0; c < (int)L::kChunks; ++c)
-                    tma_load_3d(sK + st * L::kTileBytes + c * (kBKV * 128), &map_k, &k_full[st],
-                                c * 64, head, row);
-                mbar_arrive_expect_tx(&v_full[st], L::kTileBytes);
-#pragma unroll
-                for (int c = 0; c < (int)L::kChunks; ++c)
-                    tma_load_3d(sV + st * L::kTileBytes + c * (kBKV * 128), &map_v, &v_full[st],
-                                c * 64, head, row);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
-            constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
-            const uint32_t q_addr = smem_u32(sQ);
-            auto issue_s = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&k_full[st], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t k_addr = smem_u32(sK + st * L::kTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    umma_bf16_ss(tmem_s[st], make_desc_sw128(q_addr + off, 16, 1024),
-                                 make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
-                }
-                umma_commit(&s_full[st]);
-            };
-            mbar_wait(bar_q, 0);
-            tc_fence_after();
-            issue_s(0);
-            for (int j = 0; j < n_tiles; ++j) {
-                const int st = j & 1;
-                if (j + 1 < n_tiles) issue_s(j + 1);
-                mbar_wait(&p_full[st], (j >> 1) & 1);
-                mbar_wait(&v_full[st], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t p_addr = smem_u32(sP + st * L::kPBytes);
-                const uint32_t v_addr = smem_u32(sV + st * L::kTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < kBKV / 16; ++kk) {
-                    const uint32_t p_off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    const uint32_t v_off = kk * 16 * 128;
-                    umma_bf16_ss(tmem_o, make_desc_sw128(p_addr + p_off, 16, 1024),
-                                 make_desc_sw128(v_addr + v_off, kBKV * 128, 1024), idesc_o,
-                                 (j | kk) != 0);
-                }
-                umma_commit(&pv_done[st]);
-                umma_commit(&kv_empty[st]);
-            }
-        }
-    } else if (warp >= 4) {
-        const int ew = warp - 4;
-        const int r = ew * 32 + lane;   // query row within the tile == TMEM lane
-        const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
-        float m_run = -INFINITY;
-        float l_run = 0.0f;
-        for (int j = 0; j < n_tiles; ++j) {
-            const int st = j & 1;
-            int row, valid;
-            kv_tile_coords(p, j, row, valid);
-            mbar_wait(&s_full[st], (j >> 1) & 1);
-            tc_fence_after();
-            float s[kBKV];
-#pragma unroll
-            for (int c = 0; c < kBKV / 32; ++c) {
-                uint32_t u[32];
-                tmem_ld32(tmem_s[st] + lane_off + c * 32, u);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(u[e]) * p.scale_log2;
-            }
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < kBKV; ++c) {
-                if (c < valid) mx = fmaxf(mx, s[c]);
-            }
-            const float m_new = fmaxf(m_run, mx);
-            if (j == 0) {
-                m_run = m_new;
-            } else {
-                const bool need = m_new > m_run + kRescaleThreshold;
-                if (__any_sync(0xffffffffu, need)) {
-                    // rescale O (after PV_{j-1} has landed) to the new running max
-                    const int pj = j - 1;
-                    mbar_wait(&pv_done[pj & 1], (pj >> 1) & 1);
-                    tc_fence_after();
-                    const float alpha = ex2_approx(m_run - m_new);
-#pragma unroll 1
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t u[32];
-                        tmem_ld32(tmem_o + lane_off + c * 32, u);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
-                        tmem_st32(tmem_o + lane_off + c * 32, u);
-                    }
-                    tmem_st_wait();
-                    l_run *= alpha;
-                    m_run = m_new;
-                }
-            }
-            // P_j goes into buffer st: PV_{j-2} must have finished reading it
-            if (j >= 2) mbar_wait(&pv_done[st], ((j - 2) >> 1) & 1);
-            uint8_t* prow = sP + st * L::kPBytes + r * 128;
-            const uint32_t sw = static_cast<uint32_t>(r & 7);
-            float lsum = 0.0f;
-#pragma unroll
-            for (int u = 0; u < kBKV / 8; ++u) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int c0 = u * 8 + e * 2;
-                    const float p0 = (c0 < valid) ? ex2_approx(s[c0] - m_run) : 0.0f;
-                    const float p1 = (c0 + 1 < valid) ? ex2_approx(s[c0 + 1] - m_run) : 0.0f;
-                    w[e] = pack_bf16x2(p0, p1);
-                    const float2 back = unpack_bf16x2(w[e]);
-                    lsum += back.x + back.y;
-                }
-                const int chunk = u >> 3;
-                const uint32_t unit = static_cast<uint32_t>(u & 7) ^ sw;
-                *reinterpret_cast<uint4*>(prow + chunk * (128 * 128) + unit * 16) =
-                    make_uint4(w[0], w[1], w[2], w[3]);
-            }
-            l_run += lsum;
-            fence_proxy_async_smem();
-            tc_fence_before();
-            mbar_arrive(&p_full[st]);
-        }
-        const int last = n_tiles - 1;
-        mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
-        tc_fence_after();
-        const float inv_l = 1.0f / l_run;
-        const int qi = q_tile * kBQ + r;
-        bf16* dst = nullptr;
-        if (qi < p.sq) {
-            const int chunk = qi / p.rows_per_chunk;
-            dst = p.out_base[chunk] + b * p.out_batch_stride +
-                  static_cast<int64_t>(qi - chunk * p.rows_per_chunk) * p.out_row_stride +
-                  static_cast<int64_t>(head) * D;
-        }
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-            uint32_t u[32];
-            tmem_ld32(tmem_o + lane_off + c * 32, u);
-            tmem_ld_wait();
-            if (dst) {
-                uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    d4[q] = make_uint4(
-                        pack_bf16x2(__uint_as_float(u[q * 8 + 0]) * inv_l,
-                                    __uint_as_float(u[q * 8 + 1]) * inv_l),
-                        pack_bf16x2(__uint_as_float(u[q * 8 + 2]) * inv_l,
-                                    __uint_as_float(u[q * 8 + 3]) * inv_l),
-                        pack_bf16x2(__uint_as_float(u[q * 8 + 4]) * inv_l,
-                                    __uint_as_float(u[q * 8 + 5]) * inv_l),
-                        pack_bf16x2(__uint_as_float(u[q * 8 + 6]) * inv_l,
-                                    __uint_as_float(u[q * 8 + 7]) * inv_l));
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
     }
 }
 
@@ -946,19 +683,6 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
     }
 }
 
-template <int D>
-void attn_set_attr() {
-    static bool done[64] = {};
-    int dev = 0;
-    SPX_CUDA(cudaGetDevice(&dev));
-    if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(AttnSmem<D>::kBytes)));
-        done[dev & 63] = true;
-    }
-}
-
 }  // namespace
 
 int attn_max_splits(const AttnOperands& ops, int sm_count) {
@@ -1079,10 +803,6 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     }
     dim3 grid(static_cast<unsigned>(ceil_div(o.sq, kBQ)), static_cast<unsigned>(o.heads),
               static_cast<unsigned>(o.batch));
-    static const bool use_v1 = [] {
-        const char* e = std::getenv("SPX_ATTN_KERNEL");
-        return e && std::string(e) == "v1";
-    }();
     // D = 128 kernel: 0 single CTA (default); opt-in, both measured slower on B200:
     //   1 CTA-pair MMAs (SPX_ATTN_KERNEL=pair): 4680x4680x12 0.225 vs 0.135 ms -- every
     //     S -> P -> PV hand-off crosses SMs with only two S buffers to hide it;
@@ -1094,17 +814,7 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         if (e && std::string(e) == "mcast") return 2;
         return 0;
     }();
-    if (use_v1) {
-        if (o.head_dim == 128) {
-            attn_set_attr<128>();
-            attn_fwd_kernel<128><<<grid, kThreads, AttnSmem<128>::kBytes, stream>>>(
-                plan.map_q, plan.map_k, plan.map_v, p);
-        } else {
-            attn_set_attr<64>();
-            attn_fwd_kernel<64><<<grid, kThreads, AttnSmem<64>::kBytes, stream>>>(
-                plan.map_q, plan.map_k, plan.map_v, p);
-        }
-    } else if (o.head_dim == 128 && mode128 != 0) {
+    if (o.head_dim == 128 && mode128 != 0) {
         grid.x = (grid.x + 1) & ~1u;  // whole CTA pairs; the padding tile's rows are all >= sq
         grid.z = static_cast<unsigned>(p.splits);
         if (mode128 == 1)
