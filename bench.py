@@ -154,6 +154,8 @@ def main():
     ap.add_argument("--impl", default="spx", choices=["spx", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no timing line)")
+    ap.add_argument("--skip-long-video", action="store_true",
+                    help="skip the C5 60 s rolling-window run (about 10 s of GPU time)")
     ap.add_argument("--no-fuse-rope", action="store_true",
                     help="standalone K3 RoPE/pack kernel instead of the QKV GEMM epilogue")
     args = ap.parse_args()
@@ -294,8 +296,14 @@ def main():
     d2h = Lp * C * 2
 
     # ---- C3: 5 s 480P video = 7 chunks, unlimited KV window (the ring grows to 21 frames) ----
-    video = run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev, out_dev,
-                      barrier, max_over_ranks, stream_ptr)
+    video = video_5s(run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev,
+                               out_dev, barrier, max_over_ranks, blocks=7))
+    # ---- C5: 60 s 480P (80 chunks) with a 21-frame rolling window, kernels already warm ----
+    long_video = None
+    if not args.skip_long_video:
+        long_video = video_60s(run_video(args, spattn, lib, check, ptr_array, world, world_size,
+                                         noise_dev, out_dev, barrier, max_over_ranks, blocks=80,
+                                         window=21, warmup=False), 21)
 
     # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
     peaks, peak_src = load_peaks()
@@ -334,6 +342,7 @@ def main():
         "stage_note": "one extra untimed chunk with CUDA events between every stage (K2+K3 are "
                       "one kernel when the RoPE epilogue is fused: 'rope' is then empty)",
         "video_5s": video,
+        "video_60s": long_video,
         "rope_microbench": rope_mb,
         "clocks": clocks, "gpu_launches": launches, "ledger": eng.stats(),
     }
@@ -370,18 +379,19 @@ def _set_profile(eng, level):
 
 
 def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev, out_dev,
-              barrier, max_over_ranks, stream_ptr):
-    """C3: a 5 s 480P video (21 latent frames = 7 chunks, 4 denoise steps, unlimited KV
-    window) on a second engine; per-chunk device times (CUDA events on the engine stream),
-    one untimed warm-up video first. Noise: block 0's draws reused for every chunk (the
-    timing does not depend on the values)."""
+              barrier, max_over_ranks, blocks=7, window=-1, warmup=True):
+    """A video of `blocks` chunks (3 latent frames each, 30 layers, 4 denoise steps) on a
+    second engine; per-chunk device times (CUDA events on the engine stream). window < 0:
+    unlimited KV cache; otherwise the rolling window of `window` frames (the ring wraps and
+    attention walks two segments). Noise: block 0's draws reused for every chunk (timing does
+    not depend on the values)."""
     import torch
 
     F, Hg, Wg, H, D = WAN["frames"], WAN["grid_h"], WAN["grid_w"], WAN["heads"], WAN["head_dim"]
-    blocks = 7
     cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(F, Hg, Wg), num_blocks=blocks,
                                   layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H,
                                   head_dim=D, world_size=world_size, seed=0, profile=False,
+                                  window_frames=window if window > 0 else None,
                                   fuse_rope_epilogue=not args.no_fuse_rope)
     eng = spattn.Engine(cfg, world=world)
     sp = ctypes.c_void_p()
@@ -392,10 +402,11 @@ def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev,
         check(lib().spx_engine_generate_block_device(eng._h, b, ptr_array([noise_dev.data_ptr()]),
                                                      ptr_array([out_dev.data_ptr()])))
 
-    for b in range(blocks):  # warm-up video
-        chunk(b)
-    barrier()
-    eng.reset_cache()
+    if warmup:
+        for b in range(blocks):
+            chunk(b)
+        barrier()
+        eng.reset_cache()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(blocks + 1)]
     evs[0].record(stream)
     for b in range(blocks):
@@ -403,13 +414,29 @@ def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev,
         evs[b + 1].record(stream)
     barrier()
     chunk_ms = [max_over_ranks(evs[b].elapsed_time(evs[b + 1])) for b in range(blocks)]
-    total = sum(chunk_ms)
     del eng
     torch.cuda.empty_cache()
+    return chunk_ms
+
+
+def video_5s(chunk_ms):
+    total = sum(chunk_ms)
     return {"workload": "C3: 5 s 480P = 7 chunks x 3 latent frames, 30 layers, 4 denoise steps, "
                         "unlimited KV window (visible frames 3, 6, ..., 21)",
-            "latent_frames_per_s": 3 * blocks / (total / 1e3), "total_ms": total,
+            "latent_frames_per_s": 3 * len(chunk_ms) / (total / 1e3), "total_ms": total,
             "first_frame_latency_ms": chunk_ms[0], "chunk_ms": chunk_ms}
+
+
+def video_60s(chunk_ms, window):
+    steady = chunk_ms[window // 3:]
+    srt = sorted(steady)
+    return {"workload": f"C5: 60 s 480P = {len(chunk_ms)} chunks x 3 latent frames, rolling KV "
+                        f"window of {window} frames (the ring wraps: attention over 2 segments)",
+            "latent_frames_per_s": 3 * len(chunk_ms) / (sum(chunk_ms) / 1e3),
+            "steady_state_frames_per_s": 3 * len(steady) / (sum(steady) / 1e3),
+            "steady_chunk_ms": {"mean": sum(steady) / len(steady), "p50": srt[len(srt) // 2],
+                                "max": srt[-1], "min": srt[0]},
+            "first_frame_latency_ms": chunk_ms[0], "total_ms": sum(chunk_ms)}
 
 
 def run_rope_microbench(torch, spattn, lib, check, peaks):
