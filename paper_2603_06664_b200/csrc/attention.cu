@@ -327,8 +327,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 for (uint32_t k = 0; k < kSlots; ++k, ++t)
                     mbar_wait(&slot_empty[t % kSlots], ((t / kSlots) & 1) ^ 1);
             }
-        } else if (warp == 1 && lane == 0 && leader) {
+        } else if (warp == 1 && leader) {
             // ---------------- MMA issuer ----------------
+            // The whole warp runs the control flow (waits, slot and descriptor arithmetic stay
+            // warp-uniform, in uniform registers); one elected lane issues the tcgen05 ops.
+            const bool issuer = elect_one();
             constexpr uint32_t kM = kPair ? 2 * kBQ : kBQ;
             constexpr uint32_t idesc_s = make_idesc_bf16(kM, kBKV, false, false);
             constexpr uint32_t idesc_o = make_idesc_bf16(kM, D, false, true);
@@ -358,20 +361,25 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             auto issue_s = [&](int i) {
                 const uint32_t slot = take();
                 const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
+                if (issuer) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    const uint32_t koff = (kk >> 2) * kKChunk + (kk & 3) * 32;
-                    if constexpr (kPair)
-                        umma_bf16_ss_pair(tmem_base + i * 128,
-                                          make_desc_sw128(q_addr + qoff, 16, 1024),
-                                          make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
-                    else
-                        umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + qoff, 16, 1024),
-                                     make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                        const uint32_t koff = (kk >> 2) * kKChunk + (kk & 3) * 32;
+                        if constexpr (kPair)
+                            umma_bf16_ss_pair(tmem_base + i * 128,
+                                              make_desc_sw128(q_addr + qoff, 16, 1024),
+                                              make_desc_sw128(k_addr + koff, 16, 1024), idesc_s,
+                                              kk > 0);
+                        else
+                            umma_bf16_ss(tmem_base + i * 128,
+                                         make_desc_sw128(q_addr + qoff, 16, 1024),
+                                         make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
+                    }
+                    commit(&s_full[i]);
+                    release(&slot_empty[slot]);
                 }
-                commit(&s_full[i]);
-                release(&slot_empty[slot]);
+                __syncwarp();
             };
             auto issue_pv = [&](int i, int j) {
                 const uint32_t slot = take();
@@ -381,19 +389,23 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     mbar_wait(&p_full[i], j & 1);
                 tc_fence_after();
                 const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
+                if (issuer) {
 #pragma unroll
-                for (int kk = 0; kk < kBKV / 16; ++kk) {
-                    if constexpr (kPair)
-                        umma_bf16_ts_pair(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
-                                          make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                          idesc_o, (j | kk) != 0);
-                    else
-                        umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
-                                     make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                     idesc_o, (j | kk) != 0);
+                    for (int kk = 0; kk < kBKV / 16; ++kk) {
+                        if constexpr (kPair)
+                            umma_bf16_ts_pair(tmem_base + 256 + i * 128,
+                                              tmem_base + i * 128 + kk * 8,
+                                              make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                              idesc_o, (j | kk) != 0);
+                        else
+                            umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                                         make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                         idesc_o, (j | kk) != 0);
+                    }
+                    commit(&pv_done[i]);
+                    release(&slot_empty[slot]);
                 }
-                commit(&pv_done[i]);
-                release(&slot_empty[slot]);
+                __syncwarp();
             };
             mbar_wait(q_full, 0);
             tc_fence_after();

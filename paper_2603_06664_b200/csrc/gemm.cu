@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // whole warp: uniform control flow and descriptors; one elected lane issues
+        const bool issuer = elect_one();
+        {
             constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, false, false);
             int stage = 0;
             uint32_t phase = 0;
@@ -274,19 +276,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * kABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+                    if (issuer) {
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        umma_bf16_ss(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
-                                     make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                                     (kt | k) != 0);
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            umma_bf16_ss(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
+                                         make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                                         (kt | k) != 0);
+                        }
+                        umma_commit(&empty[stage]);
                     }
-                    umma_commit(&empty[stage]);
+                    __syncwarp();
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                if (issuer) umma_commit(&tfull[acc]);
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
@@ -422,7 +428,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        const bool issuer = elect_one();
+        if (leader) {
             constexpr uint32_t idesc = make_idesc_bf16(256, BN, false, false);
             int stage = 0;
             uint32_t phase = 0;
@@ -438,19 +445,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * kABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+                    if (issuer) {
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        umma_bf16_ss_pair(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
-                                          make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                                          (kt | k) != 0);
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            umma_bf16_ss_pair(d_tmem, make_desc_sw128(a_addr + k * 32, 16, 1024),
+                                              make_desc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                                              (kt | k) != 0);
+                        }
+                        umma_commit_pair(&empty[stage], 0x3);
                     }
-                    umma_commit_pair(&empty[stage], 0x3);
+                    __syncwarp();
                     if (++stage == kPairStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit_pair(&tfull[acc], 0x3);
+                if (issuer) umma_commit_pair(&tfull[acc], 0x3);
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
