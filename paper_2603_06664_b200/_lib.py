@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_uint8, c_uint16, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspx.so")
+# SPX_LIB: an alternative build of the same library (tools/build_variant.sh experiments)
+LIB_PATH = os.environ.get("SPX_LIB") or os.path.join(_HERE, "libspx.so")
 
 
 class SpxError(RuntimeError):

@@ -23,6 +23,17 @@ namespace {
 constexpr int kBQ = 128;     // query rows per CTA
 constexpr int kBKV = 128;    // kv rows per tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// exponentials computed by the FMA-pipe polynomial, out of every 8 (the rest on MUFU.EX2)
+// (measured on B200: 0 of 8 is fastest -- 0.741 vs 0.764 ms at 4680 x 32760 x 12 with 2 of 8;
+// MUFU.EX2 is not the limit once the MMA issue is warp-uniform)
+#ifndef SPX_POLY_OF_8
+#define SPX_POLY_OF_8 0
+#endif
+// P_i hand-off to the MMA thread: one arrival per softmax warp (after __syncwarp) instead of
+// one per thread
+#ifndef SPX_PFULL_PER_WARP
+#define SPX_PFULL_PER_WARP 0
+#endif
 
 struct AttnParams {
     int sq;
@@ -117,19 +128,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
         "r"(r[15])
         : "memory");
-}
-
-// 2^x on the FMA pipe (offloads part of the exponentials from MUFU): round-to-nearest split,
-// degree-3 minimax for 2^f on [-1/2, 1/2] (max rel. error 8.4e-5 << bf16's 2^-9)
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -126.0f);  // keeps the exponent add >= 0 (no sign/NaN wrap)
-    const float t = x + 12582912.0f;
-    const int ji = __float_as_int(t) - 0x4B400000;
-    const float f = x - (t - 12582912.0f);
-    float p = fmaf(0.0553458875f, f, 0.24260599f);
-    p = fmaf(p, f, 0.69322751f);
-    p = fmaf(p, f, 0.999927776f);
-    return __int_as_float(__float_as_int(p) + (ji << 23));
 }
 
 // ---- packed f32x2 arithmetic (FFMA2 / FADD2: two lanes per issue slot on sm_100) ----
@@ -249,7 +247,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], kPair ? 256 : 128);
+            mbar_init(&p_full[i], (kPair ? 2 : 1) * (SPX_PFULL_PER_WARP ? 4 : 128));
             mbar_init(&pv_done[i], 1);
         }
         fence_mbar_init();
@@ -441,10 +439,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tc_fence_after();
             if (p.experiment == 1) {  // profiling: MMA/TMA/barrier skeleton only
                 tc_fence_before();
-                if constexpr (kPair)
-                    mbar_arrive_leader(&p_full[i]);
-                else
-                    mbar_arrive(&p_full[i]);
+                if (SPX_PFULL_PER_WARP) __syncwarp();
+                if (!SPX_PFULL_PER_WARP || lane == 0) {
+                    if constexpr (kPair)
+                        mbar_arrive_leader(&p_full[i]);
+                    else
+                        mbar_arrive(&p_full[i]);
+                }
                 continue;
             }
             uint32_t u[kBKV];
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2,
                     nm2);
                 float2 pr;
-                if ((e & 7) >= 6) {  // 1/4 of the exponentials on the FMA pipe
+                if ((e & 7) >= 8 - SPX_POLY_OF_8) {  // part of the exponentials on the FMA pipe
                     pr = ex2_poly2(x);
                 } else {
                     if (p.experiment == 2) {  // profiling: no MUFU
@@ -520,10 +521,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_s + c * 16, &pk[c * 16]);
             tmem_st_wait();
             tc_fence_before();
-            if constexpr (kPair)
-                mbar_arrive_leader(&p_full[i]);
-            else
-                mbar_arrive(&p_full[i]);
+            if (SPX_PFULL_PER_WARP) __syncwarp();
+            if (!SPX_PFULL_PER_WARP || lane == 0) {
+                if constexpr (kPair)
+                    mbar_arrive_leader(&p_full[i]);
+                else
+                    mbar_arrive(&p_full[i]);
+            }
         }
         if (n > 0) {
             mbar_wait(&pv_done[i], (n - 1) & 1);
