@@ -218,6 +218,12 @@ spx_status spx_exchange_plan(int32_t which, int32_t rank, int32_t world_size, in
  * ------------------------------------------------------------------------------------- */
 typedef struct spx_engine spx_engine;
 
+/* AblationFlags bits (proj/include/spattn/sp_attention.hpp:36-44) */
+#define SPX_ABLATION_FUSED_ALL_TO_ALL 1
+#define SPX_ABLATION_LOCAL_ROPE 2
+#define SPX_ABLATION_PRECOMPUTED_FREQS 4
+#define SPX_ABLATION_ALL 7
+
 typedef struct spx_engine_config {
     int64_t frames, grid_h, grid_w;   /* GridSpec per block (F = tau, H_g, W_g) */
     int64_t num_blocks;
@@ -237,6 +243,10 @@ typedef struct spx_engine_config {
                                          2: the attention launch only */
     int32_t fuse_rope_epilogue;       /* 1 (default): Causal-RoPE + pack in the QKV GEMM
                                          epilogue when qk_norm = 0; 0: standalone K3 kernel */
+    int32_t ablation;                 /* AblationFlags (sp_attention.hpp:36-44) as bits:
+                                         1 use_fused_all_to_all, 2 use_local_rope,
+                                         4 use_precomputed_freqs; 7 = optimized (default),
+                                         0 = the baseline Alg. 1 schedule */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */

@@ -680,6 +680,7 @@ void spx_engine_config_defaults(spx_engine_config* c) {
     c->norm_eps = 1e-6f;
     c->profile = 0;
     c->fuse_rope_epilogue = 1;
+    c->ablation = SPX_ABLATION_ALL;
 }
 
 spx_status spx_engine_config_validate(const spx_engine_config* cfg, int32_t world_size) {

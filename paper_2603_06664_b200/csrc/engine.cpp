@@ -70,6 +70,8 @@ void Engine::validate(const spx_engine_config& c, int world_size) {
     const int64_t G = choose_head_groups(world_size, c.heads);
     require(G <= 8 && world_size / G <= 8, SPX_ERR_PARTITION,
             "partition needs <= 8 head groups and <= 8 query splits");
+    require(c.ablation >= 0 && c.ablation <= SPX_ABLATION_ALL, SPX_ERR_CONFIG,
+            "ablation must be a combination of the three AblationFlags bits");
 }
 
 Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_(cfg) {
@@ -161,6 +163,14 @@ void Engine::allocate() {
         rs.qkv = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * 3 * C_));
         rs.q_recv = dev_alloc<bf16>(rs, static_cast<size_t>(Lq_ * Hl_ * D_));
         rs.o_recv = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
+        if (!(cfg_.ablation & SPX_ABLATION_FUSED_ALL_TO_ALL)) {  // all-gather targets (L, C)
+            for (auto** g : {&rs.gq, &rs.gk, &rs.gv}) *g = dev_alloc<bf16>(rs, static_cast<size_t>(L_ * C_));
+        }
+        if (!(cfg_.ablation & SPX_ABLATION_PRECOMPUTED_FREQS)) {  // recomputed table slice
+            const int64_t n = (cfg_.num_blocks * F_) * table_->pairs(0) + Hg_ * table_->pairs(1) +
+                              Wg_ * table_->pairs(2);
+            rs.tab_scratch = dev_alloc<float2>(rs, static_cast<size_t>(n));
+        }
         if (nccl) {
             rs.q_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
             rs.k_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
@@ -357,6 +367,11 @@ RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start
         rl.tab[b] = t.band[b];
         rl.pairs[b] = static_cast<int>(table_->pairs(b));
     }
+    if (!(cfg_.ablation & SPX_ABLATION_PRECOMPUTED_FREQS)) {  // this call's recomputed slice
+        rl.tab[0] = rs.tab_scratch;
+        rl.tab[1] = rl.tab[0] + (start_frame + F_) * rl.pairs[0];
+        rl.tab[2] = rl.tab[1] + Hg_ * rl.pairs[1];
+    }
     if (cfg_.qk_norm) {
         const DeviceWeights& w = weights_.at(rs.device);
         rl.norm = 1;
@@ -417,12 +432,40 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
             SPX_CUDA(cudaEventRecord(prof->ev[k], ranks_[0].stream));
     };
 
+    // AblationFlags (sp_attention.cpp:229-292); the default is the optimized schedule
+    const bool fused = cfg_.ablation & SPX_ABLATION_FUSED_ALL_TO_ALL;
+    const bool local_rope = cfg_.ablation & SPX_ABLATION_LOCAL_ROPE;
+    if (!(cfg_.ablation & SPX_ABLATION_PRECOMPUTED_FREQS)) {
+        // recompute_slice (sp_attention.cpp:191-195): frames [0, s + F), all rows, all columns
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            const int pairs[3] = {static_cast<int>(table_->pairs(0)), static_cast<int>(table_->pairs(1)),
+                                  static_cast<int>(table_->pairs(2))};
+            const int rows[3] = {static_cast<int>(start_frame + F_), static_cast<int>(Hg_),
+                                 static_cast<int>(Wg_)};
+            float2* band[3] = {rs.tab_scratch, rs.tab_scratch + rows[0] * pairs[0],
+                               rs.tab_scratch + rows[0] * pairs[0] + rows[1] * pairs[1]};
+            rope_table_run(band, rows, pairs, cfg_.rope_base, rs.stream);
+        }
+    }
+
     // K2 + K3 (the fused exchange is carried by K3's stores on the LOCAL transport)
     for (int li = 0; li < nl; ++li) {
         RankState& rs = ranks_[static_cast<size_t>(li)];
         SPX_CUDA(cudaSetDevice(rs.device));
         mark(li, 0);
-        const RopeLaunch rl = rope_launch(rs, layer, start_frame);
+        RopeLaunch rl = rope_launch(rs, layer, start_frame);
+        if (!local_rope) rl.rotate = 0;  // exchange first, rotate after (apply_rope_global)
+        if (!fused) {  // this rank's rows of the all-gathered q | k | v (all heads)
+            rl.groups = 1;
+            rl.dst = RopeDest{};
+            const int64_t off = static_cast<int64_t>(rs.rank) * Lp_ * C_;
+            rl.dst.q[0] = rs.gq + off;
+            rl.dst.k[0][0] = rs.gk + off;
+            rl.dst.v[0][0] = rs.gv + off;
+            rl.dst.copies = 1;
+            rl.dst_row_stride = C_;
+        }
         const GemmPlan& qp = *qkv[static_cast<size_t>(li)];
         if (cfg_.fuse_rope_epilogue && gemm_rope_fusable(qp, rl)) {
             // K2+K3 in one kernel: RoPE + pack in the QKV GEMM epilogue (no qkv round trip)
@@ -436,22 +479,79 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         mark(li, 2);
         if (local) SPX_CUDA(cudaEventRecord(rs.ev_k3, rs.stream));
     }
-    if (local) {
-        for (int li = 0; li < nl; ++li) {
-            RankState& rs = ranks_[static_cast<size_t>(li)];
+    if (fused) {
+        if (local) {
+            for (int li = 0; li < nl; ++li) {
+                RankState& rs = ranks_[static_cast<size_t>(li)];
+                SPX_CUDA(cudaSetDevice(rs.device));
+                for (int lj = 0; lj < nl; ++lj)
+                    if (lj != li)
+                        SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(lj)].ev_k3, 0));
+            }
+        } else if (P_ > 1) {
+            // one NCCL group == one round: the plan's sends and receives (exchange_plan.cpp)
+            RankState& rs = ranks_[0];
             SPX_CUDA(cudaSetDevice(rs.device));
-            for (int lj = 0; lj < nl; ++lj)
-                if (lj != li)
-                    SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(lj)].ev_k3, 0));
+            run_plan(rs, layer, plan_qkv_exchange(part_, rs.rank, block_base_row_));
         }
-    } else if (P_ > 1) {
-        // one NCCL group == one round: the plan's sends and receives (exchange_plan.cpp)
-        RankState& rs = ranks_[0];
-        SPX_CUDA(cudaSetDevice(rs.device));
-        run_plan(rs, layer, plan_qkv_exchange(part_, rs.rank, block_base_row_));
+        // ledger: one fused exchange (q: G-1 peers, k/v: P-1 peers per source) ...
+        world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
+    } else {
+        // three all-gathers along the sequence (collectives.cpp:180-201; ledger +1 each)
+        const int64_t shape[4] = {1, Lp_, H_, D_};
+        for (int t = 0; t < 3; ++t) {
+            std::vector<void*> in, out;
+            for (RankState& rs : ranks_) {
+                bf16* g = t == 0 ? rs.gq : t == 1 ? rs.gk : rs.gv;
+                in.push_back(g + static_cast<int64_t>(rs.rank) * Lp_ * C_);
+                out.push_back(g);
+            }
+            world_->all_gather(in.data(), out.data(), shape, 2, 1);
+        }
     }
-    // ledger: one fused exchange (q: G-1 peers, k/v: P-1 peers per source) ...
-    world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
+    if (!local_rope) {
+        // apply_rope_global after the exchange: in place on this rank's q and k rows
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            const RopeLaunch base = rope_launch(rs, layer, start_frame);
+            auto rotate_in_place = [&](bf16* x, int64_t rows, int64_t row_offset, int64_t heads) {
+                RopeLaunch r = base;
+                r.in = x;
+                r.in_row_stride = heads * D_;
+                r.rows = rows;
+                r.rows_per_batch = rows;
+                r.heads = static_cast<int>(heads);
+                r.groups = 1;
+                r.has_kv = 0;
+                r.norm = 0;
+                r.row_offset = row_offset;
+                r.dst = RopeDest{};
+                r.dst.q[0] = x;
+                r.dst_row_stride = heads * D_;
+                rope_run(r, rs.stream);
+            };
+            if (fused) {  // the head shard: q rows of this query split, k rows of the block
+                rotate_in_place(rs.q_recv, Lq_, rs.p * Lq_, Hl_);
+                rotate_in_place(rs.rings[static_cast<size_t>(layer)].k + block_base_row_ * Hl_ * D_,
+                                L_, 0, Hl_);
+            } else {      // the full sequence, every head (Alg. 1)
+                rotate_in_place(rs.gq, L_, 0, H_);
+                rotate_in_place(rs.gk, L_, 0, H_);
+            }
+        }
+    }
+    if (!fused) {
+        // split_heads (collectives.cpp:298-312): this rank's head group (and query split)
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            KvRingStorage& ring = rs.rings[static_cast<size_t>(layer)];
+            Box4 bq{{1, Lq_, Hl_, D_}, {L_ * C_, C_, D_, 1}, {Lq_ * Hl_ * D_, Hl_ * D_, D_, 1}};
+            copy_box_run(rs.q_recv, rs.gq + rs.p * Lq_ * C_ + rs.g * Hl_ * D_, bq, 2, rs.stream);
+            Box4 bkv{{1, L_, Hl_, D_}, {L_ * C_, C_, D_, 1}, {L_ * Hl_ * D_, Hl_ * D_, D_, 1}};
+            copy_box_run(ring.k + block_base_row_ * Hl_ * D_, rs.gk + rs.g * Hl_ * D_, bkv, 2, rs.stream);
+            copy_box_run(ring.v + block_base_row_ * Hl_ * D_, rs.gv + rs.g * Hl_ * D_, bkv, 2, rs.stream);
+        }
+    }
 
     // K6 attention, output rows stored straight into their source's o_recv slab
     for (int li = 0; li < nl; ++li) {

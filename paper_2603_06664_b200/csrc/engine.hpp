@@ -57,6 +57,10 @@ struct RankState {
     bf16* k_send = nullptr;
     bf16* v_send = nullptr;
     bf16* o_send = nullptr;           // NCCL: [G][L/P][H/G*D]
+    bf16* gq = nullptr;               // ablation without the fused exchange: all-gathered
+    bf16* gk = nullptr;               //   q, k, v of the whole block, (L, C)
+    bf16* gv = nullptr;
+    float2* tab_scratch = nullptr;    // ablation without precomputed freqs: per-call table
     std::vector<KvRingStorage> rings; // per layer
     std::vector<GemmPlan> qkv_plan;   // per layer, A = x[layer % 2]
     std::vector<GemmPlan> o_plan;     // per layer, out = x[(layer + 1) % 2]

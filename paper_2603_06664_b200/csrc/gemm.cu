@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
             if (p.epi_mode == 2 && row < p.M) rr = rope_row(p.rope, rope_l, s_rope, row);
-            if (p.experiment == 1) rr.valid = false;
+            if (p.experiment == 1 || !p.rope.rotate) rr.valid = false;
 #pragma unroll 1
             for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
                 uint32_t r[32];
@@ -479,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
             if (p.epi_mode == 2 && row < p.M) rr = rope_row(p.rope, rope_l, s_rope, row);
-            if (p.experiment == 1) rr.valid = false;
+            if (p.experiment == 1 || !p.rope.rotate) rr.valid = false;
 #pragma unroll 1
             for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
                 uint32_t r[32];

@@ -134,11 +134,17 @@ struct RopeLaunch {
     const bf16* norm_w_k = nullptr;
     float norm_eps = 1e-6f;
     int norm = 0;
+    int rotate = 1;                  // 0: pack only (the exchange-first ablation rotates later)
     RopeDest dst;
     int64_t dst_row_stride = 0;      // elements between rows in a destination slab (H/G * D)
 };
 
 void rope_run(const RopeLaunch& l, cudaStream_t stream);
+// precompute_frequencies on the device (the use_precomputed_freqs = false ablation recomputes
+// a slice every call, sp_attention.cpp:191-195): band b rows [0, rows[b]) x pairs[b] of
+// (cos, sin)(m * base^(-j / pairs[b])) in fp64, stored as fp32
+void rope_table_run(float2* const band[3], const int rows[3], const int pairs[3], double base,
+                    cudaStream_t stream);
 // Debug probe: the kernel's own (t, h, w) index math for every local row.
 void rope_positions_run(int64_t rows, int64_t row_offset, int64_t hw, int64_t grid_w,
                         int64_t start_frame, int32_t* t, int32_t* h, int32_t* w,

@@ -12,6 +12,8 @@
 // channels, a Wan-mode extension with no reference counterpart); v is copied. Every vector is
 // written straight into the destination slab of its head group (the sequence<->head
 // all-to-all's pack step), for every query-split copy of k/v.
+#include <algorithm>
+
 #include "common.hpp"
 #include "kernels.hpp"
 #include "rope_device.cuh"
@@ -95,7 +97,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const int e0 = (8 * lane) % l.head_dim;
     float2 cs[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) cs[e] = band_cs(l, e0 / 2 + e, t, h, w);
+    for (int e = 0; e < 4; ++e)
+        cs[e] = l.rotate ? band_cs(l, e0 / 2 + e, t, h, w) : make_float2(1.0f, 0.0f);
 
     float scale_q = 1.0f, scale_k = 1.0f;
     if constexpr (NORM) {  // QK-RMSNorm over the C channels (Wan mode; no reference counterpart)
@@ -147,6 +150,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                 *reinterpret_cast<uint4*>(l.dst.v[g][c] + off) = xv[i];
             }
         }
+    }
+}
+
+__global__ void rope_table_kernel(float2* b0, float2* b1, float2* b2, int r0, int r1, int r2,
+                                  int p0, int p1, int p2, double base) {
+    const int n0 = r0 * p0, n1 = r1 * p1, n2 = r2 * p2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2;
+         i += gridDim.x * blockDim.x) {
+        int k = i, p;
+        float2* out;
+        if (k < n0) {
+            p = p0;
+            out = b0;
+        } else if (k - n0 < n1) {
+            k -= n0;
+            p = p1;
+            out = b1;
+        } else {
+            k -= n0 + n1;
+            p = p2;
+            out = b2;
+        }
+        const int m = k / p, j = k - m * p;
+        // rope.cpp:37-41: freq = base^(-j/p), angle = m * freq
+        const double freq = pow(base, -static_cast<double>(j) / static_cast<double>(p));
+        double sn, cs;
+        sincos(static_cast<double>(m) * freq, &sn, &cs);
+        out[k] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
     }
 }
 
@@ -204,6 +235,16 @@ void rope_run(const RopeLaunch& l, cudaStream_t stream) {
             SPX_ERR_RANGE, "rope kernel: row indices must fit in 32 bits");
     const unsigned blocks = static_cast<unsigned>(ceil_div(l.rows, kWarpsPerBlock));
     launch_rope(l, (C / 8 + 31) / 32, blocks, stream);
+    SPX_CUDA_LAUNCH();
+    count_launch();
+}
+
+void rope_table_run(float2* const band[3], const int rows[3], const int pairs[3], double base,
+                    cudaStream_t stream) {
+    const int n = rows[0] * pairs[0] + rows[1] * pairs[1] + rows[2] * pairs[2];
+    if (n == 0) return;
+    rope_table_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148)), 256, 0, stream>>>(
+        band[0], band[1], band[2], rows[0], rows[1], rows[2], pairs[0], pairs[1], pairs[2], base);
     SPX_CUDA_LAUNCH();
     count_launch();
 }

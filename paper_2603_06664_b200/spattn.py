@@ -381,6 +381,33 @@ class CommWorld:
         return outs
 
 
+@dataclass(frozen=True)
+class AblationFlags:
+    """AblationFlags (sp_attention.hpp:36-44): the optimized schedule is all_on(), the
+    baseline Alg. 1 schedule (3 all-gathers, global RoPE, head split) all_off()."""
+
+    use_fused_all_to_all: bool = False
+    use_local_rope: bool = False
+    use_precomputed_freqs: bool = False
+
+    @staticmethod
+    def all_off():
+        return AblationFlags()
+
+    @staticmethod
+    def all_on():
+        return AblationFlags(True, True, True)
+
+    @staticmethod
+    def lattice():
+        """the 2^3 combinations (tests/acceptance.cpp:269-321)"""
+        return [AblationFlags(bool(m & 1), bool(m & 2), bool(m & 4)) for m in range(8)]
+
+    def bits(self) -> int:
+        return int(self.use_fused_all_to_all) | int(self.use_local_rope) << 1 | \
+            int(self.use_precomputed_freqs) << 2
+
+
 @dataclass
 class GenerationConfig:
     """GenerationConfig (generator.hpp:14-42) with the device knobs of spx_engine_config."""
@@ -402,6 +429,7 @@ class GenerationConfig:
     norm_eps: float = 1e-6
     profile: bool = False
     fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
+    ablation: AblationFlags = field(default_factory=AblationFlags.all_on)
 
     def block_len(self):
         return self.grid_per_block.seq_len()
@@ -430,6 +458,7 @@ class GenerationConfig:
         c.norm_eps = self.norm_eps
         c.profile = int(self.profile)
         c.fuse_rope_epilogue = int(self.fuse_rope_epilogue)
+        c.ablation = self.ablation.bits()
         return c
 
     def validate(self):

@@ -317,3 +317,57 @@ def test_rope_epilogue_matches_k3_at_wan_grid(cuda, world):
         assert err[True][b][0] < 5e-3 and err[False][b][0] < 5e-3, err
         assert err[True][b][1] < 3e-2 and err[False][b][1] < 3e-2, err
         assert err[True][b][1] <= 1.1 * err[False][b][1] + 1e-3, err
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_ablation_lattice_bit_identical(cuda, world):
+    """The 2^3 AblationFlags lattice (tests/acceptance.cpp:269-321, test_sp_attention.cpp:
+    169-192) on the device: baseline Alg. 1 (3 all-gathers, global RoPE, head split),
+    exchange-then-rotate, local RoPE + all-gather, per-call table recompute ... all produce
+    the optimized P = 1 output bit for bit (K3 standalone, so every path rounds q/k once after
+    the projection and once after the rotation; P = 8 with H = 4 runs 4 groups x 2 splits)."""
+    s = spattn()
+    kw = dict(TINY)
+    w = _scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 4.0, seed=13)
+    base = s.bf16_bits_to_float(
+        _engine_with_weights(cfg_from(kw, world=1, fuse_rope_epilogue=False), w).generate())
+    for flags in s.AblationFlags.lattice():
+        eng = _engine_with_weights(cfg_from(kw, world=world, fuse_rope_epilogue=False,
+                                            ablation=flags), w)
+        got = s.bf16_bits_to_float(eng.generate())
+        assert np.array_equal(got, base), flags
+
+
+def test_ablation_lattice_fused_epilogue_close(cuda):
+    """With the QKV-epilogue RoPE (one rounding), rotate-after-exchange variants round twice:
+    equal to within bf16 rounding of q/k."""
+    s = spattn()
+    kw = dict(TINY)
+    w = _scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 4.0, seed=13)
+    base = s.bf16_bits_to_float(_engine_with_weights(cfg_from(kw, world=2), w).generate())
+    for flags in s.AblationFlags.lattice():
+        got = s.bf16_bits_to_float(_engine_with_weights(cfg_from(kw, world=2, ablation=flags), w).generate())
+        for b in range(kw["num_blocks"]):
+            assert rel_l2(got[b], base[b]) < 5e-3, flags
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ablation_ledger_matches_reference(cuda, world):
+    """Ledger signatures per call: fused -> {fused 1, a2a 1}, otherwise {all_gather 3, a2a 1}
+    (test_sp_attention.cpp:132-148), and elements equal to a live reference run of the same
+    ablation mask."""
+    s = spattn()
+    kw = dict(frames=3, grid_h=4, grid_w=4, num_blocks=2, layers=2, heads=8, head_dim=64)
+    calls = 2 * 2 * 2
+    for flags in s.AblationFlags.lattice():
+        eng = s.Engine(cfg_from(kw, world=world, ablation=flags))
+        eng.generate()
+        st = eng.stats()
+        if flags.use_fused_all_to_all:
+            assert (st["fused_all_to_all"], st["all_gather"], st["all_to_all"]) == (calls, 0, calls)
+        else:
+            assert (st["fused_all_to_all"], st["all_gather"], st["all_to_all"]) == (0, 3 * calls, calls)
+        if oracle.ref_available():
+            _, ledger = oracle.ref_generate(**kw, steps=2, world=world, variant="optimized",
+                                            ablation=flags.bits())
+            assert st == ledger, flags
