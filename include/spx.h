@@ -304,6 +304,13 @@ spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
  * ------------------------------------------------------------------------------------- */
 spx_status spx_debug_naive_gemm(const void* a, const void* b, float* out, int64_t m, int64_t n,
                                 int64_t k, void* stream);
+/* Force the projection GEMM tile variant for plans made after the call: -1 = the planner's
+ * modelled choice; 0 pair 256x256, 1 pair 256x128, 2 single 128x256, 3 single 128x128,
+ * 4 single 128x192 (tests and tuning; also SPX_GEMM_VARIANT at load time). */
+spx_status spx_debug_set_gemm_variant(int32_t variant);
+/* SPX_GEMM_EXPERIMENT=5 only: copy n of the pair GEMM's per-tile clock64 marks of the last
+ * launch ([cta][16 tiles][mma start, mma issued, epilogue start, epilogue end]) */
+spx_status spx_debug_gemm_trace(int64_t* out, int64_t n);
 spx_status spx_debug_naive_attention(const void* q, const void* k, const void* v, float* out,
                                      int64_t batch, int64_t sq, int64_t skv, int64_t heads,
                                      int64_t head_dim, void* stream);

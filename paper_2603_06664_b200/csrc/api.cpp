@@ -825,6 +825,23 @@ spx_status spx_debug_naive_gemm(const void* a, const void* b, float* out, int64_
     });
 }
 
+spx_status spx_debug_gemm_trace(int64_t* out, int64_t n) {
+    return guarded([&] {
+        require(out && n >= 0 && n <= 1024 * 16 * 4, SPX_ERR_CONFIG, "trace buffer");
+        SPX_CUDA(cudaDeviceSynchronize());
+        SPX_CUDA(cudaMemcpy(out, gemm_trace_buffer(), static_cast<size_t>(n) * 8,
+                            cudaMemcpyDeviceToHost));
+    });
+}
+
+spx_status spx_debug_set_gemm_variant(int32_t variant) {
+    return guarded([&] {
+        require(variant >= -1 && variant < gemm_num_variants(), SPX_ERR_CONFIG,
+                "gemm variant out of range");
+        gemm_force_variant(variant);
+    });
+}
+
 spx_status spx_debug_naive_attention(const void* q, const void* k, const void* v, float* out,
                                      int64_t batch, int64_t sq, int64_t skv, int64_t heads,
                                      int64_t head_dim, void* stream) {

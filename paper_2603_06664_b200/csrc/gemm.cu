@@ -12,6 +12,7 @@
 //                 tcgen05.ld -> (gate, residual | RoPE + pack) -> bf16 -> global
 //
 // The smem ring is 4 stages of (A 16 KB + B BN*128 B), SWIZZLE_128B everywhere.
+#include <atomic>
 #include <cstdlib>
 
 #include "common.hpp"
@@ -35,6 +36,8 @@ constexpr int kEpiWarps = 8;  // warps 4..11: two per TMEM lane quarter, splitti
 // its tokens span, all H rows, all W rows (the scattered per-row table reads from L1/L2 cost
 // more than the whole mainloop: 0.111 vs 0.054 ms for the Wan QKV GEMM)
 constexpr int kRopeSmemPairs = 2048;
+// per epilogue warp: 32 rows x 32 bf16 columns staged for the coalescing transpose
+constexpr int kEpiStageBytes = 32 * 64;
 
 struct GemmParams {
     int M, N, K, k_inner;
@@ -46,13 +49,19 @@ struct GemmParams {
     int64_t ldr;
     const float* gate;
     RopeLaunch rope;  // epi_mode 2
-    int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation
+    int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation,
+                      // 5 = per-tile clock64 timeline of the pair kernel into `trace`
+    long long* trace;  // [cta][16 tiles][4]: mma start, mma issued, epilogue start, end
 };
+
+__device__ __forceinline__ void trace_mark(const GemmParams& p, int it, int kind) {
+    if (p.experiment == 5 && it < 16) p.trace[(blockIdx.x * 16 + it) * 4 + kind] = clock64();
+}
 
 template <int BN>
 constexpr size_t gemm_smem_bytes() {
     return 1024 + static_cast<size_t>(kStages) * (kBM * kBK * 2 + BN * kBK * 2) + 256 +
-           kRopeSmemPairs * 8;
+           kRopeSmemPairs * 8 + kEpiWarps * kEpiStageBytes;
 }
 
 
@@ -78,7 +87,7 @@ __host__ __device__ inline int rope_smem_pairs(const RopeLaunch& l) {
 }
 
 // every thread of the CTA: copy the slice (before the CTA-wide barrier that follows setup)
-__device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, float2* st) {
+__device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, uint32_t st) {
     const RopeSmem r = rope_smem_layout(l);
     const int nt = r.n_t * l.pairs[0];
     const int total = rope_smem_pairs(l);
@@ -90,32 +99,70 @@ __device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, float2* s
             v = __ldg(&l.tab[1][i - r.off_h]);
         else
             v = __ldg(&l.tab[2][i - r.off_w]);
-        st[i] = v;
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(st + 8u * i), "f"(v.x), "f"(v.y)
+                     : "memory");
     }
 }
 
-// a token row's three band rows in the staged tables (computed once per row per tile)
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+// a token row's three band rows in the staged tables (shared-memory byte addresses, computed
+// once per row per tile; explicit ld.shared keeps the reads off the generic/long-scoreboard path)
 struct RopeRow {
-    const float2* t;  // T band row of its frame
-    const float2* h;  // H band row
-    const float2* w;  // W band row
+    uint32_t t;  // T band row of its frame
+    uint32_t h;  // H band row
+    uint32_t w;  // W band row
     bool valid;
 };
 
-__device__ __forceinline__ RopeRow rope_row(const RopeLaunch& l, const RopeSmem& r,
-                                            const float2* st, int row) {
+__device__ __forceinline__ RopeRow rope_row(const RopeLaunch& l, const RopeSmem& r, uint32_t st,
+                                            int row) {
     int t, h, w;
     rope_thw(l, row, t, h, w);
-    return {st + (t - r.t_lo) * l.pairs[0], st + r.off_h + h * l.pairs[1],
-            st + r.off_w + w * l.pairs[2], true};
+    return {st + 8u * static_cast<uint32_t>((t - r.t_lo) * l.pairs[0]),
+            st + 8u * static_cast<uint32_t>(r.off_h + h * l.pairs[1]),
+            st + 8u * static_cast<uint32_t>(r.off_w + w * l.pairs[2]), true};
 }
 
-// epi_mode 2: a 32-column slice of one head of q, k or v for token `row` at (t, h, w):
-// q/k pairs (2j, 2j+1) rotate in fp32 (rope.cpp:106-126) before the single bf16 rounding,
-// then the slice is stored into its head group's q slab / every KV-ring copy (the pack of
-// the fused all-to-all, as K3 does)
-__device__ __forceinline__ void rope_pack_chunk(const RopeLaunch& l, const RopeRow& rr, int row,
-                                                int col0, float (&f)[32]) {
+// epi_mode 2: RoPE of a 32-column slice of one head of q or k for token `row` at (t, h, w):
+// pairs (2j, 2j+1) rotate in fp32 (rope.cpp:106-126) before the single bf16 rounding. All 16
+// (cos, sin) pairs are loaded before any math (branch-free band selection), so the shared-
+// memory latency is paid once per slice, not once per pair.
+__device__ __forceinline__ void rope_rotate_chunk(const RopeLaunch& l, const RopeRow& rr, int d0,
+                                                  float (&f)[32]) {
+    const int p0 = l.pairs[0], p01 = l.pairs[0] + l.pairs[1];
+    float2 cs[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int j = d0 / 2 + e;
+        const uint32_t at = rr.t + 8u * j, ah = rr.h + 8u * (j - p0), aw = rr.w + 8u * (j - p01);
+        const uint32_t a = j < p0 ? at : (j < p01 ? ah : aw);
+        cs[e] = lds_f2(a);
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const float x0 = f[2 * e], x1 = f[2 * e + 1];
+        f[2 * e] = x0 * cs[e].x - x1 * cs[e].y;
+        f[2 * e + 1] = x0 * cs[e].y + x1 * cs[e].x;
+    }
+}
+
+// Destinations of a 32-column slice (warp-uniform): column `col0` of row 0. epi_mode 2 is the
+// pack of the fused all-to-all, as K3 does: q slices go to their head group's q slab, k / v
+// slices to every KV-ring copy of the group.
+struct ChunkDst {
+    int which, g, n;  // which: 0 q, 1 k, 2 v (epi_mode 2); -1 the plain output
+    int d0;           // first head-dim element of the slice (epi_mode 2)
+    int64_t off, stride;
+};
+
+__device__ __forceinline__ ChunkDst chunk_dst(const GemmParams& p, int col0) {
+    if (p.epi_mode != 2) return {-1, 0, 1, 0, col0, p.ldo};
+    const RopeLaunch& l = p.rope;
     const int C = l.heads * l.head_dim;
     const int which = col0 / C;
     const int c = col0 - which * C;
@@ -123,50 +170,33 @@ __device__ __forceinline__ void rope_pack_chunk(const RopeLaunch& l, const RopeR
     const int d0 = c - head * l.head_dim;
     const int hpg = l.heads / l.groups;
     const int g = head / hpg;
-    const int64_t off =
-        static_cast<int64_t>(row) * l.dst_row_stride + (head - g * hpg) * l.head_dim + d0;
-    if (which < 2 && rr.valid) {
-        const int p0 = l.pairs[0], p01 = l.pairs[0] + l.pairs[1];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int j = d0 / 2 + e;  // warp-uniform band selection
-            const float2 cs = j < p0 ? rr.t[j] : (j < p01 ? rr.h[j - p0] : rr.w[j - p01]);
-            const float a = f[2 * e], b = f[2 * e + 1];
-            f[2 * e] = a * cs.x - b * cs.y;
-            f[2 * e + 1] = a * cs.y + b * cs.x;
-        }
-    }
-    uint4 v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        v[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
-                          pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
-    if (which == 0) {
-        uint4* d = reinterpret_cast<uint4*>(l.dst.q[g] + off);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) d[q] = v[q];
-    } else {
-        for (int cp = 0; cp < l.dst.copies; ++cp) {
-            uint4* d = reinterpret_cast<uint4*>((which == 1 ? l.dst.k[g][cp] : l.dst.v[g][cp]) + off);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[q] = v[q];
-        }
-    }
+    return {which, g, which == 0 ? 1 : l.dst.copies, d0, (head - g * hpg) * l.head_dim + d0,
+            l.dst_row_stride};
 }
 
-// one 32-column slice of an accumulator row -> (gate, residual | rope + pack) -> bf16 -> global
-__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0,
-                                               const uint32_t (&r)[32],
+__device__ __forceinline__ bf16* chunk_base(const GemmParams& p, const ChunkDst& d, int cp) {
+    bf16* b = d.which < 0 ? p.out
+              : d.which == 0 ? p.rope.dst.q[d.g]
+              : d.which == 1 ? p.rope.dst.k[d.g][cp] : p.rope.dst.v[d.g][cp];
+    return b + d.off;
+}
+
+// One 32-column slice of the warp's 32 accumulator rows (lane = row) -> (gate, residual |
+// RoPE) -> bf16 -> global. The slice is transposed through the warp's 2 KB of shared memory
+// (16-byte units XOR-swizzled, conflict-free both ways) so each store instruction writes
+// 8 rows x 64 contiguous bytes (full sectors) instead of 32 rows x 16 bytes.
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, int lane, int col0,
+                                               const uint32_t (&r)[32], uint32_t stage,
                                                const RopeRow& rr = RopeRow{}) {
-    if (row >= p.M || col0 >= p.N) return;
+    if (col0 >= p.N) return;  // warp-uniform
+    const int row = row0 + lane;
     float f[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+    const ChunkDst d = chunk_dst(p, col0);
     if (p.epi_mode == 2) {
-        rope_pack_chunk(p.rope, rr, row, col0, f);
-        return;
-    }
-    if (p.epi_mode == 1) {
+        if (d.which < 2 && rr.valid) rope_rotate_chunk(p.rope, rr, d.d0, f);
+    } else if (p.epi_mode == 1 && row < p.M) {
         const uint4* res = reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -174,21 +204,40 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
             const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                float2 rr = unpack_bf16x2(rw[e]);
+                float2 rs = unpack_bf16x2(rw[e]);
                 const int j = q * 8 + e * 2;
-                f[j] = rr.x + p.gate[col0 + j] * f[j];
-                f[j + 1] = rr.y + p.gate[col0 + j + 1] * f[j + 1];
+                f[j] = rs.x + p.gate[col0 + j] * f[j];
+                f[j + 1] = rs.y + p.gate[col0 + j + 1] * f[j + 1];
             }
         }
     }
-    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(row) * p.ldo + col0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]),
-                            pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
-                            pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]),
-                            pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+        const uint32_t a = stage + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                     "r"(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1])), "r"(pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3])),
+                     "r"(pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5])), "r"(pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]))
+                     : "memory");
     }
+    __syncwarp();
+    const int u = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr_ = (lane >> 2) + 8 * i;
+        uint4 w;
+        const uint32_t a = stage + rr_ * 64 + ((u ^ ((rr_ >> 1) & 3)) << 4);
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(a)
+                     : "memory");
+        const int grow = row0 + rr_;
+        if (grow < p.M) {
+            for (int cp = 0; cp < d.n; ++cp)
+                *reinterpret_cast<uint4*>(chunk_base(p, d, cp) + static_cast<int64_t>(grow) * d.stride +
+                                          u * 8) = w;
+        }
+    }
+    __syncwarp();  // the slice's shared memory is read before the next slice overwrites it
 }
 
 template <int BN>
@@ -200,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     constexpr uint32_t kABytes = kBM * kBK * 2;
     constexpr uint32_t kBBytes = BN * kBK * 2;
-    constexpr uint32_t kTmemCols = 2 * BN;
+    constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 x BN
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kABytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
@@ -208,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float2* s_rope = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(full) + 256);
+    const uint32_t s_rope = smem_u32(reinterpret_cast<uint8_t*>(full) + 256);
+    const uint32_t s_stage = s_rope + kRopeSmemPairs * 8 + (threadIdx.x / 32 - 4) * kEpiStageBytes;
     const RopeSmem rope_l = p.epi_mode == 2 ? rope_smem_layout(p.rope) : RopeSmem{};
 
     const int warp = threadIdx.x / 32;
@@ -225,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiWarps * 32);
+            mbar_init(&tempty[a], kEpiWarps);  // one arrival per epilogue warp
         }
         fence_mbar_init();
     }
@@ -316,10 +366,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t r[32];
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
-                epilogue_chunk(p, row, n0 + c * 32, r, rr);
+                epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, rr);
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
         }
     }
     __syncthreads();
@@ -346,7 +397,7 @@ constexpr int kPairStages = 6;
 template <int BN>
 constexpr size_t gemm_pair_smem_bytes() {
     return 1024 + static_cast<size_t>(kPairStages) * (128 * kBK * 2 + (BN / 2) * kBK * 2) + 256 +
-           kRopeSmemPairs * 8;
+           kRopeSmemPairs * 8 + kEpiWarps * kEpiStageBytes;
 }
 
 template <int BN>
@@ -358,7 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     constexpr uint32_t kABytes = 128 * kBK * 2;
     constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
-    constexpr uint32_t kTmemCols = 2 * BN;
+    constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 x BN
     uint8_t* sA = smem;
     uint8_t* sB = smem + kPairStages * kABytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + kPairStages * kBBytes);
@@ -366,7 +417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + kPairStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float2* s_rope = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(full) + 256);
+    const uint32_t s_rope = smem_u32(reinterpret_cast<uint8_t*>(full) + 256);
+    const uint32_t s_stage = s_rope + kRopeSmemPairs * 8 + (threadIdx.x / 32 - 4) * kEpiStageBytes;
     const RopeSmem rope_l = p.epi_mode == 2 ? rope_smem_layout(p.rope) : RopeSmem{};
 
     const int warp = threadIdx.x / 32;
@@ -387,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * kEpiWarps * 32);
+            mbar_init(&tempty[a], 2 * kEpiWarps);  // one per epilogue warp of both CTAs
         }
         fence_mbar_init();
     }
@@ -439,6 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t aphase = (it >> 1) & 1;
                 mbar_wait_cluster(&tempty[acc], aphase ^ 1);
                 tc_fence_after();
+                if (issuer) trace_mark(p, it, 0);
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&full[stage], phase);
@@ -461,6 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (issuer) umma_commit_pair(&tfull[acc], 0x3);
+                if (issuer) trace_mark(p, it, 1);
                 __syncwarp();
             }
         }
@@ -475,6 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int n0 = (tile / p.num_m_tiles) * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
+            if (warp == 4 && lane == 0) trace_mark(p, it, 2);
             const int row = m0 + ew * 32 + lane;
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
@@ -485,10 +540,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 uint32_t r[32];
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
-                epilogue_chunk(p, row, n0 + c * 32, r, rr);
+                epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, rr);
             }
+            // the warp's TMEM reads are complete (wait::ld); no global-store ordering is
+            // needed, so the remote arrival is relaxed (no per-thread MEMBAR.GPU)
             tc_fence_before();
-            mbar_arrive_leader(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader_relaxed(&tempty[acc]);
+            if (warp == 4 && lane == 0) trace_mark(p, it, 3);
         }
     }
     tc_fence_before();
@@ -527,6 +586,30 @@ void set_smem_attr() {
 
 }  // namespace
 
+namespace {
+// tuning / test override of the planner: SPX_GEMM_VARIANT=0..4 (index into cands below) at
+// load time, or spx_debug_set_gemm_variant at run time; -1 = modelled choice
+std::atomic<int> g_forced_variant{[] {
+    const char* e = std::getenv("SPX_GEMM_VARIANT");
+    return e ? std::atoi(e) : -1;
+}()};
+}  // namespace
+
+namespace {
+long long* g_trace = nullptr;
+}
+long long* gemm_trace_buffer() {
+    if (!g_trace) {
+        SPX_CUDA(cudaMalloc(&g_trace, 1024 * 16 * 4 * sizeof(long long)));
+        SPX_CUDA(cudaMemset(g_trace, 0, 1024 * 16 * 4 * sizeof(long long)));
+    }
+    return g_trace;
+}
+
+int gemm_forced_variant() { return g_forced_variant.load(std::memory_order_relaxed); }
+void gemm_force_variant(int v) { g_forced_variant.store(v, std::memory_order_relaxed); }
+int gemm_num_variants() { return 5; }
+
 void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
     require(ops.M > 0 && ops.N > 0 && ops.K > 0, SPX_ERR_SHAPE, "gemm: empty problem");
     require(ops.K % kBK == 0, SPX_ERR_SHAPE, "gemm: K must be a multiple of 64");
@@ -537,19 +620,17 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
             SPX_ERR_ALIGNMENT, "gemm: output must be 16-byte aligned");
     plan->ops = ops;
     // Variant: modelled time = waves x per-SM tile work / efficiency, over
-    //   pair (cta_group::2) 256 x {256, 128} tiles and single-CTA 128 x {256, 128} tiles.
+    //   pair (cta_group::2) 256 x {256, 128} tiles and single-CTA 128 x {256, 192, 128} tiles.
     // The single-CTA kernels stream 1.5-2x the operand bytes per MMA cycle (L2 -> SM bound).
     struct Cand { bool pair; int bn; double eff; };
     // efficiencies measured on B200 (tools/kbench.py gemm, K = 1536): pair-256 1358 TFLOP/s
-    // at 4680x4608, pair-128 908, single-256 1237, single-128 1077
+    // at 4680x4608, pair-128 908, single-256 1237, single-128 1077; single-192 estimated
+    // between them (its 2-wave fit of the 4680x1536 O-projection is what it is for)
     static const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.65}, {false, 256, 0.88},
-                                 {false, 128, 0.72}};
-    static const int forced = [] {  // tuning override: SPX_GEMM_VARIANT=0..3 (index above)
-        const char* e = std::getenv("SPX_GEMM_VARIANT");
-        return e ? std::atoi(e) : -1;
-    }();
+                                 {false, 128, 0.72}, {false, 192, 0.85}};
+    const int forced = gemm_forced_variant();
     double best = 1e30;
-    for (int ci = 0; ci < 4; ++ci) {
+    for (int ci = 0; ci < 5; ++ci) {
         const Cand& c = cands[ci];
         if (ops.N % 32 != 0) continue;
         const int64_t bm = c.pair ? 256 : 128;
@@ -623,6 +704,7 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
         return e ? std::atoi(e) : 0;
     }();
     p.experiment = experiment;
+    if (experiment == 5) p.trace = gemm_trace_buffer();
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         gemm_bf16_tn_pair_kernel<256><<<plan.grid, kThreads, gemm_pair_smem_bytes<256>(), stream>>>(
@@ -630,6 +712,10 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     } else if (plan.pair) {
         set_pair_smem_attr<128>();
         gemm_bf16_tn_pair_kernel<128><<<plan.grid, kThreads, gemm_pair_smem_bytes<128>(), stream>>>(
+            plan.map_a, plan.map_b, p);
+    } else if (plan.bn == 192) {
+        set_smem_attr<192>();
+        gemm_bf16_tn_kernel<192><<<plan.grid, kThreads, gemm_smem_bytes<192>(), stream>>>(
             plan.map_a, plan.map_b, p);
     } else if (plan.bn == 256) {
         set_smem_attr<256>();

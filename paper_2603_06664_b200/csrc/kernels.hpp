@@ -51,6 +51,12 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count);
 // rotate-and-pack without its qkv round trip); requires gemm_rope_fusable()
 void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope = nullptr);
 bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope);
+// planner override (tests / tuning): -1 = modelled choice, else a tile variant index
+int gemm_forced_variant();
+void gemm_force_variant(int v);
+int gemm_num_variants();
+// SPX_GEMM_EXPERIMENT=5: the pair kernel's per-tile clock64 timeline ([cta][16][4], device)
+long long* gemm_trace_buffer();
 
 // ---------------------------------------------------------------------------------------
 // K6: chunk-causal flash attention, tcgen05/TMEM, TMA-fed.

@@ -17,6 +17,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;
     asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
@@ -214,6 +220,13 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
 // arrive on the leader CTA's mbarrier (same offset) from either CTA of the pair
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                     leader_addr(bar))
+                 : "memory");
+}
+// relaxed variant: no release fence (the arriving thread's prior memory writes need not be
+// ordered, e.g. an epilogue warp handing a TMEM accumulator back after tcgen05.wait::ld)
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                      leader_addr(bar))
                  : "memory");
 }

@@ -56,6 +56,29 @@ def test_project_tokens_matches_fp32(cuda, M, K, N):
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
+@pytest.mark.parametrize("variant", range(5))
+@pytest.mark.parametrize("M,K,N", [(300, 128, 1600), (4680, 1536, 1536), (585, 1536, 4608)])
+def test_project_tokens_every_tile_variant(cuda, variant, M, K, N):
+    """each tile variant (pair 256x{256,128}, single 128x{256,128,192}) on ragged M and an N
+    that no tile width divides, forced through the planner override"""
+    torch = _t()
+    g = torch.Generator(device="cuda").manual_seed(M + N + variant)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    y = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+    _check(_lib().spx_debug_set_gemm_variant(variant))
+    try:
+        _check(_lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(), M, K, N,
+                                         _stream()))
+        torch.cuda.synchronize()
+    finally:
+        _check(_lib().spx_debug_set_gemm_variant(-1))
+    ref = x.float() @ w.float().t()
+    assert bool(torch.isfinite(y.float()).all())
+    assert rel_l2(y.float(), ref) < 4e-3
+    assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
+
+
 @pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),
                                         (4680, 4680, 12, 128), (1170, 9360, 3, 128)])
 def test_attention_matches_fp32(cuda, sq, skv, H, D):
