@@ -144,10 +144,14 @@ spx_status spx_kv_ring_attention(const spx_kv_ring* ring, const void* q, void* o
 
 /* ---------------------------------------------------------------------------------------
  * Communicator (CommWorld: proj/include/spattn/collectives.hpp:39-113,
- * proj/src/collectives.cpp). Two transports behind one interface:
+ * proj/src/collectives.cpp). Three transports behind one interface:
  *   LOCAL : all ranks live in this process (one stream each; devices may repeat, i.e.
  *           several ranks can share one GPU); chunks move by direct (peer) stores.
  *   NCCL  : one rank per process, grouped ncclSend/ncclRecv over NVLink.
+ *   PEER  : one rank per process; the engine's exchange buffers are shared through CUDA
+ *           IPC, the producing kernels store straight into the peer's buffers (NVLink P2P,
+ *           or the same device) and device-side flags order the ranks (engine only: the
+ *           standalone collectives below need LOCAL or NCCL).
  * Buffers passed to the collectives are indexed by LOCAL rank (1 entry for NCCL).
  * ------------------------------------------------------------------------------------- */
 typedef struct spx_world spx_world;
@@ -161,11 +165,14 @@ typedef struct spx_comm_stats {
 } spx_comm_stats; /* CommStats, collectives.hpp:20-33 */
 
 enum { SPX_AXIS_BATCH = 0, SPX_AXIS_SEQ = 1, SPX_AXIS_HEADS = 2, SPX_AXIS_HEAD_DIM = 3 };
-enum { SPX_TRANSPORT_LOCAL = 0, SPX_TRANSPORT_NCCL = 1 };
+enum { SPX_TRANSPORT_LOCAL = 0, SPX_TRANSPORT_NCCL = 1, SPX_TRANSPORT_PEER = 2 };
 
 /* devices == NULL -> every rank on the current device */
 spx_status spx_world_create_local(int world_size, const int* devices, spx_world** out);
 spx_status spx_nccl_get_unique_id(uint8_t out_id[128]);
+/* PEER transport: rank `rank` of `world_size`, one per process, on `device`. An engine made
+ * on it exchanges buffer handles once (spx_engine_ipc_export / _import) before running. */
+spx_status spx_world_create_peer(int rank, int world_size, int device, spx_world** out);
 spx_status spx_world_create_nccl(int rank, int world_size, const uint8_t id[128], int device,
                                  spx_world** out);
 void spx_world_destroy(spx_world* world);
@@ -298,6 +305,11 @@ spx_status spx_engine_reset_stage_times(spx_engine* engine);
 /* CUDA-event stage timing for subsequent calls: 0 off, 1 every stage, 2 attention only */
 spx_status spx_engine_set_profile(spx_engine* engine, int32_t on);
 spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
+/* PEER transport: this rank's exchange buffers as CUDA IPC handles (an opaque blob of
+ * *bytes <= capacity; query the size with out == NULL). Every rank gathers all blobs in rank
+ * order (any host channel: torch.distributed, MPI, a file) and passes them to _import. */
+spx_status spx_engine_ipc_export(spx_engine* engine, void* out, int64_t capacity, int64_t* bytes);
+spx_status spx_engine_ipc_import(spx_engine* engine, const void* blobs, int64_t bytes_per_rank);
 
 /* ---------------------------------------------------------------------------------------
  * Debug / GPU-oracle kernels (fp32 SIMT; tests only)

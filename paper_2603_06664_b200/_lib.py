@@ -164,6 +164,9 @@ _SIGS = [
     ("spx_engine_reset_stage_times", c_int, [c_void_p]),
     ("spx_engine_set_profile", c_int, [c_void_p, c_int32]),
     ("spx_engine_stats", c_int, [c_void_p, POINTER(CommStats)]),
+    ("spx_world_create_peer", c_int, [c_int, c_int, c_int, c_void_p]),
+    ("spx_engine_ipc_export", c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("spx_engine_ipc_import", c_int, [c_void_p, c_void_p, c_int64]),
     ("spx_debug_set_gemm_variant", c_int, [c_int32]),
     ("spx_debug_gemm_trace", c_int, [c_void_p, c_int64]),
     ("spx_debug_naive_gemm", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),

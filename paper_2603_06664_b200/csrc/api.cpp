@@ -542,6 +542,16 @@ spx_status spx_world_create_nccl(int rank, int world_size, const uint8_t id[128]
     });
 }
 
+spx_status spx_world_create_peer(int rank, int world_size, int device, spx_world** out) {
+    return guarded([&] {
+        require_ptr(out, "out");
+        *out = nullptr;
+        auto w = std::make_unique<spx_world>();
+        w->w = std::make_unique<World>(rank, world_size, device);
+        *out = w.release();
+    });
+}
+
 void spx_world_destroy(spx_world* world) { delete world; }
 
 spx_status spx_world_info(const spx_world* world, int32_t out[4]) {
@@ -811,6 +821,26 @@ spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out) {
     return guarded([&] {
         require(engine && out, SPX_ERR_CONFIG, "null argument");
         *out = engine->e->stats();
+    });
+}
+
+spx_status spx_engine_ipc_export(spx_engine* engine, void* out, int64_t capacity, int64_t* bytes) {
+    return guarded([&] {
+        require(engine && bytes, SPX_ERR_CONFIG, "null argument");
+        const std::vector<uint8_t> blob = engine->e->ipc_export();
+        *bytes = static_cast<int64_t>(blob.size());
+        if (out) {
+            require(capacity >= *bytes, SPX_ERR_SHAPE, "ipc_export: buffer too small");
+            std::memcpy(out, blob.data(), blob.size());
+        }
+    });
+}
+
+spx_status spx_engine_ipc_import(spx_engine* engine, const void* blobs, int64_t bytes_per_rank) {
+    return guarded([&] {
+        require(engine && blobs && bytes_per_rank > 0, SPX_ERR_CONFIG, "null argument");
+        engine->e->ipc_import(static_cast<const uint8_t*>(blobs),
+                              static_cast<size_t>(bytes_per_rank));
     });
 }
 

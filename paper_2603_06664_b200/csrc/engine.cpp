@@ -76,6 +76,11 @@ void Engine::validate(const spx_engine_config& c, int world_size) {
 
 Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_(cfg) {
     validate(cfg, world->size());
+    if (world->transport() == SPX_TRANSPORT_PEER) {
+        require(cfg.ablation == SPX_ABLATION_ALL, SPX_ERR_UNSUPPORTED,
+                "the PEER transport runs the optimized schedule only (ablation = ALL)");
+        require(world->size() <= kMaxPeers, SPX_ERR_UNSUPPORTED, "PEER transport: at most 8 ranks");
+    }
     F_ = cfg.frames;
     Hg_ = cfg.grid_h;
     Wg_ = cfg.grid_w;
@@ -107,6 +112,11 @@ Engine::~Engine() {
     for (RankState& rs : ranks_) {
         cudaSetDevice(rs.device);
         cudaStreamSynchronize(rs.stream);
+    }
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (RankState& rs : ranks_) {
+        cudaSetDevice(rs.device);
+        cudaStreamSynchronize(rs.stream);
         for (auto& ring : rs.rings) ring.release();
         for (void* p : rs.allocations) cudaFree(p);
         if (rs.ev_k3) cudaEventDestroy(rs.ev_k3);
@@ -126,6 +136,119 @@ Engine::~Engine() {
 }
 
 int Engine::local_of(int rank) const { return world_->local_index(rank); }
+
+bf16* Engine::q_recv_of(int rank) const {
+    if (world_->transport() == SPX_TRANSPORT_PEER) return peers_[static_cast<size_t>(rank)].q_recv;
+    return ranks_[static_cast<size_t>(local_of(rank))].q_recv;
+}
+
+bf16* Engine::o_recv_of(int rank) const {
+    if (world_->transport() == SPX_TRANSPORT_PEER) return peers_[static_cast<size_t>(rank)].o_recv;
+    return ranks_[static_cast<size_t>(local_of(rank))].o_recv;
+}
+
+bf16* Engine::ring_k_of(int rank, int64_t layer) const {
+    if (world_->transport() == SPX_TRANSPORT_PEER)
+        return peers_[static_cast<size_t>(rank)].ring_k[static_cast<size_t>(layer)];
+    return ranks_[static_cast<size_t>(local_of(rank))].rings[static_cast<size_t>(layer)].k;
+}
+
+bf16* Engine::ring_v_of(int rank, int64_t layer) const {
+    if (world_->transport() == SPX_TRANSPORT_PEER)
+        return peers_[static_cast<size_t>(rank)].ring_v[static_cast<size_t>(layer)];
+    return ranks_[static_cast<size_t>(local_of(rank))].rings[static_cast<size_t>(layer)].v;
+}
+
+// ---- PEER transport: buffer handles and the device-side rank barrier ----
+namespace {
+constexpr uint32_t kIpcMagic = 0x53505849u;  // "SPXI"
+struct IpcHeader {
+    uint32_t magic;
+    int32_t rank, world, layers;
+    int64_t device_bytes;  // q_recv + o_recv + ring sizes, a shape cross-check
+    int64_t handles;
+};
+}  // namespace
+
+std::vector<uint8_t> Engine::ipc_export() const {
+    require(world_->transport() == SPX_TRANSPORT_PEER, SPX_ERR_CONFIG,
+            "ipc_export needs the PEER transport");
+    const RankState& rs = ranks_[0];
+    std::vector<const void*> ptrs = {rs.q_recv, rs.o_recv, rs.flags};
+    for (const auto& ring : rs.rings) ptrs.push_back(ring.k);
+    for (const auto& ring : rs.rings) ptrs.push_back(ring.v);
+    IpcHeader h{kIpcMagic, rs.rank, static_cast<int32_t>(P_), static_cast<int32_t>(cfg_.layers),
+                (Lq_ * Hl_ * D_ + G_ * Lp_ * Hl_ * D_ + 2 * cfg_.layers * rs.rings[0].rows() * Hl_ * D_),
+                static_cast<int64_t>(ptrs.size())};
+    std::vector<uint8_t> blob(sizeof(h) + ptrs.size() * sizeof(cudaIpcMemHandle_t));
+    std::memcpy(blob.data(), &h, sizeof(h));
+    SPX_CUDA(cudaSetDevice(rs.device));
+    for (size_t i = 0; i < ptrs.size(); ++i) {
+        cudaIpcMemHandle_t mh;
+        SPX_CUDA(cudaIpcGetMemHandle(&mh, const_cast<void*>(ptrs[i])));
+        std::memcpy(blob.data() + sizeof(h) + i * sizeof(mh), &mh, sizeof(mh));
+    }
+    return blob;
+}
+
+void Engine::ipc_import(const uint8_t* blobs, size_t per_rank) {
+    require(world_->transport() == SPX_TRANSPORT_PEER, SPX_ERR_CONFIG,
+            "ipc_import needs the PEER transport");
+    require(!peers_ready_, SPX_ERR_CONFIG, "ipc_import: peers are already mapped");
+    const RankState& rs = ranks_[0];
+    const std::vector<uint8_t> mine = ipc_export();
+    require(blobs && per_rank == mine.size(), SPX_ERR_SHAPE,
+            "ipc_import: blob size " + std::to_string(per_rank) + ", expected " +
+                std::to_string(mine.size()));
+    SPX_CUDA(cudaSetDevice(rs.device));
+    peers_.assign(static_cast<size_t>(P_), PeerView{});
+    for (int r = 0; r < P_; ++r) {
+        const uint8_t* b = blobs + static_cast<size_t>(r) * per_rank;
+        IpcHeader h;
+        std::memcpy(&h, b, sizeof(h));
+        IpcHeader m;
+        std::memcpy(&m, mine.data(), sizeof(m));
+        require(h.magic == kIpcMagic && h.rank == r && h.world == P_ && h.layers == cfg_.layers &&
+                    h.device_bytes == m.device_bytes && h.handles == m.handles,
+                SPX_ERR_COLLECTIVE,
+                "ipc_import: blob " + std::to_string(r) + " is not rank " + std::to_string(r) +
+                    " of an engine with the same configuration");
+        PeerView& v = peers_[static_cast<size_t>(r)];
+        if (r == rs.rank) {
+            v.q_recv = rs.q_recv;
+            v.o_recv = rs.o_recv;
+            v.flags = rs.flags;
+            for (const auto& ring : rs.rings) {
+                v.ring_k.push_back(ring.k);
+                v.ring_v.push_back(ring.v);
+            }
+            continue;
+        }
+        auto open = [&](int64_t i) {
+            cudaIpcMemHandle_t mh;
+            std::memcpy(&mh, b + sizeof(h) + static_cast<size_t>(i) * sizeof(mh), sizeof(mh));
+            void* p = nullptr;
+            SPX_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened_.push_back(p);
+            return p;
+        };
+        v.q_recv = static_cast<bf16*>(open(0));
+        v.o_recv = static_cast<bf16*>(open(1));
+        v.flags = static_cast<uint64_t*>(open(2));
+        for (int64_t l = 0; l < cfg_.layers; ++l) v.ring_k.push_back(static_cast<bf16*>(open(3 + l)));
+        for (int64_t l = 0; l < cfg_.layers; ++l)
+            v.ring_v.push_back(static_cast<bf16*>(open(3 + cfg_.layers + l)));
+    }
+    peers_ready_ = true;
+}
+
+void Engine::peer_barrier(RankState& rs, int slot) {
+    const uint64_t e = ++epoch_[slot];
+    PeerFlags f{};
+    for (int r = 0; r < P_; ++r) f.rank_flags[r] = peers_[static_cast<size_t>(r)].flags;
+    peer_signal_run(f, static_cast<int>(P_), rs.rank, slot, e, rs.stream);
+    peer_wait_run(rs.flags, static_cast<int>(P_), slot, e, rs.stream);
+}
 
 void Engine::allocate() {
     const bool nccl = world_->transport() == SPX_TRANSPORT_NCCL;
@@ -171,6 +294,8 @@ void Engine::allocate() {
                               Wg_ * table_->pairs(2);
             rs.tab_scratch = dev_alloc<float2>(rs, static_cast<size_t>(n));
         }
+        if (world_->transport() == SPX_TRANSPORT_PEER)
+            rs.flags = dev_alloc<uint64_t>(rs, static_cast<size_t>(kPeerSlots * P_));
         if (nccl) {
             rs.q_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
             rs.k_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
@@ -348,7 +473,8 @@ void Engine::begin_block(int64_t block_index) {
 }
 
 RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const {
-    const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
+    // LOCAL and PEER store straight into the destination rank's buffers
+    const bool direct = world_->transport() != SPX_TRANSPORT_NCCL;
     RopeLaunch rl{};
     rl.in = rs.qkv;
     rl.in_row_stride = 3 * C_;
@@ -383,18 +509,17 @@ RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start
     const int64_t row_elems = Hl_ * D_;
     for (int64_t g = 0; g < G_; ++g) {
         const int d = static_cast<int>(rs.p * G_ + g);
-        if (local) {
-            rl.dst.q[g] = ranks_[static_cast<size_t>(local_of(d))].q_recv + (rs.rank % G_) * slab;
+        if (direct) {
+            rl.dst.q[g] = q_recv_of(d) + (rs.rank % G_) * slab;
         } else {
             rl.dst.q[g] = d == rs.rank ? rs.q_recv + (rs.rank % G_) * slab : rs.q_send + g * slab;
         }
         for (int64_t c = 0; c < S_; ++c) {
             const int dk = static_cast<int>(c * G_ + g);
             const int64_t row0 = block_base_row_ + static_cast<int64_t>(rs.rank) * Lp_;
-            if (local || dk == rs.rank) {
-                const RankState& dst = local ? ranks_[static_cast<size_t>(local_of(dk))] : rs;
-                rl.dst.k[g][c] = dst.rings[static_cast<size_t>(layer)].k + row0 * row_elems;
-                rl.dst.v[g][c] = dst.rings[static_cast<size_t>(layer)].v + row0 * row_elems;
+            if (direct || dk == rs.rank) {
+                rl.dst.k[g][c] = ring_k_of(dk, layer) + row0 * row_elems;
+                rl.dst.v[g][c] = ring_v_of(dk, layer) + row0 * row_elems;
             } else {
                 rl.dst.k[g][c] = rs.k_send + g * slab;
                 rl.dst.v[g][c] = rs.v_send + g * slab;
@@ -411,6 +536,10 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
                        const std::vector<const GemmPlan*>& oproj) {
     require(have_block_, SPX_ERR_EMPTY_CACHE, "layer call before any block was registered");
     const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
+    const bool peer = world_->transport() == SPX_TRANSPORT_PEER;
+    const bool nccl = world_->transport() == SPX_TRANSPORT_NCCL;
+    require(!peer || peers_ready_, SPX_ERR_COLLECTIVE,
+            "PEER transport: exchange buffer handles first (spx_engine_ipc_import)");
     const int nl = static_cast<int>(ranks_.size());
     const int64_t slab = Lp_ * Hl_ * D_;
 
@@ -488,7 +617,10 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
                     if (lj != li)
                         SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(lj)].ev_k3, 0));
             }
-        } else if (P_ > 1) {
+        } else if (peer && P_ > 1) {
+            // K3 stored into the peers' buffers; every rank's stores land before attention
+            peer_barrier(ranks_[0], 0);
+        } else if (nccl && P_ > 1) {
             // one NCCL group == one round: the plan's sends and receives (exchange_plan.cpp)
             RankState& rs = ranks_[0];
             SPX_CUDA(cudaSetDevice(rs.device));
@@ -563,8 +695,8 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         attn_set_segments(&plan, seg_start_, seg_len_, num_segs_);
         for (int64_t c = 0; c < G_; ++c) {
             const int i = static_cast<int>(rs.p * G_ + c);
-            if (local) {
-                plan.ops.out_base[c] = ranks_[static_cast<size_t>(local_of(i))].o_recv + rs.g * slab;
+            if (local || peer) {
+                plan.ops.out_base[c] = o_recv_of(i) + rs.g * slab;
             } else {
                 plan.ops.out_base[c] = i == rs.rank ? rs.o_recv + rs.g * slab : rs.o_send + c * slab;
             }
@@ -584,7 +716,11 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
                     SPX_CUDA(cudaStreamWaitEvent(rs.stream, ranks_[static_cast<size_t>(ld)].ev_attn, 0));
             }
         }
-    } else if (P_ > 1) {
+    } else if (peer && P_ > 1) {
+        // attention stored o rows into their sources' slabs (and every rank is past reading
+        // this layer's q buffer, which the next call's K3 overwrites)
+        peer_barrier(ranks_[0], 1);
+    } else if (nccl && P_ > 1) {
         RankState& rs = ranks_[0];
         SPX_CUDA(cudaSetDevice(rs.device));
         run_plan(rs, layer, plan_out_exchange(part_, rs.rank));

@@ -61,6 +61,7 @@ struct RankState {
     bf16* gk = nullptr;               //   q, k, v of the whole block, (L, C)
     bf16* gv = nullptr;
     float2* tab_scratch = nullptr;    // ablation without precomputed freqs: per-call table
+    uint64_t* flags = nullptr;        // PEER: [kPeerSlots][P] barrier epochs (IPC-shared)
     std::vector<KvRingStorage> rings; // per layer
     std::vector<GemmPlan> qkv_plan;   // per layer, A = x[layer % 2]
     std::vector<GemmPlan> o_plan;     // per layer, out = x[(layer + 1) % 2]
@@ -108,6 +109,10 @@ class Engine {
     // 0 off, 1 every stage (six CUDA-event intervals per call), 2 attention launch only
     void set_profile(int level) { cfg_.profile = level; }
     spx_comm_stats stats() const { return world_->stats(); }
+    // PEER transport: CUDA IPC handles of this rank's exchange buffers, and the mapping of
+    // every peer's (blobs of all ranks in rank order)
+    std::vector<uint8_t> ipc_export() const;
+    void ipc_import(const uint8_t* blobs, size_t bytes_per_rank);
 
   private:
     void allocate();
@@ -119,6 +124,13 @@ class Engine {
     void run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>& plan);
     RopeLaunch rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const;
     int local_of(int rank) const;
+    // exchange destinations of a global rank: a local rank's buffers (LOCAL), or the IPC
+    // mapping of a peer's (PEER; the own rank maps to its own buffers)
+    bf16* q_recv_of(int rank) const;
+    bf16* o_recv_of(int rank) const;
+    bf16* ring_k_of(int rank, int64_t layer) const;
+    bf16* ring_v_of(int rank, int64_t layer) const;
+    void peer_barrier(RankState& rs, int slot);
 
     World* world_;
     spx_engine_config cfg_;
@@ -139,6 +151,17 @@ class Engine {
     // pinned staging for generated noise
     uint16_t* noise_pinned_ = nullptr;
     std::vector<double> noise_f64_;
+    // PEER transport
+    struct PeerView {
+        bf16* q_recv = nullptr;
+        bf16* o_recv = nullptr;
+        uint64_t* flags = nullptr;
+        std::vector<bf16*> ring_k, ring_v;
+    };
+    std::vector<PeerView> peers_;  // by global rank
+    std::vector<void*> ipc_opened_;
+    bool peers_ready_ = false;
+    uint64_t epoch_[2] = {0, 0};
     // profiling
     std::vector<StageEvents> pending_events_;
     std::vector<StageEvents> free_events_;

@@ -167,6 +167,21 @@ struct Box4 {
 void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
+// PEER transport: device-side rank barrier over IPC-mapped flag words. Each rank owns
+// flags[kPeerSlots][P] (uint64, epoch values). signal: after this stream's prior kernels
+// (whose stores may target peer memory), st.release.sys flags[slot][my_rank] = epoch in
+// every rank's array. wait: spin (ld.acquire.sys) until every entry of flags[slot] >= epoch.
+// ---------------------------------------------------------------------------------------
+constexpr int kPeerSlots = 2;
+constexpr int kMaxPeers = 8;
+struct PeerFlags {
+    uint64_t* rank_flags[kMaxPeers];  // every rank's flag array (this process's mapping)
+};
+void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint64_t epoch,
+                     cudaStream_t s);
+void peer_wait_run(uint64_t* my_flags, int world, int slot, uint64_t epoch, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------
 // Kd: naive fp32 SIMT reference kernels (GPU oracle at shapes the CPU oracle cannot reach).
 // ---------------------------------------------------------------------------------------
 void naive_gemm_run(const bf16* a, const bf16* b, float* out, int M, int N, int K,

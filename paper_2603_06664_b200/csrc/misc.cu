@@ -13,6 +13,30 @@ namespace spx {
 
 namespace {
 
+// PEER barrier (see kernels.hpp). One thread per rank.
+__global__ void peer_signal_kernel(PeerFlags f, int world, int my_rank, int slot, uint64_t epoch) {
+    const int r = threadIdx.x;
+    if (r >= world) return;
+    uint64_t* dst = f.rank_flags[r] + slot * world + my_rank;
+    // release at system scope: this stream's earlier kernels (stores into peer memory
+    // included) happen-before the flag as seen by the peer
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(uint64_t* flags, int world, int slot, uint64_t epoch) {
+    const int r = threadIdx.x;
+    if (r < world) {
+        const uint64_t* src = flags + slot * world + r;
+        uint64_t v = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
+            if (v >= epoch) break;
+            __nanosleep(64);
+        }
+    }
+    __syncwarp();
+}
+
 template <typename T>
 __global__ void copy_box_kernel(T* __restrict__ dst, const T* __restrict__ src, Box4 box,
                                 int64_t total) {
@@ -108,6 +132,19 @@ __global__ void naive_attention_kernel(const bf16* __restrict__ q, const bf16* _
 }
 
 }  // namespace
+
+void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint64_t epoch,
+                     cudaStream_t s) {
+    peer_signal_kernel<<<1, 32, 0, s>>>(f, world, my_rank, slot, epoch);
+    SPX_CUDA_LAUNCH();
+    count_launch();
+}
+
+void peer_wait_run(uint64_t* my_flags, int world, int slot, uint64_t epoch, cudaStream_t s) {
+    peer_wait_kernel<<<1, 32, 0, s>>>(my_flags, world, slot, epoch);
+    SPX_CUDA_LAUNCH();
+    count_launch();
+}
 
 void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s) {
     const int64_t total = box.ext[0] * box.ext[1] * box.ext[2] * box.ext[3];

@@ -166,6 +166,20 @@ World::World(int rank, int world_size, const uint8_t id[128], int device)
     comm_ = comm;
 }
 
+World::World(int rank, int world_size, int device) : world_size_(world_size) {
+    require(world_size >= 1, SPX_ERR_CONFIG, "world size must be >= 1");
+    require(rank >= 0 && rank < world_size, SPX_ERR_COLLECTIVE,
+            "rank " + std::to_string(rank) + " out of range");
+    transport_ = SPX_TRANSPORT_PEER;
+    local_.resize(1);
+    LocalRank& lr = local_[0];
+    lr.rank = rank;
+    lr.device = device;
+    SPX_CUDA(cudaSetDevice(device));
+    SPX_CUDA(cudaStreamCreateWithFlags(&lr.stream, cudaStreamNonBlocking));
+    SPX_CUDA(cudaEventCreateWithFlags(&lr.ev, cudaEventDisableTiming));
+}
+
 World::~World() {
     for (LocalRank& lr : local_) {
         cudaSetDevice(lr.device);
@@ -260,6 +274,8 @@ void World::reset_stats() {
 // ---------------------------------------------------------------------------------------
 void World::all_to_all(void* const* in, void* const* out, const int64_t shape[4],
                        int elem_bytes, int scatter_axis, int gather_axis, bool fused_member) {
+    require(transport_ != SPX_TRANSPORT_PEER, SPX_ERR_UNSUPPORTED,
+            "standalone collectives need the LOCAL or NCCL transport (PEER is engine-only)");
     validate_shape(shape);
     validate_width(elem_bytes);
     validate_axis(scatter_axis);
@@ -365,6 +381,8 @@ void World::fused_all_to_all(void* const* const ins[3], void* const* const outs[
 
 void World::all_gather(void* const* in, void* const* out, const int64_t shape[4],
                        int elem_bytes, int axis) {
+    require(transport_ != SPX_TRANSPORT_PEER, SPX_ERR_UNSUPPORTED,
+            "standalone collectives need the LOCAL or NCCL transport (PEER is engine-only)");
     validate_shape(shape);
     validate_width(elem_bytes);
     validate_axis(axis);

@@ -6,7 +6,9 @@
 //   LOCAL : every rank of the world lives in this process (devices may repeat, so P ranks
 //           can share one GPU); a chunk moves by direct stores into the destination
 //           buffer (peer memory across GPUs), ordering by CUDA events between the streams;
-//   NCCL  : one rank per process; grouped ncclSend/ncclRecv, one group == one round.
+//   NCCL  : one rank per process; grouped ncclSend/ncclRecv, one group == one round;
+//   PEER  : one rank per process; the engine maps its peers' exchange buffers through CUDA
+//           IPC and its kernels store into them directly, device-side flags order the ranks.
 // The traffic ledger (CommStats) counts logical collectives exactly like the reference:
 // one per invocation, elements_sent = scalars crossing a rank boundary, sender side.
 #pragma once
@@ -32,6 +34,7 @@ class World {
   public:
     World(int world_size, const int* devices);                            // LOCAL
     World(int rank, int world_size, const uint8_t id[128], int device);  // NCCL
+    World(int rank, int world_size, int device);                          // PEER
     ~World();
     World(const World&) = delete;
     World& operator=(const World&) = delete;

@@ -289,6 +289,14 @@ class CommWorld:
         check(lib().spx_world_create_nccl(rank, world_size, uid, device, ctypes.byref(h)))
         return cls(world_size, _handle=h)
 
+    @classmethod
+    def peer(cls, rank, world_size, device):
+        """PEER transport (one rank per process): the engine's kernels store into the peers'
+        exchange buffers through CUDA IPC mappings; call Engine.connect_peers once."""
+        h = ctypes.c_void_p()
+        check(lib().spx_world_create_peer(rank, world_size, device, ctypes.byref(h)))
+        return cls(world_size, _handle=h)
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         uid = (ctypes.c_uint8 * 128)()
@@ -491,6 +499,31 @@ class Engine:
         if getattr(self, "_h", None):
             lib().spx_engine_destroy(self._h)
             self._h = None
+
+    def ipc_export(self) -> bytes:
+        """PEER transport: this rank's exchange-buffer handles (an opaque blob)."""
+        n = ctypes.c_int64()
+        check(lib().spx_engine_ipc_export(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        check(lib().spx_engine_ipc_export(self._h, buf, n.value, ctypes.byref(n)))
+        return bytes(buf)
+
+    def ipc_import(self, blobs: Sequence[bytes]):
+        """PEER transport: map every rank's buffers (blobs of all ranks, in rank order)."""
+        per = len(blobs[0])
+        if any(len(b) != per for b in blobs):
+            raise ShapeError("ipc blobs differ in size")
+        joined = b"".join(blobs)
+        buf = (ctypes.c_uint8 * len(joined)).from_buffer_copy(joined)
+        check(lib().spx_engine_ipc_import(self._h, buf, per))
+
+    def connect_peers(self, all_gather_object):
+        """PEER transport: exchange handles through a host all-gather (e.g.
+        torch.distributed.all_gather_object) and map them."""
+        mine = self.ipc_export()
+        blobs = [None] * self.world.world_size()
+        all_gather_object(blobs, mine)
+        self.ipc_import(blobs)
 
     def set_layer_weights(self, layer, wq, wk, wv, wo):
         """host weights (dim, dim) [out][in]; float arrays are rounded to bf16 (RNE)."""
