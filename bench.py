@@ -10,7 +10,8 @@ latents. The reference arm (--impl reference) times the reference's own CPU oper
 (oracle/_ref, compiled from /root/reference sources) on a bounded sample of a layer call.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl spx|reference]
-  (N > 1: launched by torchrun, one process per GPU, NCCL transport)
+  (N > 1: launched by torchrun, one process per GPU; PEER transport by default -- the
+   producing kernels store into the peers' CUDA-IPC-mapped buffers -- or --transport nccl)
 """
 import argparse
 import ctypes
@@ -158,6 +159,12 @@ def main():
                     help="skip the C5 60 s rolling-window run (about 10 s of GPU time)")
     ap.add_argument("--no-fuse-rope", action="store_true",
                     help="standalone K3 RoPE/pack kernel instead of the QKV GEMM epilogue")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: PEER (kernels store into the peers' IPC-mapped buffers, device "
+                         "flag barriers) or NCCL (grouped send/recv of packed slabs)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="debug: every rank on cuda:0 (PEER only; checks the multi-process "
+                         "path on one GPU, not a performance number)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -172,17 +179,32 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world_size != args.gpus:
         world_size = args.gpus if world_size == 1 and args.gpus == 1 else world_size
-    torch.cuda.set_device(local_rank)
+    device = 0 if args.same_device else local_rank
+    torch.cuda.set_device(device)
     dist = None
     if world_size > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        uid = [spattn.CommWorld.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        world = spattn.CommWorld.nccl(rank, world_size, uid[0], local_rank)
+        if args.same_device:
+            if args.transport != "peer":
+                raise SystemExit("--same-device needs the PEER transport")
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        if args.transport == "nccl":
+            uid = [spattn.CommWorld.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            world = spattn.CommWorld.nccl(rank, world_size, uid[0], device)
+        else:
+            world = spattn.CommWorld.peer(rank, world_size, device)
     else:
-        world = spattn.CommWorld(1, [local_rank])
+        world = spattn.CommWorld(1, [device])
+
+    def new_engine(cfg):
+        e = spattn.Engine(cfg, world=world)  # seeded random-init weights (reference init, bf16)
+        if world_size > 1 and args.transport == "peer":
+            e.connect_peers(dist.all_gather_object)  # CUDA IPC handles of the exchange buffers
+        return e
 
     F, Hg, Wg, H, D = WAN["frames"], WAN["grid_h"], WAN["grid_w"], WAN["heads"], WAN["head_dim"]
     L, C = F * Hg * Wg, H * D
@@ -190,7 +212,7 @@ def main():
                                   layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H, head_dim=D,
                                   world_size=world_size, seed=0, profile=False,
                                   fuse_rope_epilogue=not args.no_fuse_rope)
-    eng = spattn.Engine(cfg, world=world)  # seeded random-init weights (reference init, bf16)
+    eng = new_engine(cfg)
     Lp = eng.local_len
     steps = WAN["steps"]
 
@@ -229,7 +251,8 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cpu" if args.same_device else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -250,7 +273,7 @@ def main():
     # ---- timed: inputs resident in HBM (device events on the engine stream, max over ranks) ----
     stream = torch.cuda.ExternalStream(stream_ptr.value)
     check(lib().spx_engine_reset_stage_times(eng._h))
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(device)
     launches0 = int(lib().spx_launch_count())
     barrier()
     sampler.start()
@@ -296,13 +319,14 @@ def main():
     d2h = Lp * C * 2
 
     # ---- C3: 5 s 480P video = 7 chunks, unlimited KV window (the ring grows to 21 frames) ----
-    video = video_5s(run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev,
-                               out_dev, barrier, max_over_ranks, blocks=7))
+    video = video_5s(run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
+                               noise_dev, out_dev, barrier, max_over_ranks, blocks=7))
     # ---- C5: 60 s 480P (80 chunks) with a 21-frame rolling window, kernels already warm ----
     long_video = None
     if not args.skip_long_video:
-        long_video = video_60s(run_video(args, spattn, lib, check, ptr_array, world, world_size,
-                                         noise_dev, out_dev, barrier, max_over_ranks, blocks=80,
+        long_video = video_60s(run_video(args, new_engine, spattn, lib, check, ptr_array, world,
+                                         world_size, noise_dev, out_dev, barrier, max_over_ranks,
+                                         blocks=80,
                                          window=21, warmup=False), 21)
 
     # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
@@ -329,6 +353,8 @@ def main():
         "config": {"workload": "C2: Wan2.1-1.3B shape, 1 chunk of 3x30x52 = 4680 tokens, 30 layers, "
                                "4 denoise steps (120 self-attention calls)",
                    "global_batch": 1, "seq_len": L, "parallelism": f"sp{world_size}",
+                   "transport": (args.transport if world_size > 1 else "none") +
+                                (" (same device: path check, not a scaling number)" if args.same_device else ""),
                    "head_groups": eng.head_groups, "query_splits": eng.query_splits,
                    "l2": "inputs larger than L2: 566 MB of weights + 58 MB KV ring stream per chunk"},
         "e2e": {"value": e2e_fps, "unit": "latent frames/s", "h2d_bytes_per_step": h2d,
@@ -378,8 +404,8 @@ def _set_profile(eng, level):
     check(lib().spx_engine_set_profile(eng._h, int(level)))
 
 
-def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev, out_dev,
-              barrier, max_over_ranks, blocks=7, window=-1, warmup=True):
+def run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size, noise_dev,
+              out_dev, barrier, max_over_ranks, blocks=7, window=-1, warmup=True):
     """A video of `blocks` chunks (3 latent frames each, 30 layers, 4 denoise steps) on a
     second engine; per-chunk device times (CUDA events on the engine stream). window < 0:
     unlimited KV cache; otherwise the rolling window of `window` frames (the ring wraps and
@@ -393,7 +419,7 @@ def run_video(args, spattn, lib, check, ptr_array, world, world_size, noise_dev,
                                   head_dim=D, world_size=world_size, seed=0, profile=False,
                                   window_frames=window if window > 0 else None,
                                   fuse_rope_epilogue=not args.no_fuse_rope)
-    eng = spattn.Engine(cfg, world=world)
+    eng = new_engine(cfg)
     sp = ctypes.c_void_p()
     check(lib().spx_world_stream(world._h, 0, ctypes.byref(sp)))
     stream = torch.cuda.ExternalStream(sp.value)

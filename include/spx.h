@@ -254,6 +254,11 @@ typedef struct spx_engine_config {
                                          1 use_fused_all_to_all, 2 use_local_rope,
                                          4 use_precomputed_freqs; 7 = optimized (default),
                                          0 = the baseline Alg. 1 schedule */
+    int32_t adaln;                    /* 0 = reference semantics; 1 = the Wan block's adaLN
+                                         modulation: x_in = LN(x)(1 + scale) + shift before
+                                         the QKV projection (K1), x + gate * W_o o in the
+                                         O-projection epilogue (extension, no reference
+                                         counterpart; per-layer shift/scale/gate) */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */
@@ -272,6 +277,10 @@ spx_status spx_engine_set_layer_weights(spx_engine* engine, int64_t layer, const
                                         const uint16_t* wk, const uint16_t* wv,
                                         const uint16_t* wo);
 /* QK-RMSNorm weights (host bf16 [dim] each); only used when cfg.qk_norm = 1 */
+/* adaLN modulation of one layer (fp32 [dim] each; used when cfg.adaln = 1). Default: seeded
+ * N(0, 1)/sqrt(dim), the Wan modulation-parameter init, from derive_seed(seed, 0x30, layer). */
+spx_status spx_engine_set_modulation(spx_engine* engine, int64_t layer, const float* shift,
+                                     const float* scale, const float* gate);
 spx_status spx_engine_set_norm_weights(spx_engine* engine, int64_t layer, const uint16_t* wq,
                                        const uint16_t* wk);
 /* KvCache::update bookkeeping for a block (once per denoise step; every layer's ring gets
@@ -316,6 +325,10 @@ spx_status spx_engine_ipc_import(spx_engine* engine, const void* blobs, int64_t 
  * ------------------------------------------------------------------------------------- */
 spx_status spx_debug_naive_gemm(const void* a, const void* b, float* out, int64_t m, int64_t n,
                                 int64_t k, void* stream);
+/* K1 (Wan adaLN extension) on device buffers: y = LayerNorm(x)(1 + scale) + shift over the
+ * last dim; x, y (tokens, dim) bf16; shift, scale fp32 [dim] device pointers. */
+spx_status spx_layernorm_modulate(const void* x, void* y, int64_t tokens, int64_t dim,
+                                  const float* shift, const float* scale, float eps, void* stream);
 /* Force the projection GEMM tile variant for plans made after the call: -1 = the planner's
  * modelled choice; 0 pair 256x256, 1 pair 256x128, 2 single 128x256, 3 single 128x128,
  * 4 single 128x192 (tests and tuning; also SPX_GEMM_VARIANT at load time). */

@@ -58,8 +58,9 @@ def _ol():
             "oracle_sdpa": (None, [D_P, D_P, D_P, D_P, c_int64, c_int64, c_int64, c_int64]),
             "oracle_rms_norm": (None, [D_P, D_P, c_int64, c_int64, c_double]),
             "oracle_checksum": (c_uint64, [D_P, c_int64]),
-            "oracle_generate": (None, [I64_P, c_uint64, c_double, I64_P, D_P, D_P, D_P, c_double,
-                                       D_P, D_P]),
+            "oracle_generate": (None, [I64_P, c_uint64, c_double, I64_P, D_P, D_P, D_P, D_P,
+                                       c_double, D_P, D_P]),
+            "oracle_layernorm_modulate": (None, [D_P, D_P, D_P, D_P, c_int64, c_int64, c_double]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -210,20 +211,33 @@ def rms_norm(x, w=None, eps=1e-6):
     return x
 
 
+def layernorm_modulate(x, shift, scale, eps=1e-6):
+    """Wan adaLN modulation (extension, no reference counterpart): LN(x) (1 + scale) + shift."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    tokens = x.shape[0]
+    dim = x.size // tokens
+    y = np.empty_like(x)
+    _ol().oracle_layernorm_modulate(_dp(x), _dp(y), _dp(np.ascontiguousarray(shift, dtype=np.float64)),
+                                    _dp(np.ascontiguousarray(scale, dtype=np.float64)), tokens, dim, eps)
+    return y
+
+
 def generate(frames=3, grid_h=4, grid_w=4, num_blocks=5, layers=4, steps=2, heads=8, head_dim=16,
              window=None, force_start_frame_zero=False, seed=0, base=10000.0, split=None,
              weights=None, noise=None, round_inputs=False, qk_norm=False, norm_weights=None,
-             norm_eps=1e-6, return_layers=False):
+             norm_eps=1e-6, return_layers=False, modulation=None):
     """generate() with the reference pipeline at P = 1 (generator.cpp:50-147), fp64.
 
     weights: (layers, 4, dim, dim) or None (seeded); noise: (blocks, steps, L, dim) or None.
+    modulation: (layers, 3, dim) [shift | scale | gate] switches on the Wan adaLN extension
+    (x_in = LN(x)(1 + scale) + shift before the projections, x += gate * W_o o after).
     Returns (num_blocks, L, H, D) [, per-call outputs (blocks, steps, layers, L, H, D)].
     """
     L = frames * grid_h * grid_w
     dim = heads * head_dim
     cfg = _i64([frames, grid_h, grid_w, num_blocks, layers, steps, heads, head_dim,
                 -1 if window is None else window, int(force_start_frame_zero), int(round_inputs),
-                int(qk_norm)])
+                int(qk_norm), int(modulation is not None)])
     out = np.empty((num_blocks, L, heads, head_dim), dtype=np.float64)
     lo = None
     if return_layers:
@@ -231,9 +245,11 @@ def generate(frames=3, grid_h=4, grid_w=4, num_blocks=5, layers=4, steps=2, head
     w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
     nz = None if noise is None else np.ascontiguousarray(noise, dtype=np.float64)
     nw = None if norm_weights is None else np.ascontiguousarray(norm_weights, dtype=np.float64)
+    md = None if modulation is None else np.ascontiguousarray(modulation, dtype=np.float64)
     _ol().oracle_generate(cfg, seed, base, _i64(split) if split else None,
                           _dp(w) if w is not None else None, _dp(nz) if nz is not None else None,
-                          _dp(nw) if nw is not None else None, norm_eps, _dp(out),
+                          _dp(nw) if nw is not None else None, _dp(md) if md is not None else None,
+                          norm_eps, _dp(out),
                           _dp(lo) if lo is not None else None)
     return (out, lo) if return_layers else out
 

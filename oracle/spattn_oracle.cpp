@@ -180,6 +180,25 @@ void rms_norm(double* x, const double* w, int64_t tokens, int64_t dim, double ep
     }
 }
 
+// Wan adaLN modulation (extension; no reference counterpart): non-affine LayerNorm
+// over the model dim (biased variance, eps inside the sqrt), then x * (1 + scale) + shift.
+void layernorm_modulate(const double* x, double* y, const double* shift, const double* scale,
+                        int64_t tokens, int64_t dim, double eps) {
+    for (int64_t s = 0; s < tokens; ++s) {
+        const double* r = x + s * dim;
+        double* o = y + s * dim;
+        double mean = 0.0;
+        for (int64_t c = 0; c < dim; ++c) mean += r[c];
+        mean /= static_cast<double>(dim);
+        double var = 0.0;
+        for (int64_t c = 0; c < dim; ++c) var += (r[c] - mean) * (r[c] - mean);
+        var /= static_cast<double>(dim);
+        const double rstd = 1.0 / std::sqrt(var + eps);
+        for (int64_t c = 0; c < dim; ++c)
+            o[c] = (r[c] - mean) * rstd * (1.0 + scale[c]) + shift[c];
+    }
+}
+
 // ---- KV cache ---------------------------------------------------------------------------
 struct Cache {
     int64_t tpf, row;  // tokens per frame, elements per token
@@ -309,6 +328,11 @@ void oracle_rms_norm(double* x, const double* w, int64_t tokens, int64_t dim, do
     rms_norm(x, w, tokens, dim, eps);
 }
 
+void oracle_layernorm_modulate(const double* x, double* y, const double* shift,
+                               const double* scale, int64_t tokens, int64_t dim, double eps) {
+    layernorm_modulate(x, y, shift, scale, tokens, dim, eps);
+}
+
 uint64_t oracle_checksum(const double* p, int64_t n) {
     uint64_t h = 0xcbf29ce484222325ULL;
     for (int64_t i = 0; i < n; ++i) {
@@ -324,18 +348,20 @@ uint64_t oracle_checksum(const double* p, int64_t n) {
 
 // generate() with the reference (P = 1) pipeline.
 //   cfg: frames, Hg, Wg, num_blocks, layers, steps, heads, head_dim, window (<0 unlimited),
-//        force_start_frame_zero, round_inputs_bf16, qk_norm
+//        force_start_frame_zero, round_inputs_bf16, qk_norm, adaln
 //   weights: NULL (seeded) or layers x 4 x dim x dim ([q|k|v|o], [out][in])
 //   noise:   NULL (seeded) or num_blocks x steps x L x dim
 //   norm_w:  NULL (ones) or layers x 2 x dim  (only with qk_norm)
+//   mod:     layers x 3 x dim [shift | scale | gate] (only with adaln, the Wan block's
+//            self-attention modulation: x_in = LN(x)(1 + scale) + shift, x += gate * W_o o)
 //   out:     num_blocks x L x dim
 //   layer_out (optional): num_blocks x steps x layers x L x dim (every call's output)
 void oracle_generate(const int64_t* cfg, uint64_t seed, double base, const int64_t* split,
                      const double* weights, const double* noise, const double* norm_w,
-                     double norm_eps, double* out, double* layer_out) {
+                     const double* mod, double norm_eps, double* out, double* layer_out) {
     const int64_t F = cfg[0], Hg = cfg[1], Wg = cfg[2], blocks = cfg[3], layers = cfg[4],
                   steps = cfg[5], H = cfg[6], D = cfg[7], window = cfg[8], force0 = cfg[9],
-                  round_in = cfg[10], qk_norm = cfg[11];
+                  round_in = cfg[10], qk_norm = cfg[11], adaln = cfg[12];
     const int64_t hw = Hg * Wg, L = F * hw, dim = H * D;
     int64_t sp[3];
     if (split) {
@@ -360,7 +386,7 @@ void oracle_generate(const int64_t* cfg, uint64_t seed, double base, const int64
     }
     std::vector<Cache> caches(static_cast<size_t>(layers), Cache{hw, dim, window, {}});
     const size_t be = static_cast<size_t>(L * dim);
-    std::vector<double> x(be), q(be), k(be), v(be), o(be), ck, cv;
+    std::vector<double> x(be), q(be), k(be), v(be), o(be), xm(adaln ? be : 0), ck, cv;
     for (int64_t b = 0; b < blocks; ++b) {
         const int64_t start = force0 ? 0 : b * F;
         for (int64_t s = 0; s < steps; ++s) {
@@ -373,9 +399,15 @@ void oracle_generate(const int64_t* cfg, uint64_t seed, double base, const int64
                 for (double& e : x) e = round_bf16(e);
             for (int64_t l = 0; l < layers; ++l) {
                 const double* w = W.data() + l * 4 * mat;
-                project(x.data(), w, q.data(), L, dim);
-                project(x.data(), w + mat, k.data(), L, dim);
-                project(x.data(), w + 2 * mat, v.data(), L, dim);
+                const double* xin = x.data();
+                if (adaln) {
+                    const double* m = mod + l * 3 * dim;
+                    layernorm_modulate(x.data(), xm.data(), m, m + dim, L, dim, norm_eps);
+                    xin = xm.data();
+                }
+                project(xin, w, q.data(), L, dim);
+                project(xin, w + mat, k.data(), L, dim);
+                project(xin, w + 2 * mat, v.data(), L, dim);
                 if (qk_norm) {
                     rms_norm(q.data(), norm_w ? norm_w + l * 2 * dim : nullptr, L, dim, norm_eps);
                     rms_norm(k.data(), norm_w ? norm_w + l * 2 * dim + dim : nullptr, L, dim,
@@ -388,7 +420,15 @@ void oracle_generate(const int64_t* cfg, uint64_t seed, double base, const int64
                 c.read(ck, cv);
                 sdpa(q.data(), ck.data(), cv.data(), o.data(), L,
                      static_cast<int64_t>(ck.size()) / dim, H, D);
-                project(o.data(), w + 3 * mat, x.data(), L, dim);
+                if (adaln) {  // residual + gate (x += gate * W_o o)
+                    const double* gate = mod + l * 3 * dim + 2 * dim;
+                    project(o.data(), w + 3 * mat, q.data(), L, dim);
+                    for (int64_t t = 0; t < L; ++t)
+                        for (int64_t c = 0; c < dim; ++c)
+                            x[static_cast<size_t>(t * dim + c)] += gate[c] * q[static_cast<size_t>(t * dim + c)];
+                } else {
+                    project(o.data(), w + 3 * mat, x.data(), L, dim);
+                }
                 if (layer_out)
                     std::memcpy(layer_out + ((b * steps + s) * layers + l) * be, x.data(),
                                 be * sizeof(double));

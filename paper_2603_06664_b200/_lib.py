@@ -86,7 +86,7 @@ class EngineConfig(ctypes.Structure):
                 ("band_split", c_int64 * 3), ("seed", c_uint64),
                 ("force_start_frame_zero", c_int32), ("qk_norm", c_int32),
                 ("norm_eps", c_float), ("profile", c_int32),
-                ("fuse_rope_epilogue", c_int32), ("ablation", c_int32)]
+                ("fuse_rope_epilogue", c_int32), ("ablation", c_int32), ("adaln", c_int32)]
 
 
 # (name, restype, argtypes); restype None for void
@@ -165,6 +165,9 @@ _SIGS = [
     ("spx_engine_set_profile", c_int, [c_void_p, c_int32]),
     ("spx_engine_stats", c_int, [c_void_p, POINTER(CommStats)]),
     ("spx_world_create_peer", c_int, [c_int, c_int, c_int, c_void_p]),
+    ("spx_engine_set_modulation", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    ("spx_layernorm_modulate", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_float,
+                                       c_void_p]),
     ("spx_engine_ipc_export", c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     ("spx_engine_ipc_import", c_int, [c_void_p, c_void_p, c_int64]),
     ("spx_debug_set_gemm_variant", c_int, [c_int32]),

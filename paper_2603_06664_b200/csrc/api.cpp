@@ -691,6 +691,7 @@ void spx_engine_config_defaults(spx_engine_config* c) {
     c->profile = 0;
     c->fuse_rope_epilogue = 1;
     c->ablation = SPX_ABLATION_ALL;
+    c->adaln = 0;
 }
 
 spx_status spx_engine_config_validate(const spx_engine_config* cfg, int32_t world_size) {
@@ -821,6 +822,23 @@ spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out) {
     return guarded([&] {
         require(engine && out, SPX_ERR_CONFIG, "null argument");
         *out = engine->e->stats();
+    });
+}
+
+spx_status spx_engine_set_modulation(spx_engine* engine, int64_t layer, const float* shift,
+                                     const float* scale, const float* gate) {
+    return guarded([&] {
+        require(engine, SPX_ERR_CONFIG, "null engine");
+        engine->e->set_modulation(layer, shift, scale, gate);
+    });
+}
+
+spx_status spx_layernorm_modulate(const void* x, void* y, int64_t tokens, int64_t dim,
+                                  const float* shift, const float* scale, float eps, void* stream) {
+    return guarded([&] {
+        require(x && y && shift && scale, SPX_ERR_CONFIG, "null buffer");
+        ln_modulate_run(static_cast<const bf16*>(x), static_cast<bf16*>(y), tokens, dim, shift,
+                        scale, eps, as_stream(stream));
     });
 }
 

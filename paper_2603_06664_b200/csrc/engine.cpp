@@ -72,6 +72,8 @@ void Engine::validate(const spx_engine_config& c, int world_size) {
             "partition needs <= 8 head groups and <= 8 query splits");
     require(c.ablation >= 0 && c.ablation <= SPX_ABLATION_ALL, SPX_ERR_CONFIG,
             "ablation must be a combination of the three AblationFlags bits");
+    require(c.adaln == 0 || c.adaln == 1, SPX_ERR_CONFIG, "adaln must be 0 or 1");
+    require(c.qk_norm == 0 || c.qk_norm == 1, SPX_ERR_CONFIG, "qk_norm must be 0 or 1");
 }
 
 Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_(cfg) {
@@ -128,6 +130,7 @@ Engine::~Engine() {
         cudaFree(kv.second.wo);
         cudaFree(kv.second.norm_q);
         cudaFree(kv.second.norm_k);
+        cudaFree(kv.second.mod);
     }
     for (auto* set : {&pending_events_, &free_events_})
         for (StageEvents& se : *set)
@@ -266,6 +269,8 @@ void Engine::allocate() {
             SPX_CUDA(cudaMalloc(&w.wo, no * sizeof(bf16)));
             SPX_CUDA(cudaMalloc(&w.norm_q, nn * sizeof(bf16)));
             SPX_CUDA(cudaMalloc(&w.norm_k, nn * sizeof(bf16)));
+            SPX_CUDA(cudaMalloc(&w.mod, 3 * nn * sizeof(float)));
+            SPX_CUDA(cudaMemset(w.mod, 0, 3 * nn * sizeof(float)));
             SPX_CUDA(cudaMemset(w.wqkv, 0, nqkv * sizeof(bf16)));
             SPX_CUDA(cudaMemset(w.wo, 0, no * sizeof(bf16)));
             // norm weights default to 1.0 (bf16 0x3F80)
@@ -284,6 +289,7 @@ void Engine::allocate() {
         rs.x[0] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
         rs.x[1] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
         rs.qkv = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * 3 * C_));
+        if (cfg_.adaln) rs.xm = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
         rs.q_recv = dev_alloc<bf16>(rs, static_cast<size_t>(Lq_ * Hl_ * D_));
         rs.o_recv = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
         if (!(cfg_.ablation & SPX_ABLATION_FUSED_ALL_TO_ALL)) {  // all-gather targets (L, C)
@@ -327,7 +333,7 @@ void Engine::build_plans() {
         rs.attn_plan.resize(static_cast<size_t>(cfg_.layers));
         for (int64_t l = 0; l < cfg_.layers; ++l) {
             GemmOperands q{};
-            q.a = rs.x[l % 2];
+            q.a = cfg_.adaln ? rs.xm : rs.x[l % 2];
             q.a_row_stride = C_;
             q.a_group_stride = Lp_ * C_;
             q.groups = 1;
@@ -351,6 +357,12 @@ void Engine::build_plans() {
             o.b_row_stride = C_;
             o.out = rs.x[(l + 1) % 2];
             o.out_row_stride = C_;
+            if (cfg_.adaln) {  // x + gate * (W_o o): the gated residual in the epilogue
+                o.epi_mode = 1;
+                o.residual = rs.x[l % 2];
+                o.residual_row_stride = C_;
+                o.gate = w.mod + (l * 3 + 2) * C_;
+            }
             o.M = static_cast<int>(Lp_);
             o.N = static_cast<int>(C_);
             o.K = static_cast<int>(C_);
@@ -423,6 +435,27 @@ void Engine::seed_weights() {
             const uint16_t* b = bufs[static_cast<size_t>(l - l0)].data();
             set_layer_weights(l, b, b + mat, b + 2 * mat, b + 3 * mat);
         }
+    }
+    // adaLN modulation (Wan init: N(0, 1) / sqrt(dim)), fp32
+    for (int64_t l = 0; l < layers; ++l) {
+        HostRng rng(derive_seed(cfg_.seed, 0x30, static_cast<uint64_t>(l)));
+        std::vector<float> m(static_cast<size_t>(3 * C_));
+        const double sc = 1.0 / std::sqrt(static_cast<double>(C_));
+        for (float& e : m) e = static_cast<float>(rng.next_normal() * sc);
+        set_modulation(l, m.data(), m.data() + C_, m.data() + 2 * C_);
+    }
+}
+
+void Engine::set_modulation(int64_t layer, const float* shift, const float* scale,
+                            const float* gate) {
+    require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    require(shift && scale && gate, SPX_ERR_CONFIG, "null modulation vector");
+    for (auto& kv : weights_) {
+        SPX_CUDA(cudaSetDevice(kv.first));
+        float* m = kv.second.mod + layer * 3 * C_;
+        SPX_CUDA(cudaMemcpy(m, shift, C_ * 4, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(m + C_, scale, C_ * 4, cudaMemcpyHostToDevice));
+        SPX_CUDA(cudaMemcpy(m + 2 * C_, gate, C_ * 4, cudaMemcpyHostToDevice));
     }
 }
 
@@ -533,7 +566,8 @@ RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start
 
 void Engine::run_layer(int64_t layer, int64_t start_frame,
                        const std::vector<const GemmPlan*>& qkv,
-                       const std::vector<const GemmPlan*>& oproj) {
+                       const std::vector<const GemmPlan*>& oproj,
+                       const std::vector<const bf16*>& x_in) {
     require(have_block_, SPX_ERR_EMPTY_CACHE, "layer call before any block was registered");
     const bool local = world_->transport() == SPX_TRANSPORT_LOCAL;
     const bool peer = world_->transport() == SPX_TRANSPORT_PEER;
@@ -583,6 +617,11 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         RankState& rs = ranks_[static_cast<size_t>(li)];
         SPX_CUDA(cudaSetDevice(rs.device));
         mark(li, 0);
+        if (cfg_.adaln) {  // K1: x_in = LN(x)(1 + scale) + shift, the QKV GEMM's A operand
+            const float* m = weights_.at(rs.device).mod + layer * 3 * C_;
+            ln_modulate_run(x_in[static_cast<size_t>(li)], rs.xm, Lp_, C_, m, m + C_, cfg_.norm_eps,
+                            rs.stream);
+        }
         RopeLaunch rl = rope_launch(rs, layer, start_frame);
         if (!local_rope) rl.rotate = 0;  // exchange first, rotate after (apply_rope_global)
         if (!fused) {  // this rank's rows of the all-gathered q | k | v (all heads)
@@ -764,19 +803,22 @@ void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, v
     begin_block(block);  // KvCache::update of this call (idempotent within a block)
     std::vector<GemmPlan> qp(ranks_.size()), op(ranks_.size());
     std::vector<const GemmPlan*> qv, ov;
+    std::vector<const bf16*> xv;
     for (size_t li = 0; li < ranks_.size(); ++li) {
         RankState& rs = ranks_[li];
         SPX_CUDA(cudaSetDevice(rs.device));
         GemmOperands q = rs.qkv_plan[static_cast<size_t>(layer)].ops;
-        q.a = static_cast<const bf16*>(x[li]);
+        if (!cfg_.adaln) q.a = static_cast<const bf16*>(x[li]);  // adaLN: A is K1's output
         gemm_plan(&qp[li], q, device_sm_count(rs.device));
         GemmOperands o = rs.o_plan[static_cast<size_t>(layer)].ops;
         o.out = static_cast<bf16*>(y[li]);
+        if (cfg_.adaln) o.residual = static_cast<const bf16*>(x[li]);
         gemm_plan(&op[li], o, device_sm_count(rs.device));
         qv.push_back(&qp[li]);
         ov.push_back(&op[li]);
+        xv.push_back(static_cast<const bf16*>(x[li]));
     }
-    run_layer(layer, start_frame, qv, ov);
+    run_layer(layer, start_frame, qv, ov, xv);
 }
 
 void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_step) {
@@ -787,11 +829,13 @@ void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_s
         load_step(step);  // fresh noise into x[0] of every local rank (steps do not chain)
         for (int64_t l = 0; l < cfg_.layers; ++l) {
             std::vector<const GemmPlan*> qv, ov;
+            std::vector<const bf16*> xv;
             for (RankState& rs : ranks_) {
                 qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
                 ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
+                xv.push_back(rs.x[l % 2]);
             }
-            run_layer(l, start, qv, ov);
+            run_layer(l, start, qv, ov, xv);
         }
     }
 }

@@ -41,6 +41,7 @@ struct DeviceWeights {
     bf16* wo = nullptr;    // [layers][C][C]
     bf16* norm_q = nullptr;  // [layers][C]
     bf16* norm_k = nullptr;
+    float* mod = nullptr;  // [layers][3][C] adaLN shift | scale | gate (cfg.adaln)
 };
 
 struct RankState {
@@ -51,6 +52,7 @@ struct RankState {
     int g = 0, p = 0;
     bf16* x[2] = {nullptr, nullptr};  // (L/P, C) ping-pong
     bf16* qkv = nullptr;              // (L/P, 3C)
+    bf16* xm = nullptr;               // (L/P, C) adaLN-modulated layer input (cfg.adaln)
     bf16* q_recv = nullptr;           // (L/S, H/G, D)
     bf16* o_recv = nullptr;           // [G][L/P][H/G*D]
     bf16* q_send = nullptr;           // NCCL: [G][L/P][H/G][D]
@@ -92,6 +94,7 @@ class Engine {
     void set_layer_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk,
                            const uint16_t* wv, const uint16_t* wo);
     void set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk);
+    void set_modulation(int64_t layer, const float* shift, const float* scale, const float* gate);
     void begin_block(int64_t block_index);
     // a new video: every layer's KV cache empty again (generate() builds fresh caches,
     // generator.cpp:69-81); device ring memory is reused as is
@@ -118,8 +121,10 @@ class Engine {
     void allocate();
     void run_block(int64_t block, const std::function<void(int64_t)>& load_step);
     void build_plans();
+    // x_in[local]: the layer input (the K1 source with cfg.adaln; otherwise the QKV plans'
+    // A operand already points at it)
     void run_layer(int64_t layer, int64_t start_frame, const std::vector<const GemmPlan*>& qkv,
-                   const std::vector<const GemmPlan*>& oproj);
+                   const std::vector<const GemmPlan*>& oproj, const std::vector<const bf16*>& x_in);
     void harvest_events();
     void run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>& plan);
     RopeLaunch rope_launch(const RankState& rs, int64_t layer, int64_t start_frame) const;

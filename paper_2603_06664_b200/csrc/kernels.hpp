@@ -166,6 +166,11 @@ struct Box4 {
 };
 void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s);
 
+// K1 (Wan adaLN extension): y = LayerNorm(x) * (1 + scale) + shift, rows x dim bf16,
+// shift/scale fp32 [dim] (modulate.cu)
+void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const float* shift,
+                     const float* scale, float eps, cudaStream_t s);
+
 // ---------------------------------------------------------------------------------------
 // PEER transport: device-side rank barrier over IPC-mapped flag words. Each rank owns
 // flags[kPeerSlots][P] (uint64, epoch values). signal: after this stream's prior kernels

@@ -437,6 +437,7 @@ class GenerationConfig:
     norm_eps: float = 1e-6
     profile: bool = False
     fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
+    adaln: bool = False  # Wan adaLN modulation + gated residual (extension, default off)
     ablation: AblationFlags = field(default_factory=AblationFlags.all_on)
 
     def block_len(self):
@@ -467,6 +468,7 @@ class GenerationConfig:
         c.profile = int(self.profile)
         c.fuse_rope_epilogue = int(self.fuse_rope_epilogue)
         c.ablation = self.ablation.bits()
+        c.adaln = int(self.adaln)
         return c
 
     def validate(self):
@@ -524,6 +526,11 @@ class Engine:
         blobs = [None] * self.world.world_size()
         all_gather_object(blobs, mine)
         self.ipc_import(blobs)
+
+    def set_modulation(self, layer, shift, scale, gate):
+        """adaLN modulation of one layer (cfg.adaln): fp32 [dim] shift, scale, gate."""
+        arrs = [np.ascontiguousarray(a, dtype=np.float32).reshape(-1) for a in (shift, scale, gate)]
+        check(lib().spx_engine_set_modulation(self._h, layer, *[a.ctypes.data for a in arrs]))
 
     def set_layer_weights(self, layer, wq, wk, wv, wo):
         """host weights (dim, dim) [out][in]; float arrays are rounded to bf16 (RNE)."""

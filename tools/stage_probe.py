@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--P", type=int, default=1, help="virtual ranks on one device (LOCAL transport)")
     ap.add_argument("--chunks", type=int, default=5)
     ap.add_argument("--label", default="")
+    ap.add_argument("--wan", action="store_true", help="Wan mode: QK-RMSNorm + adaLN modulation")
     args = ap.parse_args()
     F, Hg, Wg, H, D, layers, steps = 3, 30, 52, 12, 128, 30, 4
     L, C = F * Hg * Wg, H * D
@@ -29,7 +30,8 @@ def main():
     cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(F, Hg, Wg), num_blocks=1,
                                   layers=layers, denoise_steps=steps, heads=H, head_dim=D,
                                   world_size=args.P, seed=0, profile=False,
-                                  fuse_rope_epilogue=not args.no_fuse_rope)
+                                  fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=args.wan,
+                                  adaln=args.wan)
     eng = spattn.Engine(cfg, world=world)
     Lp = L // args.P
     noise = [torch.randn(steps, Lp, C, device="cuda").mul_(D ** -0.5).to(torch.bfloat16)
@@ -72,7 +74,7 @@ def main():
             rows = [[round((v - tr[cta, 0, 2 if cta % 2 else 0]) / 1965.0, 2) if v else None
                      for v in tr[cta, it]] for it in range(6) if tr[cta, it].any()]
             print(json.dumps({"cta": cta, "us_since_first[mma_start,mma_issued,epi_start,epi_end]": rows}))
-    print(json.dumps({"label": args.label, "P": args.P, "fuse_rope": not args.no_fuse_rope,
+    print(json.dumps({"label": args.label, "P": args.P, "fuse_rope": not args.no_fuse_rope, "wan": args.wan,
                       "env": {k: v for k, v in os.environ.items() if k.startswith("SPX_")},
                       "chunk_ms": round(ms, 3), "frames_per_s": round(3e3 / ms, 2),
                       "stage_us_per_call": {k: round(v / max(calls, 1) * 1e3, 2)
