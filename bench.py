@@ -329,6 +329,16 @@ def main():
                                          blocks=80,
                                          window=21, warmup=False), 21)
 
+    # ---- Wan mode (extensions): QK-RMSNorm + adaLN modulation + gated residual, C2 chunk ----
+    wan_ms = run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
+                       noise_dev, out_dev, barrier, max_over_ranks, blocks=2, wan=True)
+    wan_block = {"workload": "C2 chunk with the Wan block's self-attention extensions: adaLN "
+                             "LayerNorm+modulation (K1), QK-RMSNorm + Causal-RoPE (K3), gated "
+                             "residual in the O-projection epilogue (no reference counterpart)",
+                 "first_frame_latency_ms": wan_ms[0],
+                 "latent_frames_per_s": 3 / (wan_ms[0] / 1e3),
+                 "chunk_ms": wan_ms, "note": "frames/s of the first chunk (C2); chunk 2 attends 6 frames"}
+
     # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
     peaks, peak_src = load_peaks()
     rope_mb = run_rope_microbench(torch, spattn, lib, check, peaks) if rank == 0 else None
@@ -369,6 +379,7 @@ def main():
                       "one kernel when the RoPE epilogue is fused: 'rope' is then empty)",
         "video_5s": video,
         "video_60s": long_video,
+        "wan_block": wan_block,
         "rope_microbench": rope_mb,
         "clocks": clocks, "gpu_launches": launches, "ledger": eng.stats(),
     }
@@ -405,7 +416,7 @@ def _set_profile(eng, level):
 
 
 def run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size, noise_dev,
-              out_dev, barrier, max_over_ranks, blocks=7, window=-1, warmup=True):
+              out_dev, barrier, max_over_ranks, blocks=7, window=-1, warmup=True, wan=False):
     """A video of `blocks` chunks (3 latent frames each, 30 layers, 4 denoise steps) on a
     second engine; per-chunk device times (CUDA events on the engine stream). window < 0:
     unlimited KV cache; otherwise the rolling window of `window` frames (the ring wraps and
@@ -418,7 +429,7 @@ def run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size
                                   layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H,
                                   head_dim=D, world_size=world_size, seed=0, profile=False,
                                   window_frames=window if window > 0 else None,
-                                  fuse_rope_epilogue=not args.no_fuse_rope)
+                                  fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=wan, adaln=wan)
     eng = new_engine(cfg)
     sp = ctypes.c_void_p()
     check(lib().spx_world_stream(world._h, 0, ctypes.byref(sp)))

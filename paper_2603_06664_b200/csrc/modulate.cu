@@ -3,10 +3,11 @@
 // (a Wan-mode extension with no reference counterpart; the residual + gate after
 // the output projection, x += gate * W_o o, is the O-GEMM's epi_mode 1 epilogue).
 //
-// HBM-bound: one read and one write of the (rows, C) bf16 activation. One warp per token
-// row; each lane owns the 16-byte vectors v = lane + 32 i of the row, all issued before any
-// math; mean and biased variance come from two warp reductions over the registers (no second
-// pass over memory); shift / scale are fp32 per column (L1/L2 resident across rows).
+// HBM-bound: one read and one write of the (rows, C) bf16 activation. Each lane owns the
+// 16-byte vectors v = lane + 32 i of a row, all issued before any math; mean and biased
+// variance come from two warp reductions over the registers (no second pass over memory).
+#include <algorithm>
+
 #include "common.hpp"
 #include "kernels.hpp"
 #include "sm100.cuh"
@@ -25,65 +26,93 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Two rows per warp-iteration (their loads issued together, 2 x 48 B x 32 lanes in flight per
+// warp), persistent grid-stride over row pairs; shift / scale staged once per CTA in shared
+// memory and read once per vector for both rows (L1 traffic ~ the activation bytes, not 5x).
 template <int NV>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     ln_modulate_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int rows, int dim,
                        const float* __restrict__ shift, const float* __restrict__ scale,
                        float eps) {
+    extern __shared__ float4 s_mod[];  // [nvec][4]: shift lo, shift hi, scale lo, scale hi
     const int lane = threadIdx.x % 32;
-    const int row = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
-    if (row >= rows) return;
     const int nvec = dim / 8;
-    const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * dim);
-    uint4 v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int c = lane + 32 * i;
-        v[i] = c < nvec ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) {
+        const int v = i / 4, q = i % 4;
+        const float* srcp = (q < 2 ? shift : scale) + v * 8 + (q & 1) * 4;
+        s_mod[i] = __ldg(reinterpret_cast<const float4*>(srcp));
     }
-    float s = 0.0f;
+    __syncthreads();
+    const int warps = static_cast<int>(gridDim.x) * kWarpsPerBlock;
+    const int pairs = (rows + 1) / 2;
+    for (int pr = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
+         pr < pairs; pr += warps) {
+        const int r0 = 2 * pr;
+        const bool has1 = r0 + 1 < rows;
+        const uint4* s0 = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(r0) * dim);
+        const uint4* s1 = s0 + nvec;
+        uint4 v0[NV], v1[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = unpack_bf16x2(w[e]);
-            s += f.x + f.y;
+        for (int i = 0; i < NV; ++i) {
+            const int c = lane + 32 * i;
+            const bool ok = c < nvec;
+            v0[i] = ok ? __ldg(s0 + c) : make_uint4(0, 0, 0, 0);
+            v1[i] = ok && has1 ? __ldg(s1 + c) : make_uint4(0, 0, 0, 0);
         }
-    }
-    const float mean = warp_sum(s) / static_cast<float>(dim);
-    float q = 0.0f;
+        float sum0 = 0.0f, sum1 = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        if (lane + 32 * i >= nvec) continue;
-        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+        for (int i = 0; i < NV; ++i) {
+            const uint32_t a[4] = {v0[i].x, v0[i].y, v0[i].z, v0[i].w};
+            const uint32_t b[4] = {v1[i].x, v1[i].y, v1[i].z, v1[i].w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = unpack_bf16x2(w[e]);
-            q += (f.x - mean) * (f.x - mean) + (f.y - mean) * (f.y - mean);
+            for (int e = 0; e < 4; ++e) {
+                const float2 fa = unpack_bf16x2(a[e]), fb = unpack_bf16x2(b[e]);
+                sum0 += fa.x + fa.y;
+                sum1 += fb.x + fb.y;
+            }
         }
-    }
-    const float rstd = rsqrtf(warp_sum(q) / static_cast<float>(dim) + eps);
-    uint4* dst = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row) * dim);
+        const float mean0 = warp_sum(sum0) / static_cast<float>(dim);
+        const float mean1 = warp_sum(sum1) / static_cast<float>(dim);
+        float q0 = 0.0f, q1 = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int c = lane + 32 * i;
-        if (c >= nvec) continue;
-        const float4* sh = reinterpret_cast<const float4*>(shift + c * 8);
-        const float4* sc = reinterpret_cast<const float4*>(scale + c * 8);
-        const float4 sh0 = __ldg(sh), sh1 = __ldg(sh + 1), sc0 = __ldg(sc), sc1 = __ldg(sc + 1);
-        const float shv[8] = {sh0.x, sh0.y, sh0.z, sh0.w, sh1.x, sh1.y, sh1.z, sh1.w};
-        const float scv[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
-        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-        uint32_t o[4];
+        for (int i = 0; i < NV; ++i) {
+            if (lane + 32 * i >= nvec) continue;
+            const uint32_t a[4] = {v0[i].x, v0[i].y, v0[i].z, v0[i].w};
+            const uint32_t b[4] = {v1[i].x, v1[i].y, v1[i].z, v1[i].w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = unpack_bf16x2(w[e]);
-            const float a = (f.x - mean) * rstd * (1.0f + scv[2 * e]) + shv[2 * e];
-            const float b = (f.y - mean) * rstd * (1.0f + scv[2 * e + 1]) + shv[2 * e + 1];
-            o[e] = pack_bf16x2(a, b);
+            for (int e = 0; e < 4; ++e) {
+                const float2 fa = unpack_bf16x2(a[e]), fb = unpack_bf16x2(b[e]);
+                q0 += (fa.x - mean0) * (fa.x - mean0) + (fa.y - mean0) * (fa.y - mean0);
+                q1 += (fb.x - mean1) * (fb.x - mean1) + (fb.y - mean1) * (fb.y - mean1);
+            }
         }
-        dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+        const float rstd0 = rsqrtf(warp_sum(q0) / static_cast<float>(dim) + eps);
+        const float rstd1 = rsqrtf(warp_sum(q1) / static_cast<float>(dim) + eps);
+        uint4* d0 = reinterpret_cast<uint4*>(y + static_cast<int64_t>(r0) * dim);
+        uint4* d1 = d0 + nvec;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int c = lane + 32 * i;
+            if (c >= nvec) continue;
+            const float4 sh0 = s_mod[c * 4], sh1 = s_mod[c * 4 + 1];
+            const float4 sc0 = s_mod[c * 4 + 2], sc1 = s_mod[c * 4 + 3];
+            const float shv[8] = {sh0.x, sh0.y, sh0.z, sh0.w, sh1.x, sh1.y, sh1.z, sh1.w};
+            const float scv[8] = {1.0f + sc0.x, 1.0f + sc0.y, 1.0f + sc0.z, 1.0f + sc0.w,
+                                  1.0f + sc1.x, 1.0f + sc1.y, 1.0f + sc1.z, 1.0f + sc1.w};
+            const uint32_t a[4] = {v0[i].x, v0[i].y, v0[i].z, v0[i].w};
+            const uint32_t b[4] = {v1[i].x, v1[i].y, v1[i].z, v1[i].w};
+            uint32_t oa[4], ob[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 fa = unpack_bf16x2(a[e]), fb = unpack_bf16x2(b[e]);
+                oa[e] = pack_bf16x2((fa.x - mean0) * rstd0 * scv[2 * e] + shv[2 * e],
+                                    (fa.y - mean0) * rstd0 * scv[2 * e + 1] + shv[2 * e + 1]);
+                ob[e] = pack_bf16x2((fb.x - mean1) * rstd1 * scv[2 * e] + shv[2 * e],
+                                    (fb.y - mean1) * rstd1 * scv[2 * e + 1] + shv[2 * e + 1]);
+            }
+            d0[c] = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            if (has1) d1[c] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+        }
     }
 }
 
@@ -99,18 +128,27 @@ void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const fl
             SPX_ERR_ALIGNMENT, "layernorm_modulate: 16-byte aligned buffers");
     if (rows == 0) return;
     const int nv = static_cast<int>((dim / 8 + 31) / 32);
-    const dim3 grid(static_cast<unsigned>((rows + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        SPX_CUDA(cudaGetDevice(&dev));
+        sms = device_sm_count(dev);
+    }
+    const int64_t pairs = (rows + 1) / 2;
+    const int64_t want = (pairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(want, 4LL * sms)));
     const dim3 block(kWarpsPerBlock * 32);
+    const size_t smem = static_cast<size_t>(dim / 8) * 4 * sizeof(float4);
     const int r = static_cast<int>(rows), d = static_cast<int>(dim);
     switch (nv) {
-        case 1: ln_modulate_kernel<1><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 2: ln_modulate_kernel<2><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 3: ln_modulate_kernel<3><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 4: ln_modulate_kernel<4><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 5: ln_modulate_kernel<5><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 6: ln_modulate_kernel<6><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 7: ln_modulate_kernel<7><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
-        default: ln_modulate_kernel<8><<<grid, block, 0, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 1: ln_modulate_kernel<1><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 2: ln_modulate_kernel<2><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 3: ln_modulate_kernel<3><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 4: ln_modulate_kernel<4><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 5: ln_modulate_kernel<5><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 6: ln_modulate_kernel<6><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 7: ln_modulate_kernel<7><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        default: ln_modulate_kernel<8><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -105,6 +105,28 @@ def rope(iters):
                               "frac_peak": round(gbs / PEAK_GBS, 3)}), flush=True)
 
 
+def modulate(iters):
+    """K1 (Wan adaLN): LayerNorm + modulation, rows x C bf16 -> bf16 (read + write bytes)."""
+    for rows in (4680, 585):
+        C = 1536
+        n = max(2, int(2 * 126 * 2 ** 20 // (2 * rows * C * 2)) + 2)  # rotate past L2
+        xs = [torch.randn(rows, C, device="cuda").to(torch.bfloat16) for _ in range(n)]
+        ys = [torch.empty_like(xs[0]) for _ in range(n)]
+        sh = torch.randn(C, device="cuda") * 0.1
+        sc = torch.randn(C, device="cuda") * 0.1
+        it = [0]
+
+        def fn():
+            i = it[0] % n
+            it[0] += 1
+            check(lib().spx_layernorm_modulate(xs[i].data_ptr(), ys[i].data_ptr(), rows, C,
+                                               sh.data_ptr(), sc.data_ptr(), 1e-6, stream_handle()))
+        ms = timeit(fn, iters)
+        gbs = 2 * rows * C * 2 / (ms * 1e-3) / 1e9
+        print(json.dumps({"kernel": "ln_modulate", "rows": rows, "ms": round(ms, 5), "GBs": round(gbs, 1),
+                          "frac_peak": round(gbs / PEAK_GBS, 3), "l2": "cold (rotating buffers)"}), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which.startswith("attn:"):  # attn:SQxSKVxH
@@ -120,3 +142,5 @@ if __name__ == "__main__":
         gemm(iters)
     if which in ("rope", "all"):
         rope(iters)
+    if which in ("modulate", "all"):
+        modulate(iters)
