@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    pdl_trigger();
     const int q_tile = blockIdx.x;
     const int head = blockIdx.y;
     const int split = blockIdx.z;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
 
     if (warp < 4) {
         setmaxnreg_dec56();
@@ -683,19 +685,21 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
         cfg.blockDim = dim3(kThreadsV2);
         cfg.dynamicSmemBytes = SmemV2<D, kMode>::kBytes;
         cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         // pair and multicast modes both load 64-row K boxes; multicast also 64-row V boxes
         SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q,
                                     plan.map_k_pair, kMode == 2 ? plan.map_v_half : plan.map_v, p));
     } else {
-        attn_fwd_v2_kernel<D, kMode><<<grid, kThreadsV2, SmemV2<D, kMode>::kBytes, stream>>>(
-            plan.map_q, plan.map_k, plan.map_v, p);
+        launch_pdl(attn_fwd_v2_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV2<D, kMode>::kBytes,
+                   stream, plan.map_q, plan.map_k, plan.map_v, p);
     }
 }
 

@@ -2,6 +2,7 @@
 #include "common.hpp"
 
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -17,6 +18,14 @@ const std::string& last_error() { return g_last_error; }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPX_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
 
 int device_sm_count(int device) {
     static std::mutex mu;

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "../../include/spx.h"
 
@@ -62,5 +63,30 @@ void count_launch(int n = 1);
 int64_t launch_count();
 
 int device_sm_count(int device);
+
+// Programmatic dependent launch (PDL) between the stream-ordered kernels of a layer call:
+// every hot kernel triggers its dependents on entry and waits (griddepcontrol.wait) after its
+// prologue (barrier init, TMEM allocation, descriptor prefetch, constant-table staging), so
+// the next kernel's launch and prologue overlap the tail of the previous one. SPX_PDL=0
+// turns it off (plain stream serialisation).
+bool pdl_enabled();
+
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SPX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+#endif
 
 }  // namespace spx

@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    pdl_trigger();  // the next kernel may launch; it waits for this grid before its main loop
     const int num_tiles = p.num_m_tiles * p.num_n_tiles;
     const int num_kt = p.K / kBK;
 
@@ -280,6 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+    // the previous kernel's outputs (A operand, destinations, a per-call RoPE table) are
+    // complete past this point; everything above overlapped its tail
+    pdl_wait();
     if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     __syncthreads();
@@ -423,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    pdl_trigger();  // the next kernel may launch; it waits for this grid before its main loop
     const int cta = static_cast<int>(cluster_ctarank());
     const bool leader = cta == 0;
     const int pair = blockIdx.x / 2;
@@ -444,6 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    pdl_wait();
     if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     cluster_sync_all();
@@ -707,24 +713,24 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     if (experiment == 5) p.trace = gemm_trace_buffer();
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
-        gemm_bf16_tn_pair_kernel<256><<<plan.grid, kThreads, gemm_pair_smem_bytes<256>(), stream>>>(
-            plan.map_a, plan.map_b, p);
+        launch_pdl(gemm_bf16_tn_pair_kernel<256>, dim3(plan.grid), dim3(kThreads),
+                   gemm_pair_smem_bytes<256>(), stream, plan.map_a, plan.map_b, p);
     } else if (plan.pair) {
         set_pair_smem_attr<128>();
-        gemm_bf16_tn_pair_kernel<128><<<plan.grid, kThreads, gemm_pair_smem_bytes<128>(), stream>>>(
-            plan.map_a, plan.map_b, p);
+        launch_pdl(gemm_bf16_tn_pair_kernel<128>, dim3(plan.grid), dim3(kThreads),
+                   gemm_pair_smem_bytes<128>(), stream, plan.map_a, plan.map_b, p);
     } else if (plan.bn == 192) {
         set_smem_attr<192>();
-        gemm_bf16_tn_kernel<192><<<plan.grid, kThreads, gemm_smem_bytes<192>(), stream>>>(
-            plan.map_a, plan.map_b, p);
+        launch_pdl(gemm_bf16_tn_kernel<192>, dim3(plan.grid), dim3(kThreads), gemm_smem_bytes<192>(),
+                   stream, plan.map_a, plan.map_b, p);
     } else if (plan.bn == 256) {
         set_smem_attr<256>();
-        gemm_bf16_tn_kernel<256><<<plan.grid, kThreads, gemm_smem_bytes<256>(), stream>>>(
-            plan.map_a, plan.map_b, p);
+        launch_pdl(gemm_bf16_tn_kernel<256>, dim3(plan.grid), dim3(kThreads), gemm_smem_bytes<256>(),
+                   stream, plan.map_a, plan.map_b, p);
     } else {
         set_smem_attr<128>();
-        gemm_bf16_tn_kernel<128><<<plan.grid, kThreads, gemm_smem_bytes<128>(), stream>>>(
-            plan.map_a, plan.map_b, p);
+        launch_pdl(gemm_bf16_tn_kernel<128>, dim3(plan.grid), dim3(kThreads), gemm_smem_bytes<128>(),
+                   stream, plan.map_a, plan.map_b, p);
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                        const float* __restrict__ shift, const float* __restrict__ scale,
                        float eps) {
     extern __shared__ float4 s_mod[];  // [nvec][4]: shift lo, shift hi, scale lo, scale hi
+    pdl_trigger();
     const int lane = threadIdx.x % 32;
     const int nvec = dim / 8;
     for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) {
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         s_mod[i] = __ldg(reinterpret_cast<const float4*>(srcp));
     }
     __syncthreads();
+    pdl_wait();  // x was written by the previous kernel (the last O-projection)
     const int warps = static_cast<int>(gridDim.x) * kWarpsPerBlock;
     const int pairs = (rows + 1) / 2;
     for (int pr = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
@@ -141,14 +143,14 @@ void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const fl
     const size_t smem = static_cast<size_t>(dim / 8) * 4 * sizeof(float4);
     const int r = static_cast<int>(rows), d = static_cast<int>(dim);
     switch (nv) {
-        case 1: ln_modulate_kernel<1><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 2: ln_modulate_kernel<2><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 3: ln_modulate_kernel<3><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 4: ln_modulate_kernel<4><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 5: ln_modulate_kernel<5><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 6: ln_modulate_kernel<6><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        case 7: ln_modulate_kernel<7><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
-        default: ln_modulate_kernel<8><<<grid, block, smem, s>>>(x, y, r, d, shift, scale, eps); break;
+        case 1: launch_pdl(ln_modulate_kernel<1>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 2: launch_pdl(ln_modulate_kernel<2>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 3: launch_pdl(ln_modulate_kernel<3>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 4: launch_pdl(ln_modulate_kernel<4>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 5: launch_pdl(ln_modulate_kernel<5>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 6: launch_pdl(ln_modulate_kernel<6>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 7: launch_pdl(ln_modulate_kernel<7>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        default: launch_pdl(ln_modulate_kernel<8>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -69,6 +69,8 @@ __device__ __forceinline__ uint4 rotate_vec(uint4 x, const float2 (&cs)[4], floa
 template <int NV, bool KV, bool NORM>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     rope_norm_pack_kernel(const RopeLaunch l) {
+    pdl_trigger();
+    pdl_wait();  // qkv was written by the previous kernel (the QKV projection)
     const int lane = threadIdx.x % 32;
     const int row = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
     if (row >= l.rows) return;
@@ -197,13 +199,13 @@ template <int NV>
 void launch_rope_nv(const RopeLaunch& l, unsigned blocks, cudaStream_t stream) {
     const dim3 b(kWarpsPerBlock * 32);
     if (l.has_kv && l.norm)
-        rope_norm_pack_kernel<NV, true, true><<<blocks, b, 0, stream>>>(l);
+        launch_pdl(rope_norm_pack_kernel<NV, true, true>, dim3(blocks), b, 0, stream, l);
     else if (l.has_kv)
-        rope_norm_pack_kernel<NV, true, false><<<blocks, b, 0, stream>>>(l);
+        launch_pdl(rope_norm_pack_kernel<NV, true, false>, dim3(blocks), b, 0, stream, l);
     else if (l.norm)
-        rope_norm_pack_kernel<NV, false, true><<<blocks, b, 0, stream>>>(l);
+        launch_pdl(rope_norm_pack_kernel<NV, false, true>, dim3(blocks), b, 0, stream, l);
     else
-        rope_norm_pack_kernel<NV, false, false><<<blocks, b, 0, stream>>>(l);
+        launch_pdl(rope_norm_pack_kernel<NV, false, false>, dim3(blocks), b, 0, stream, l);
 }
 
 void launch_rope(const RopeLaunch& l, int nv, unsigned blocks, cudaStream_t stream) {
