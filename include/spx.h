@@ -259,6 +259,8 @@ typedef struct spx_engine_config {
                                          the QKV projection (K1), x + gate * W_o o in the
                                          O-projection epilogue (extension, no reference
                                          counterpart; per-layer shift/scale/gate) */
+    int32_t l2_prefetch;              /* 1 (default): the attention kernel warms the next
+                                         projections' weights into L2 (bulk prefetch) */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */

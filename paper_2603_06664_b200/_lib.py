@@ -86,7 +86,8 @@ class EngineConfig(ctypes.Structure):
                 ("band_split", c_int64 * 3), ("seed", c_uint64),
                 ("force_start_frame_zero", c_int32), ("qk_norm", c_int32),
                 ("norm_eps", c_float), ("profile", c_int32),
-                ("fuse_rope_epilogue", c_int32), ("ablation", c_int32), ("adaln", c_int32)]
+                ("fuse_rope_epilogue", c_int32), ("ablation", c_int32), ("adaln", c_int32),
+                ("l2_prefetch", c_int32)]
 
 
 # (name, restype, argtypes); restype None for void

@@ -692,6 +692,7 @@ void spx_engine_config_defaults(spx_engine_config* c) {
     c->fuse_rope_epilogue = 1;
     c->ablation = SPX_ABLATION_ALL;
     c->adaln = 0;
+    c->l2_prefetch = 1;
 }
 
 spx_status spx_engine_config_validate(const spx_engine_config* cfg, int32_t world_size) {

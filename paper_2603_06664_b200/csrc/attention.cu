@@ -54,7 +54,28 @@ struct AttnParams {
     float* ws_lse;   // [splits][q_tiles * 128][heads]
     float* ws_o;     // [splits][q_tiles * 128][heads][D]
     int experiment;  // profiling only (SPX_ATTN_EXPERIMENT): 1 skip softmax math, 2 no MUFU
+    const uint8_t* pf[2];  // L2 prefetch ranges (see AttnOperands::l2_prefetch)
+    int64_t pf_bytes[2];
 };
+
+// this CTA's share of the L2 prefetch ranges, 16 KB bulk prefetches (no smem, no barrier)
+__device__ __forceinline__ void l2_prefetch_share(const AttnParams& p) {
+    const int64_t ctas = static_cast<int64_t>(gridDim.x) * gridDim.y * gridDim.z;
+    const int64_t me = (static_cast<int64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    for (int r = 0; r < 2; ++r) {
+        const int64_t n = p.pf_bytes[r];
+        if (n <= 0) continue;
+        constexpr int64_t kPiece = 16384;
+        const int64_t pieces = (n + kPiece - 1) / kPiece;
+        for (int64_t i = me; i < pieces; i += ctas) {
+            const int64_t off = i * kPiece;
+            const uint32_t bytes = static_cast<uint32_t>(min(kPiece, n - off)) & ~15u;
+            if (bytes)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf[r] + off), "r"(bytes)
+                             : "memory");
+        }
+    }
+}
 
 __device__ __forceinline__ void kv_tile_coords(const AttnParams& p, int j, int& row, int& valid) {
     if (j < p.seg_tiles0) {
@@ -266,6 +287,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp == 3 && lane == 0) l2_prefetch_share(p);  // constant data: before the PDL wait
     pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
 
     if (warp < 4) {
@@ -806,6 +828,10 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     p.experiment = experiment;
     for (int i = 0; i < 8; ++i) p.out_base[i] = o.out_base[i];
     p.rows_per_chunk = o.rows_per_chunk;
+    for (int r = 0; r < 2; ++r) {
+        p.pf[r] = static_cast<const uint8_t*>(o.l2_prefetch[r]);
+        p.pf_bytes[r] = o.l2_prefetch[r] ? o.l2_prefetch_bytes[r] : 0;
+    }
     p.out_row_stride = o.out_row_stride;
     p.out_batch_stride = o.out_batch_stride;
     // kv splits: as planned, but every CTA keeps >= 2 kv tiles (one per softmax warpgroup)

@@ -732,6 +732,14 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         mark(li, 4);  // cache: bookkeeping only, the exchange already wrote the ring slots
         AttnPlan plan = rs.attn_plan[static_cast<size_t>(layer)];
         attn_set_segments(&plan, seg_start_, seg_len_, num_segs_);
+        if (cfg_.l2_prefetch) {  // this layer's W_o and the next call's W_qkv into L2
+            const DeviceWeights& w = weights_.at(rs.device);
+            const int64_t next = (layer + 1) % cfg_.layers;
+            plan.ops.l2_prefetch[0] = w.wo + layer * C_ * C_;
+            plan.ops.l2_prefetch_bytes[0] = C_ * C_ * 2;
+            plan.ops.l2_prefetch[1] = w.wqkv + next * 3 * C_ * C_;
+            plan.ops.l2_prefetch_bytes[1] = 3 * C_ * C_ * 2;
+        }
         for (int64_t c = 0; c < G_; ++c) {
             const int i = static_cast<int>(rs.p * G_ + c);
             if (local || peer) {

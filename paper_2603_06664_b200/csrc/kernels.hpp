@@ -87,6 +87,10 @@ struct AttnOperands {
     // last CTA of a tile to finish merges them (no extra launch).
     void* workspace = nullptr;
     size_t workspace_bytes = 0;
+    // optional: byte ranges warmed into L2 while the (tensor-bound) kernel runs, e.g. the
+    // weights of the projections that follow (their HBM reads leave the GEMMs' critical path)
+    const void* l2_prefetch[2] = {nullptr, nullptr};
+    int64_t l2_prefetch_bytes[2] = {0, 0};
 };
 
 struct AttnPlan {

@@ -438,6 +438,7 @@ class GenerationConfig:
     profile: bool = False
     fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
     adaln: bool = False  # Wan adaLN modulation + gated residual (extension, default off)
+    l2_prefetch: bool = True  # attention warms the next projections' weights into L2
     ablation: AblationFlags = field(default_factory=AblationFlags.all_on)
 
     def block_len(self):
@@ -469,6 +470,7 @@ class GenerationConfig:
         c.fuse_rope_epilogue = int(self.fuse_rope_epilogue)
         c.ablation = self.ablation.bits()
         c.adaln = int(self.adaln)
+        c.l2_prefetch = int(self.l2_prefetch)
         return c
 
     def validate(self):

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--chunks", type=int, default=5)
     ap.add_argument("--label", default="")
     ap.add_argument("--wan", action="store_true", help="Wan mode: QK-RMSNorm + adaLN modulation")
+    ap.add_argument("--no-prefetch", action="store_true", help="no L2 weight prefetch in attention")
     args = ap.parse_args()
     F, Hg, Wg, H, D, layers, steps = 3, 30, 52, 12, 128, 30, 4
     L, C = F * Hg * Wg, H * D
@@ -31,7 +32,7 @@ def main():
                                   layers=layers, denoise_steps=steps, heads=H, head_dim=D,
                                   world_size=args.P, seed=0, profile=False,
                                   fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=args.wan,
-                                  adaln=args.wan)
+                                  adaln=args.wan, l2_prefetch=not args.no_prefetch)
     eng = spattn.Engine(cfg, world=world)
     Lp = L // args.P
     noise = [torch.randn(steps, Lp, C, device="cuda").mul_(D ** -0.5).to(torch.bfloat16)
