@@ -335,6 +335,9 @@ spx_status spx_layernorm_modulate(const void* x, void* y, int64_t tokens, int64_
  * modelled choice; 0 pair 256x256, 1 pair 256x128, 2 single 128x256, 3 single 128x128,
  * 4 single 128x192 (tests and tuning; also SPX_GEMM_VARIANT at load time). */
 spx_status spx_debug_set_gemm_variant(int32_t variant);
+/* Force the attention kernel's kv splits per query tile (1..8) for plans made after the call;
+ * 0 = the planner's wave model (tests and tuning; also SPX_ATTN_SPLITS at load time). */
+spx_status spx_debug_set_attn_splits(int32_t splits);
 /* SPX_GEMM_EXPERIMENT=5 only: copy n of the pair GEMM's per-tile clock64 marks of the last
  * launch ([cta][16 tiles][mma start, mma issued, epilogue start, epilogue end]) */
 spx_status spx_debug_gemm_trace(int64_t* out, int64_t n);

@@ -883,6 +883,13 @@ spx_status spx_debug_gemm_trace(int64_t* out, int64_t n) {
     });
 }
 
+spx_status spx_debug_set_attn_splits(int32_t splits) {
+    return guarded([&] {
+        require(splits >= 0 && splits <= 8, SPX_ERR_CONFIG, "attention splits must be 0..8");
+        attn_force_splits(splits);
+    });
+}
+
 spx_status spx_debug_set_gemm_variant(int32_t variant) {
     return guarded([&] {
         require(variant >= -1 && variant < gemm_num_variants(), SPX_ERR_CONFIG,

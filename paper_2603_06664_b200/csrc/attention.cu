@@ -9,6 +9,9 @@
 // range split between two softmax warpgroups that ping-pong against one MMA thread.
 #include <algorithm>
 
+#include <atomic>
+#include <cstdlib>
+
 #include "common.hpp"
 #include "kernels.hpp"
 #include "sm100.cuh"
@@ -56,7 +59,14 @@ struct AttnParams {
     int experiment;  // profiling only (SPX_ATTN_EXPERIMENT): 1 skip softmax math, 2 no MUFU
     const uint8_t* pf[2];  // L2 prefetch ranges (see AttnOperands::l2_prefetch)
     int64_t pf_bytes[2];
+    long long* trace;      // SPX_ATTN_EXPERIMENT=5: per-CTA clock64 marks [cta][16][4]
 };
+
+__device__ __forceinline__ void attn_mark(const AttnParams& p, int k) {
+    if (p.experiment != 5) return;
+    const int64_t me = (static_cast<int64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (me < 1024) p.trace[me * 64 + k] = clock64();
+}
 
 // this CTA's share of the L2 prefetch ranges, 16 KB bulk prefetches (no smem, no barrier)
 __device__ __forceinline__ void l2_prefetch_share(const AttnParams& p) {
@@ -115,7 +125,7 @@ struct SmemV2 {
     static constexpr uint32_t kOffQ = 0;
     static constexpr uint32_t kOffRing = kOffQ + kBQ * D * 2;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
-    static constexpr uint32_t kNumBars = 1 + 2 * kSlots + 6;
+    static constexpr uint32_t kNumBars = 1 + 2 * kSlots + 7;  // + the split-merge load barrier
     static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
@@ -240,7 +250,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint64_t* s_full = slot_empty + kSlots;  // [2]
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* pv_done = p_full + 2;          // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+    uint64_t* merge_bar = pv_done + 2;       // split-KV: other splits' partials landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 3);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
 
@@ -272,6 +283,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_init(&p_full[i], (kPair ? 2 : 1) * (SPX_PFULL_PER_WARP ? 4 : 128));
             mbar_init(&pv_done[i], 1);
         }
+        mbar_init(merge_bar, 1);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -289,6 +301,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const uint32_t tmem_base = *tmem_slot;
     if (warp == 3 && lane == 0) l2_prefetch_share(p);  // constant data: before the PDL wait
     pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
+    if (threadIdx.x == 0) attn_mark(p, 0);
 
     if (warp < 4) {
         setmaxnreg_dec56();
@@ -557,6 +570,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_wait(&pv_done[i], (n - 1) & 1);
             tc_fence_after();
         }
+        if (threadIdx.x == 128) attn_mark(p, 1);
         st_m[i * 128 + r] = m_run;
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
@@ -604,17 +618,30 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
             }
         } else {
-            // ---- split-KV: normalised fp32 partial + lse to the workspace ----
-            const int64_t prow = static_cast<int64_t>(q_tile) * kBQ + r;
-            const int64_t rows_all = static_cast<int64_t>(p.q_tiles) * kBQ;
-            float* wo = p.ws_o + ((split * rows_all + prow) * p.heads + head) * D;
+            // ---- split-KV ----
+            // Each split CTA stages its normalised fp32 partial (128 rows x D) in the now idle
+            // Q/ring smem (16-byte units XOR-swizzled by row: conflict-free, the swizzle travels
+            // with the bytes) and writes it to its own contiguous workspace block with ONE
+            // bulk copy; the last split of the tile bulk-loads the others back into smem and
+            // merges them lse-weighted. Workspace: [tile][split][128][D] fp32, [tile][split][128]
+            // lse, tile = head * q_tiles + q_tile.
+            constexpr uint32_t kUnits = D / 4;                  // 16-byte units per fp32 row
+            constexpr uint32_t kPartBytes = kBQ * D * 4;        // one partial
+            constexpr int kMaxOthers = static_cast<int>(L::kOffBar / kPartBytes) - 1;
+            const uint32_t s_base = smem_u32(smem);
+            auto unit_addr = [&](uint32_t buf, int row, uint32_t u) {
+                return s_base + buf * kPartBytes + static_cast<uint32_t>(row) * (kUnits * 16) +
+                       ((u ^ (static_cast<uint32_t>(row) & (kUnits - 1))) << 4);
+            };
+            const int64_t tile = static_cast<int64_t>(head) * p.q_tiles + q_tile;
+            float* ws_tile = p.ws_o + tile * p.splits * (kBQ * D);
+            float* lse_tile = p.ws_lse + tile * p.splits * kBQ;
 #pragma unroll 1
             for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
                 uint32_t o0[32], o1[32];
                 tmem_ld32(t_o0 + c * 32, o0);
                 if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
                 tmem_ld_wait();
-                float4* w4 = reinterpret_cast<float4*>(wo + c * 32);
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
                     float f[4];
@@ -622,16 +649,26 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     for (int e = 0; e < 4; ++e)
                         f[e] = __uint_as_float(o0[4 * v + e]) * w0 +
                                (n1 > 0 ? __uint_as_float(o1[4 * v + e]) * w1 : 0.0f);
-                    __stcg(w4 + v, make_float4(f[0], f[1], f[2], f[3]));
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     unit_addr(0, r, static_cast<uint32_t>(c * 8 + v))),
+                                 "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3])
+                                 : "memory");
                 }
             }
-            if (i == 0)
-                __stcg(p.ws_lse + (split * rows_all + prow) * p.heads + head,
-                       mm + __log2f(l0 * a0 + l1 * a1));
-            __threadfence();
+            if (i == 0) __stcg(lse_tile + split * kBQ + r, mm + __log2f(l0 * a0 + l1 * a1));
+            fence_proxy_async_smem();  // generic-proxy smem writes -> the bulk copy's reads
             named_bar_sync(1, 256);
             if (threadIdx.x == 128) {
-                int* ctr = p.counters + q_tile * p.heads + head;
+                attn_mark(p, 2);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                 ws_tile + static_cast<int64_t>(split) * (kBQ * D)),
+                             "r"(s_base), "r"(kPartBytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                int* ctr = p.counters + tile;
                 const int prev = atomicAdd(ctr, 1);
                 s_last = prev == p.splits - 1;
                 if (s_last) *ctr = 0;  // every split has arrived: re-arm for the next launch
@@ -639,28 +676,61 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             named_bar_sync(1, 256);
             if (s_last) {
                 __threadfence();
-                // merge: row r, head-dim half i, over all splits (lse-weighted)
                 float lse_max = -INFINITY;
-                for (int z = 0; z < p.splits; ++z)
-                    lse_max = fmaxf(lse_max,
-                                    __ldcg(p.ws_lse + (z * rows_all + prow) * p.heads + head));
-                float wsum = 0.0f;
+                for (int z = 0; z < p.splits; ++z) lse_max = fmaxf(lse_max, __ldcg(lse_tile + z * kBQ + r));
                 float acc[D / 2];
-#pragma unroll
-                for (int e = 0; e < D / 2; ++e) acc[e] = 0.0f;
-                for (int z = 0; z < p.splits; ++z) {
-                    const float wz = ex2_approx(
-                        __ldcg(p.ws_lse + (z * rows_all + prow) * p.heads + head) - lse_max);
-                    wsum += wz;
-                    const float4* src = reinterpret_cast<const float4*>(
-                        p.ws_o + ((z * rows_all + prow) * p.heads + head) * D + i * (D / 2));
+                float wsum;
+                {  // own partial (staging buffer 0)
+                    const float wz = ex2_approx(__ldcg(lse_tile + split * kBQ + r) - lse_max);
+                    wsum = wz;
 #pragma unroll
                     for (int v = 0; v < D / 8; ++v) {
-                        const float4 t = __ldcg(src + v);
-                        acc[4 * v + 0] = fmaf(wz, t.x, acc[4 * v + 0]);
-                        acc[4 * v + 1] = fmaf(wz, t.y, acc[4 * v + 1]);
-                        acc[4 * v + 2] = fmaf(wz, t.z, acc[4 * v + 2]);
-                        acc[4 * v + 3] = fmaf(wz, t.w, acc[4 * v + 3]);
+                        float4 t;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                     : "r"(unit_addr(0, r, static_cast<uint32_t>(i * (D / 8) + v))));
+                        acc[4 * v + 0] = wz * t.x;
+                        acc[4 * v + 1] = wz * t.y;
+                        acc[4 * v + 2] = wz * t.z;
+                        acc[4 * v + 3] = wz * t.w;
+                    }
+                }
+                // the other splits in batches of kMaxOthers (other index o -> split z)
+                uint32_t phase = 0;
+                const int others = p.splits - 1;
+                for (int o0 = 0; o0 < others; o0 += kMaxOthers) {
+                    const int cnt = min(kMaxOthers, others - o0);
+                    named_bar_sync(1, 256);  // buffers 1.. are free (previous batch read)
+                    if (threadIdx.x == 128) {
+                        mbar_arrive_expect_tx(merge_bar, static_cast<uint32_t>(cnt) * kPartBytes);
+                        for (int b = 0; b < cnt; ++b) {
+                            const int z = o0 + b < split ? o0 + b : o0 + b + 1;
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1], %2, [%3];" ::"r"(s_base + (b + 1) * kPartBytes),
+                                "l"(ws_tile + static_cast<int64_t>(z) * (kBQ * D)), "r"(kPartBytes),
+                                "r"(smem_u32(merge_bar))
+                                : "memory");
+                        }
+                    }
+                    mbar_wait(merge_bar, phase);
+                    phase ^= 1;
+                    for (int b = 0; b < cnt; ++b) {
+                        const int z = o0 + b < split ? o0 + b : o0 + b + 1;
+                        const float wz = ex2_approx(__ldcg(lse_tile + z * kBQ + r) - lse_max);
+                        wsum += wz;
+#pragma unroll
+                        for (int v = 0; v < D / 8; ++v) {
+                            float4 t;
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                         : "r"(unit_addr(static_cast<uint32_t>(b + 1), r,
+                                                         static_cast<uint32_t>(i * (D / 8) + v))));
+                            acc[4 * v + 0] = fmaf(wz, t.x, acc[4 * v + 0]);
+                            acc[4 * v + 1] = fmaf(wz, t.y, acc[4 * v + 1]);
+                            acc[4 * v + 2] = fmaf(wz, t.z, acc[4 * v + 2]);
+                            acc[4 * v + 3] = fmaf(wz, t.w, acc[4 * v + 3]);
+                        }
                     }
                 }
                 if (dst) {
@@ -676,6 +746,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             }
         }
     }
+    if (threadIdx.x == 128) attn_mark(p, 3);
     tc_fence_before();
     if constexpr (kCluster)
         cluster_sync_all();
@@ -727,19 +798,44 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
 
 }  // namespace
 
-int attn_max_splits(const AttnOperands& ops, int sm_count) {
-    static const int forced = [] {  // tuning override: SPX_ATTN_SPLITS=<1..8>
-        const char* e = std::getenv("SPX_ATTN_SPLITS");
-        return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
-    }();
-    if (forced) return forced;
-    // Split only while the doubled grid still fits in one wave: the partials cost a
-    // fp32 round trip through L2 and a merge, which only pays when SMs would idle
-    // (measured: 1170x4680x3 s=2 0.043 ms vs s=1 0.047; 4680x4680x12 s=2 0.209 vs 0.127).
-    const int64_t n = ceil_div(static_cast<int64_t>(ops.sq), kBQ) * ops.heads * ops.batch;
+namespace {
+// kv splits for n (query tile x head) CTAs over `tiles` kv tiles: the modelled time
+//   waves(n s) x (c + tiles / s)          [kv-tile units]
+// with the fixed per-CTA cost c = 3.3 tiles unsplit, 9 tiles split (fp32 partial staging, the
+// bulk copy out, the last CTA's bulk loads + merge), fitted to B200 sweeps (tools/kbench.py,
+// SPX_ATTN_SPLITS=1..8: e.g. 2340x4680x3 s=2 29.5 vs s=1 40.1 us; 2340x32760x3 s=5 113.7 vs
+// s=1 234.8; 4680x4680x6 s=1 80.8 vs s=2 82.3). Every CTA keeps >= 2 kv tiles (one per
+// softmax warpgroup).
+int choose_splits(int64_t n, int64_t tiles, int sm_count, int cap) {
     int best = 1;
-    while (best < 8 && n * 2 * best <= sm_count) best *= 2;
+    double best_t = 1e30;
+    for (int sp = 1; sp <= cap; ++sp) {
+        if (sp > 1 && tiles / sp < 2) break;
+        const double waves = static_cast<double>(ceil_div(n * sp, sm_count));
+        const double t = waves * ((sp == 1 ? 3.3 : 9.0) + static_cast<double>(tiles) / sp);
+        if (t < best_t * 0.97) {  // a split must win clearly (the model is coarse)
+            best_t = t;
+            best = sp;
+        }
+    }
     return best;
+}
+}  // namespace
+
+std::atomic<int> g_forced_splits{[] {  // tuning override: SPX_ATTN_SPLITS=<1..8>
+    const char* e = std::getenv("SPX_ATTN_SPLITS");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
+}()};
+
+void attn_force_splits(int s) { g_forced_splits.store(s, std::memory_order_relaxed); }
+
+int attn_max_splits(const AttnOperands& ops, int sm_count) {
+    const int forced = g_forced_splits.load(std::memory_order_relaxed);
+    if (forced) return forced;
+    // the workspace is sized for the longest kv range the buffers can hold (splits grow
+    // with the kv length)
+    const int64_t n = ceil_div(static_cast<int64_t>(ops.sq), kBQ) * ops.heads * ops.batch;
+    return choose_splits(n, ceil_div(ops.kv_rows, kBKV), sm_count, 8);
 }
 
 size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits) {
@@ -826,6 +922,7 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     p.experiment = experiment;
+    if (experiment == 5) p.trace = gemm_trace_buffer();
     for (int i = 0; i < 8; ++i) p.out_base[i] = o.out_base[i];
     p.rows_per_chunk = o.rows_per_chunk;
     for (int r = 0; r < 2; ++r) {
@@ -834,8 +931,16 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     }
     p.out_row_stride = o.out_row_stride;
     p.out_batch_stride = o.out_batch_stride;
-    // kv splits: as planned, but every CTA keeps >= 2 kv tiles (one per softmax warpgroup)
-    p.splits = std::max(1, std::min(plan.max_splits, p.total_tiles / 2));
+    // kv splits for this call's kv length, within the planned workspace
+    {
+        int dev = 0;
+        SPX_CUDA(cudaGetDevice(&dev));
+        const int64_t n = ceil_div(static_cast<int64_t>(o.sq), kBQ) * o.heads * o.batch;
+        const bool forced = g_forced_splits.load(std::memory_order_relaxed) != 0;
+        const int want = forced ? plan.max_splits
+                                : choose_splits(n, p.total_tiles, device_sm_count(dev), plan.max_splits);
+        p.splits = std::max(1, std::min(want, p.total_tiles / 2));
+    }
     p.heads = o.heads;
     p.q_tiles = static_cast<int>((ceil_div(o.sq, kBQ) + 1) & ~1);  // workspace stride (pairs)
     if (p.splits > 1) {

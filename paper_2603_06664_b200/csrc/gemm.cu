@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t aphase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], aphase ^ 1);
                 tc_fence_after();
+                if (issuer) trace_mark(p, it, 0);
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&full[stage], phase);
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (issuer) umma_commit(&tfull[acc]);
+                if (issuer) trace_mark(p, it, 1);
                 __syncwarp();
             }
         }
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n0 = (tile / p.num_m_tiles) * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
+            if (warp == 4 && lane == 0) trace_mark(p, it, 2);
             const int row = m0 + ew * 32 + lane;
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
@@ -375,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (warp == 4 && lane == 0) trace_mark(p, it, 3);
         }
     }
     __syncthreads();

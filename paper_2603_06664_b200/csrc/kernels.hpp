@@ -109,6 +109,8 @@ int attn_max_splits(const AttnOperands& ops, int sm_count);
 size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits);
 void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count);
 void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs);
+// split-KV override (tests / tuning): 0 = modelled choice, else the kv splits per query tile
+void attn_force_splits(int s);
 void attn_run(const AttnPlan& plan, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------------------

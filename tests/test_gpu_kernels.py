@@ -134,3 +134,29 @@ def test_rope_positions_bit_exact(cuda, grid, P, start):
         np.testing.assert_array_equal(t.cpu().numpy(), start + ig // (Hg * Wg))
         np.testing.assert_array_equal(h.cpu().numpy(), (ig % (Hg * Wg)) // Wg)
         np.testing.assert_array_equal(w.cpu().numpy(), ig % Wg)
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("sq,skv,H", [(2340, 4680, 3), (300, 2000, 2)])
+def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H):
+    """split-KV: fp32 partials staged in smem, bulk-copied out, bulk-loaded back and merged
+    lse-weighted by the last CTA of each query tile; every split count (including counts the
+    merge has to batch: 8 > 2 partials per batch at D = 128) against fp32 softmax attention."""
+    torch = _t()
+    D = 128
+    g = torch.Generator(device="cuda").manual_seed(splits * 31 + sq)
+    q = (torch.randn(1, sq, H, D, device=cuda, generator=g) * 0.5).to(torch.bfloat16)
+    k = (torch.randn(1, skv, H, D, device=cuda, generator=g) * 0.5).to(torch.bfloat16)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    _check(_lib().spx_debug_set_attn_splits(splits))
+    try:
+        for _ in range(2):  # the second launch runs on re-armed counters
+            _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq,
+                                        skv, H, D, _stream()))
+        torch.cuda.synchronize()
+    finally:
+        _check(_lib().spx_debug_set_attn_splits(0))
+    qf, kf, vf = (t.float()[0].transpose(0, 1) for t in (q, k, v))
+    ref = torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf
+    assert rel_l2(o.float()[0].transpose(0, 1), ref) < 1e-2

@@ -71,8 +71,10 @@ def main():
         check(lib().spx_debug_gemm_trace(tr.ctypes.data, tr.size))
         tr = tr.reshape(1024, 16, 4)
         for cta in (0, 1, 2, 3, 100, 101):
-            t0 = tr[cta & ~1, 0, 0] if cta % 2 else tr[cta, 0, 0]
-            rows = [[round((v - tr[cta, 0, 2 if cta % 2 else 0]) / 1965.0, 2) if v else None
+            # pair kernel: odd CTAs have no MMA marks (relative to their first epilogue);
+            # single-CTA kernel: every CTA has all four
+            base = tr[cta, 0, 0] if tr[cta, 0, 0] else tr[cta, 0, 2]
+            rows = [[round((v - base) / 1965.0, 2) if v else None
                      for v in tr[cta, it]] for it in range(6) if tr[cta, it].any()]
             print(json.dumps({"cta": cta, "us_since_first[mma_start,mma_issued,epi_start,epi_end]": rows}))
     print(json.dumps({"label": args.label, "P": args.P, "fuse_rope": not args.no_fuse_rope, "wan": args.wan,
