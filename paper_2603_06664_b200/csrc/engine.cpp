@@ -123,6 +123,14 @@ Engine::~Engine() {
         for (void* p : rs.allocations) cudaFree(p);
         if (rs.ev_k3) cudaEventDestroy(rs.ev_k3);
         if (rs.ev_attn) cudaEventDestroy(rs.ev_attn);
+        for (int b = 0; b < 2; ++b) {
+            if (rs.ev_ready[b]) cudaEventDestroy(rs.ev_ready[b]);
+            if (rs.ev_used[b]) cudaEventDestroy(rs.ev_used[b]);
+        }
+        if (rs.copy_stream) {
+            cudaStreamSynchronize(rs.copy_stream);
+            cudaStreamDestroy(rs.copy_stream);
+        }
     }
     for (auto& kv : weights_) {
         cudaSetDevice(kv.first);
@@ -851,11 +859,52 @@ void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_s
 void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t* out_host) {
     const size_t block_elems = static_cast<size_t>(L_ * C_);
     const size_t slice_bytes = static_cast<size_t>(Lp_ * C_) * sizeof(bf16);
-    run_block(block, [&](int64_t step) {
-        const uint16_t* src = nullptr;
-        if (noise_host) {
-            src = noise_host + static_cast<size_t>(step) * block_elems;
-        } else {
+    if (noise_host) {
+        // caller's noise: step s + 1 is uploaded (copy stream, into a staging buffer) while
+        // step s computes; each step starts with a device copy staging -> x[0]
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            if (!rs.copy_stream) {
+                SPX_CUDA(cudaStreamCreateWithFlags(&rs.copy_stream, cudaStreamNonBlocking));
+                for (int b = 0; b < 2; ++b) {
+                    rs.nstage[b] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
+                    SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_ready[b], cudaEventDisableTiming));
+                    SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_used[b], cudaEventDisableTiming));
+                }
+            }
+        }
+        auto upload = [&](int64_t step) {
+            for (RankState& rs : ranks_) {
+                SPX_CUDA(cudaSetDevice(rs.device));
+                const int b = static_cast<int>(step % 2);
+                // the staging buffer's previous contents (step - 2) were consumed
+                SPX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.ev_used[b], 0));
+                SPX_CUDA(cudaMemcpyAsync(rs.nstage[b],
+                                         noise_host + static_cast<size_t>(step) * block_elems +
+                                             static_cast<size_t>(rs.rank * Lp_ * C_),
+                                         slice_bytes, cudaMemcpyHostToDevice, rs.copy_stream));
+                SPX_CUDA(cudaEventRecord(rs.ev_ready[b], rs.copy_stream));
+            }
+        };
+        // the previous call's last step may still read a staging buffer: order the first upload
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            for (int b = 0; b < 2; ++b) SPX_CUDA(cudaEventRecord(rs.ev_used[b], rs.stream));
+        }
+        upload(0);
+        run_block(block, [&](int64_t step) {
+            for (RankState& rs : ranks_) {
+                SPX_CUDA(cudaSetDevice(rs.device));
+                const int b = static_cast<int>(step % 2);
+                SPX_CUDA(cudaStreamWaitEvent(rs.stream, rs.ev_ready[b], 0));
+                SPX_CUDA(cudaMemcpyAsync(rs.x[0], rs.nstage[b], slice_bytes, cudaMemcpyDeviceToDevice,
+                                         rs.stream));
+                SPX_CUDA(cudaEventRecord(rs.ev_used[b], rs.stream));
+            }
+            if (step + 1 < cfg_.denoise_steps) upload(step + 1);
+        });
+    } else {
+        run_block(block, [&](int64_t step) {
             // block_noise (generator.cpp:42-46), drawn in full on every rank, then sliced
             if (!noise_pinned_) {
                 SPX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&noise_pinned_),
@@ -867,14 +916,13 @@ void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t*
                                    static_cast<uint64_t>(step)),
                        static_cast<int64_t>(block_elems), D_, noise_f64_.data());
             for (size_t i = 0; i < block_elems; ++i) noise_pinned_[i] = f64_to_bf16(noise_f64_[i]);
-            src = noise_pinned_;
-        }
-        for (RankState& rs : ranks_) {
-            SPX_CUDA(cudaSetDevice(rs.device));
-            SPX_CUDA(cudaMemcpyAsync(rs.x[0], src + static_cast<size_t>(rs.rank * Lp_ * C_),
-                                     slice_bytes, cudaMemcpyHostToDevice, rs.stream));
-        }
-    });
+            for (RankState& rs : ranks_) {
+                SPX_CUDA(cudaSetDevice(rs.device));
+                SPX_CUDA(cudaMemcpyAsync(rs.x[0], noise_pinned_ + static_cast<size_t>(rs.rank * Lp_ * C_),
+                                         slice_bytes, cudaMemcpyHostToDevice, rs.stream));
+            }
+        });
+    }
     const int fin = static_cast<int>(cfg_.layers % 2);
     for (RankState& rs : ranks_) {
         SPX_CUDA(cudaSetDevice(rs.device));

@@ -72,6 +72,12 @@ struct RankState {
     size_t attn_ws_bytes = 0;
     cudaEvent_t ev_k3 = nullptr;
     cudaEvent_t ev_attn = nullptr;
+    // generate_block from host noise: the next denoise step's noise is uploaded on a copy
+    // stream into a staging buffer while the current step computes
+    bf16* nstage[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+    cudaEvent_t ev_used[2] = {nullptr, nullptr};
     std::vector<void*> allocations;
 };
 

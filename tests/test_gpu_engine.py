@@ -438,3 +438,30 @@ def test_wan_mode_sp_bit_identical_to_p1(cuda, world):
         eng = _engine_with_weights(cfg_from(kw, world=P, qk_norm=True, adaln=True), w)
         outs.append(eng.generate())  # seeded modulation (same seed on every rank count)
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_generate_block_host_noise_pipeline_matches_device_path(cuda):
+    """generate_block from host noise (the next step's noise uploaded on a copy stream while
+    the current step computes) == generate_block_device on the same noise, bit for bit, over
+    consecutive blocks (the staging buffers are reused across calls)."""
+    import torch
+
+    from paper_2603_06664_b200._lib import check, lib, ptr_array
+
+    s = spattn()
+    kw = dict(TINY)
+    cfg = cfg_from(kw, steps=3)
+    L, C = 192, kw["heads"] * kw["head_dim"]
+    rng = np.random.default_rng(5)
+    noise = [oracle.to_bf16_bits(oracle.round_bf16(rng.standard_normal((3, L, C)) * 0.1))
+             for _ in range(kw["num_blocks"])]
+    a = s.Engine(cfg)
+    got = [a.generate_block(b, noise[b]) for b in range(kw["num_blocks"])]
+    e = s.Engine(cfg)
+    for b in range(kw["num_blocks"]):
+        nd = torch.from_numpy(noise[b].view(np.int16)).to(cuda)
+        od = torch.empty((L, C), dtype=torch.int16, device=cuda)
+        check(lib().spx_engine_generate_block_device(e._h, b, ptr_array([nd.data_ptr()]),
+                                                     ptr_array([od.data_ptr()])))
+        check(lib().spx_engine_synchronize(e._h))
+        assert np.array_equal(got[b].reshape(L, C), od.cpu().numpy().view(np.uint16)), b
