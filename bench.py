@@ -52,13 +52,17 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.lines = []      # (host time, csv line)
+        self.windows = []    # host-time intervals the GPU was under the measured load
+
+    def mark(self, t0, t1):
+        self.windows.append((t0, t1))
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -67,7 +71,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def stop(self):
         if self.proc is None:
@@ -79,7 +83,11 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for t, ln in self.lines:
+            # only samples taken while the measured work ran (a sample reports the preceding
+            # ~20 ms, hence the slack at the end of each window)
+            if self.windows and not any(a <= t <= b + 0.03 for a, b in self.windows):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -91,10 +99,11 @@ class ClockSampler:
             for name, val in zip(names, parts[3:7]):
                 if val.lower() == "active":
                     reasons.add(name)
-        loaded = [s for s in sm if s > 500] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_min_mhz": min(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sampled": "nvidia-smi every 20 ms, samples inside the timed "
+                                               "region and the e2e region only"}
 
 
 def cpu_reference_sample(threads, tokens, rows, kv_frames=0):
@@ -150,7 +159,7 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="spx", choices=["spx", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -283,12 +292,13 @@ def main():
     # attention launches bracketed by CUDA events on the engine stream (profile level 2: two
     # events per call around the attention kernel, nothing else)
     _set_profile(eng, 2)
+    tw0 = time.perf_counter()
     ev0.record(stream)
     for _ in range(args.steps):
         chunk_device()
     ev1.record(stream)
     barrier()
-    clocks = sampler.stop()
+    sampler.mark(tw0, time.perf_counter())
     _set_profile(eng, 0)
     launches = int(lib().spx_launch_count()) - launches0
     dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -313,7 +323,10 @@ def main():
     for _ in range(args.steps):
         chunk_e2e()
     barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    t1 = time.perf_counter()
+    sampler.mark(t0, t1)
+    clocks = sampler.stop()
+    e2e_s = max_over_ranks(t1 - t0)
     e2e_fps = F * args.steps / e2e_s
     h2d = steps * Lp * C * 2
     d2h = Lp * C * 2

@@ -338,6 +338,9 @@ spx_status spx_debug_set_gemm_variant(int32_t variant);
 /* Force the attention kernel's kv splits per query tile (1..8) for plans made after the call;
  * 0 = the planner's wave model (tests and tuning; also SPX_ATTN_SPLITS at load time). */
 spx_status spx_debug_set_attn_splits(int32_t splits);
+/* SPX_SPAN_TRACE=1 only: per traced launch (GEMM, attention, in launch order) the earliest CTA
+ * start and the latest CTA end, globaltimer ns: out[2 i], out[2 i + 1] (capacity u64 slots). */
+spx_status spx_debug_spans(uint64_t* out, int64_t capacity, int64_t* count);
 /* SPX_GEMM_EXPERIMENT=5 only: copy n of the pair GEMM's per-tile clock64 marks of the last
  * launch ([cta][16 tiles][mma start, mma issued, epilogue start, epilogue end]) */
 spx_status spx_debug_gemm_trace(int64_t* out, int64_t n);

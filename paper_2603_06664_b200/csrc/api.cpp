@@ -5,6 +5,7 @@
 #include <mutex>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -880,6 +881,14 @@ spx_status spx_debug_gemm_trace(int64_t* out, int64_t n) {
         SPX_CUDA(cudaDeviceSynchronize());
         SPX_CUDA(cudaMemcpy(out, gemm_trace_buffer(), static_cast<size_t>(n) * 8,
                             cudaMemcpyDeviceToHost));
+    });
+}
+
+spx_status spx_debug_spans(uint64_t* out, int64_t capacity, int64_t* count) {
+    return guarded([&] {
+        require(count, SPX_ERR_CONFIG, "null count");
+        *count = span_count();
+        if (out) span_dump(out, std::min(capacity / 2, *count));
     });
 }
 

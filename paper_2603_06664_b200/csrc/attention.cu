@@ -60,6 +60,7 @@ struct AttnParams {
     const uint8_t* pf[2];  // L2 prefetch ranges (see AttnOperands::l2_prefetch)
     int64_t pf_bytes[2];
     long long* trace;      // SPX_ATTN_EXPERIMENT=5: per-CTA clock64 marks [cta][16][4]
+    unsigned long long* span;  // SPX_SPAN_TRACE
 };
 
 __device__ __forceinline__ void attn_mark(const AttnParams& p, int k) {
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     pdl_trigger();
+    span_begin(p.span);
     const int q_tile = blockIdx.x;
     const int head = blockIdx.y;
     const int split = blockIdx.z;
@@ -752,6 +754,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         cluster_sync_all();
     else
         __syncthreads();
+    span_end(p.span);
     if (warp == 2) {
         tc_fence_after();
         if constexpr (kPair)
@@ -923,6 +926,7 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     }();
     p.experiment = experiment;
     if (experiment == 5) p.trace = gemm_trace_buffer();
+    p.span = span_slot();
     for (int i = 0; i < 8; ++i) p.out_base[i] = o.out_base[i];
     p.rows_per_chunk = o.rows_per_chunk;
     for (int r = 0; r < 2; ++r) {

@@ -71,6 +71,12 @@ int device_sm_count(int device);
 // turns it off (plain stream serialisation).
 bool pdl_enabled();
 
+// Kernel span tracing (SPX_SPAN_TRACE=1, profiling only): each traced launch gets a slot
+// {earliest CTA start, latest CTA end} in globaltimer ns; nullptr when tracing is off.
+unsigned long long* span_slot();
+int64_t span_count();
+void span_dump(uint64_t* out, int64_t n);
+
 #ifdef __CUDACC__
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -52,6 +52,7 @@ struct GemmParams {
     int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation,
                       // 5 = per-tile clock64 timeline of the pair kernel into `trace`
     long long* trace;  // [cta][16 tiles][4]: mma start, mma issued, epilogue start, end
+    unsigned long long* span;  // SPX_SPAN_TRACE
 };
 
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int it, int kind) {
@@ -264,6 +265,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     pdl_trigger();  // the next kernel may launch; it waits for this grid before its main loop
+    span_begin(p.span);
+    if (threadIdx.x == 0 && p.experiment == 5) {
+        p.trace[(blockIdx.x * 16 + 15) * 4 + 0] = clock64();
+        p.trace[(blockIdx.x * 16 + 14) * 4 + 0] = static_cast<long long>(globaltimer_ns());
+    }
     const int num_tiles = p.num_m_tiles * p.num_n_tiles;
     const int num_kt = p.K / kBK;
 
@@ -289,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0 && p.experiment == 5) p.trace[(blockIdx.x * 16 + 15) * 4 + 1] = clock64();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -382,6 +389,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     __syncthreads();
+    span_end(p.span);
+    if (threadIdx.x == 0 && p.experiment == 5) {
+        p.trace[(blockIdx.x * 16 + 15) * 4 + 2] = clock64();
+        p.trace[(blockIdx.x * 16 + 14) * 4 + 1] = static_cast<long long>(globaltimer_ns());
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
@@ -432,6 +444,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     pdl_trigger();  // the next kernel may launch; it waits for this grid before its main loop
+    span_begin(p.span);
+    if (threadIdx.x == 0 && p.experiment == 5) {
+        p.trace[(blockIdx.x * 16 + 15) * 4 + 0] = clock64();
+        p.trace[(blockIdx.x * 16 + 14) * 4 + 0] = static_cast<long long>(globaltimer_ns());
+    }
     const int cta = static_cast<int>(cluster_ctarank());
     const bool leader = cta == 0;
     const int pair = blockIdx.x / 2;
@@ -459,6 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0 && p.experiment == 5) p.trace[(blockIdx.x * 16 + 15) * 4 + 1] = clock64();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -562,6 +580,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     cluster_sync_all();
+    span_end(p.span);
+    if (threadIdx.x == 0 && p.experiment == 5) {
+        p.trace[(blockIdx.x * 16 + 15) * 4 + 2] = clock64();
+        p.trace[(blockIdx.x * 16 + 14) * 4 + 1] = static_cast<long long>(globaltimer_ns());
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc_pair<kTmemCols>(tmem_base);
@@ -714,7 +737,10 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
         return e ? std::atoi(e) : 0;
     }();
     p.experiment = experiment;
-    if (experiment == 5) p.trace = gemm_trace_buffer();
+    // 5: trace the QKV launches (RoPE epilogue) only; 7: every launch
+    if ((experiment == 5 && rope) || experiment == 7) p.trace = gemm_trace_buffer();
+    p.experiment = p.trace ? 5 : (experiment == 5 || experiment == 7 ? 0 : experiment);
+    p.span = span_slot();
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         launch_pdl(gemm_bf16_tn_pair_kernel<256>, dim3(plan.grid), dim3(kThreads),

@@ -23,6 +23,20 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns();
+// span tracing (common.hpp span_slot): one thread per CTA
+__device__ __forceinline__ void span_begin(unsigned long long* s) {
+    if (s && threadIdx.x == 0) atomicMin(s, globaltimer_ns());
+}
+__device__ __forceinline__ void span_end(unsigned long long* s) {
+    if (s && threadIdx.x == 0) atomicMax(s + 1, globaltimer_ns());
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -70,13 +70,27 @@ def main():
         tr = np.zeros(1024 * 16 * 4, dtype=np.int64)
         check(lib().spx_debug_gemm_trace(tr.ctypes.data, tr.size))
         tr = tr.reshape(1024, 16, 4)
+        g = tr[:, 14, :2]
+        live = g[:, 0] > 0
+        ent, ex = g[live, 0], g[live, 1]
+        print(json.dumps({"ctas": int(live.sum()),
+                          "entry_spread_us": round(float(ent.max() - ent.min()) / 1e3, 2),
+                          "exit_spread_us": round(float(ex.max() - ex.min()) / 1e3, 2),
+                          "span_us": round(float(ex.max() - ent.min()) / 1e3, 2),
+                          "entry_us_sorted_pct": [round(float(np.percentile(ent - ent.min(), q)) / 1e3, 2)
+                                                  for q in (10, 50, 90, 100)]}))
         for cta in (0, 1, 2, 3, 100, 101):
             # pair kernel: odd CTAs have no MMA marks (relative to their first epilogue);
             # single-CTA kernel: every CTA has all four
             base = tr[cta, 0, 0] if tr[cta, 0, 0] else tr[cta, 0, 2]
             rows = [[round((v - base) / 1965.0, 2) if v else None
                      for v in tr[cta, it]] for it in range(6) if tr[cta, it].any()]
-            print(json.dumps({"cta": cta, "us_since_first[mma_start,mma_issued,epi_start,epi_end]": rows}))
+            ent = tr[cta, 15]
+            print(json.dumps({"cta": cta, "us_since_first[mma_start,mma_issued,epi_start,epi_end]": rows,
+                              "entry_to_prologue_end_us": round((ent[1] - ent[0]) / 1965.0, 2),
+                              "prologue_end_to_first_mma_us": round((tr[cta, 0, 0] - ent[1]) / 1965.0, 2)
+                              if tr[cta, 0, 0] else None,
+                              "entry_to_exit_us": round((ent[2] - ent[0]) / 1965.0, 2)}))
     print(json.dumps({"label": args.label, "P": args.P, "fuse_rope": not args.no_fuse_rope, "wan": args.wan,
                       "env": {k: v for k, v in os.environ.items() if k.startswith("SPX_")},
                       "chunk_ms": round(ms, 3), "frames_per_s": round(3e3 / ms, 2),
