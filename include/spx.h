@@ -63,6 +63,9 @@ spx_status spx_layer_weights(uint64_t seed, int64_t layer, int64_t model_dim, do
                              double* wk, double* wv, double* wo);
 /* host fp64 -> bf16 (round to nearest even), n elements */
 spx_status spx_f64_to_bf16(const double* in, uint16_t* out, int64_t n);
+/* tensor_checksum (proj/src/report.cpp:264-279): FNV-1a over the fp64 bytes, 16 hex digits +
+ * NUL in out[17] (reference-compatible reports of device outputs) */
+spx_status spx_checksum_f64(const double* p, int64_t n, char out[17]);
 
 /* ---------------------------------------------------------------------------------------
  * 3-D RoPE table (BandSplit / precompute_frequencies: proj/src/rope.cpp:15-64,

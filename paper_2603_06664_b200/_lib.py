@@ -166,6 +166,7 @@ _SIGS = [
     ("spx_engine_set_profile", c_int, [c_void_p, c_int32]),
     ("spx_engine_stats", c_int, [c_void_p, POINTER(CommStats)]),
     ("spx_world_create_peer", c_int, [c_int, c_int, c_int, c_void_p]),
+    ("spx_checksum_f64", c_int, [c_void_p, c_int64, c_char_p]),
     ("spx_engine_set_modulation", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     ("spx_layernorm_modulate", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_float,
                                        c_void_p]),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -841,6 +842,24 @@ spx_status spx_layernorm_modulate(const void* x, void* y, int64_t tokens, int64_
         require(x && y && shift && scale, SPX_ERR_CONFIG, "null buffer");
         ln_modulate_run(static_cast<const bf16*>(x), static_cast<bf16*>(y), tokens, dim, shift,
                         scale, eps, as_stream(stream));
+    });
+}
+
+// tensor_checksum (proj/src/report.cpp:264-279): FNV-1a over the little-endian bytes of the
+// fp64 values, as 16 hex digits (host utility for reference-compatible reports)
+spx_status spx_checksum_f64(const double* p, int64_t n, char out[17]) {
+    return guarded([&] {
+        require(out && (p || n == 0) && n >= 0, SPX_ERR_CONFIG, "null argument");
+        uint64_t h = 0xcbf29ce484222325ULL;
+        for (int64_t i = 0; i < n; ++i) {
+            uint64_t bits;
+            std::memcpy(&bits, &p[i], 8);
+            for (int b = 0; b < 8; ++b) {
+                h ^= (bits >> (8 * b)) & 0xFFULL;
+                h *= 0x100000001b3ULL;
+            }
+        }
+        std::snprintf(out, 17, "%016llx", static_cast<unsigned long long>(h));
     });
 }
 

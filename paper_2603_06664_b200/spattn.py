@@ -597,6 +597,50 @@ class Engine:
         return s.as_dict()
 
 
+def tensor_checksum(x: np.ndarray) -> str:
+    """tensor_checksum (report.cpp:264-279) of the values as fp64."""
+    d = np.ascontiguousarray(x, dtype=np.float64)
+    out = ctypes.create_string_buffer(17)
+    check(lib().spx_checksum_f64(d.ctypes.data, d.size, out))
+    return out.value.decode()
+
+
+def generation_result_json(cfg: "GenerationConfig", block_outputs: np.ndarray, stats: dict,
+                           stage_us_total: Optional[dict] = None, calls: Optional[int] = None,
+                           wall_ms: Optional[float] = None) -> dict:
+    """to_json(GenerationResult) (report.cpp:87-175): the reference's report layout for a
+    device run, so its report tooling reads GPU runs. block_outputs: (blocks, L, H, D) values
+    (bf16 bits or floats); stats: Engine.stats(); element width 2 (bf16)."""
+    out = np.asarray(block_outputs)
+    if out.dtype == np.uint16:
+        out = bf16_bits_to_float(out)
+    bits = cfg.ablation.bits()
+    variant = "baseline" if bits == 0 else "optimized"
+    ab = {"use_fused_all_to_all": bool(bits & 1), "use_local_rope": bool(bits & 2),
+          "use_precomputed_freqs": bool(bits & 4)}
+    order = (["qkv", "rope", "gather_or_fused", "cache", "attention", "output_exchange"] if bits & 2
+             else ["qkv", "gather_or_fused", "rope", "cache", "attention", "output_exchange"])
+    g = cfg.grid_per_block
+    conf = {"frames_per_block": g.frames, "grid_h": g.height, "grid_w": g.width,
+            "num_blocks": cfg.num_blocks, "layers": cfg.layers, "denoise_steps": cfg.denoise_steps,
+            "batch": cfg.batch, "heads": cfg.heads, "head_dim": cfg.head_dim,
+            "world_size": cfg.world_size, "seed": cfg.seed, "variant": variant, "ablation": ab,
+            "element_width_bytes": 2, "rope_base": cfg.rope_base,
+            "force_start_frame_zero": cfg.force_start_frame_zero,
+            "window_frames": cfg.window_frames}
+    blocks = []
+    for b in range(out.shape[0]):
+        blocks.append({"block": b, "start_frame": 0 if cfg.force_start_frame_zero else b * g.frames,
+                       "shape": [1, int(out.shape[1]), cfg.heads, cfg.head_dim],
+                       "checksum": tensor_checksum(out[b])})
+    ledger = dict(stats)
+    ledger["bytes_sent_at_width"] = ledger["elements_sent"] * 2
+    profile = {"calls": calls if calls is not None else cfg.total_calls(),
+               "wall_ms": wall_ms, "stage_order": order,
+               "stage_us_total": stage_us_total or {k: 0.0 for k in order}, "ledger": ledger}
+    return {"config": conf, "blocks": blocks, "profile": profile}
+
+
 def bf16_bits_to_float(bits: np.ndarray) -> np.ndarray:
     b = np.asarray(bits, dtype=np.uint16)
     return (b.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)

@@ -143,3 +143,18 @@ def test_config_validation_mirrors_reference():
         spattn.GenerationConfig(grid_per_block=spattn.GridSpec(0, 4, 4), heads=4, head_dim=64).validate()
     with pytest.raises(spattn.UnsupportedError):
         spattn.GenerationConfig().validate()  # reference default D = 16: no tcgen05 path
+
+
+def test_checksum_matches_reference_report_format():
+    """spx_checksum_f64 == tensor_checksum (report.cpp:264-279): the C1 tiny P=1 output of the
+    pinned oracle hashes to the reference's published block-0 checksum."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2603_06664_b200 import spattn
+
+    x = np.random.default_rng(0).standard_normal((5, 7))
+    assert spattn.tensor_checksum(x) == oracle.checksum(x)
+    out = oracle.generate(frames=3, grid_h=8, grid_w=8, num_blocks=1, layers=2, steps=2, heads=4,
+                          head_dim=64)
+    assert spattn.tensor_checksum(out[0]) == "ca4d9813b02c388e"

@@ -465,3 +465,23 @@ def test_generate_block_host_noise_pipeline_matches_device_path(cuda):
                                                      ptr_array([od.data_ptr()])))
         check(lib().spx_engine_synchronize(e._h))
         assert np.array_equal(got[b].reshape(L, C), od.cpu().numpy().view(np.uint16)), b
+
+
+def test_generation_report_matches_reference_layout(cuda):
+    """generation_result_json: the reference's to_json(GenerationResult) layout
+    (report.cpp:87-175) for a device run: config keys, per-block checksums of the outputs,
+    the ledger with bytes_sent_at_width."""
+    s = spattn()
+    cfg = cfg_from(TINY, world=2)
+    eng = s.Engine(cfg)
+    out = eng.generate()
+    rep = s.generation_result_json(cfg, out, eng.stats())
+    assert set(rep) == {"config", "blocks", "profile"}
+    assert rep["config"]["variant"] == "optimized" and rep["config"]["world_size"] == 2
+    assert [b["start_frame"] for b in rep["blocks"]] == [0, 3, 6]
+    vals = s.bf16_bits_to_float(out)
+    assert all(b["checksum"] == s.tensor_checksum(vals[i]) for i, b in enumerate(rep["blocks"]))
+    st = eng.stats()
+    assert rep["profile"]["ledger"]["rounds"] == st["rounds"]
+    assert rep["profile"]["ledger"]["bytes_sent_at_width"] == 2 * st["elements_sent"]
+    assert rep["profile"]["stage_order"][:2] == ["qkv", "rope"]
