@@ -257,8 +257,7 @@ void Engine::peer_barrier(RankState& rs, int slot) {
     const uint64_t e = ++epoch_[slot];
     PeerFlags f{};
     for (int r = 0; r < P_; ++r) f.rank_flags[r] = peers_[static_cast<size_t>(r)].flags;
-    peer_signal_run(f, static_cast<int>(P_), rs.rank, slot, e, rs.stream);
-    peer_wait_run(rs.flags, static_cast<int>(P_), slot, e, rs.stream);
+    peer_barrier_run(f, rs.flags, static_cast<int>(P_), rs.rank, slot, e, rs.stream);
 }
 
 void Engine::allocate() {

@@ -191,6 +191,9 @@ struct PeerFlags {
 void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint64_t epoch,
                      cudaStream_t s);
 void peer_wait_run(uint64_t* my_flags, int world, int slot, uint64_t epoch, cudaStream_t s);
+// signal + wait as one PDL-chained 1-warp launch (the engine's default)
+void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
+                      uint64_t epoch, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // Kd: naive fp32 SIMT reference kernels (GPU oracle at shapes the CPU oracle cannot reach).

@@ -8,8 +8,11 @@
 // shapes the CPU oracle cannot reach in seconds.
 #include "common.hpp"
 #include "kernels.hpp"
+#include "sm100.cuh"
 
 namespace spx {
+
+using namespace sm100;
 
 namespace {
 
@@ -21,6 +24,31 @@ __global__ void peer_signal_kernel(PeerFlags f, int world, int my_rank, int slot
     // release at system scope: this stream's earlier kernels (stores into peer memory
     // included) happen-before the flag as seen by the peer
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+}
+
+// signal + wait in one 1-warp launch, chained with PDL: it starts during the previous
+// kernel's tail, griddepcontrol.wait makes that kernel's stores (peer stores included)
+// complete before the release, and the next kernel's prologue overlaps the spin
+__global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, int my_rank, int slot,
+                                    uint64_t epoch) {
+    pdl_trigger();
+    pdl_wait();
+    const int r = threadIdx.x;
+    if (r < world) {
+        uint64_t* dst = f.rank_flags[r] + slot * world + my_rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+    }
+    __syncwarp();
+    if (r < world) {
+        const uint64_t* src = my_flags + slot * world + r;
+        uint64_t v = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
+            if (v >= epoch) break;
+            __nanosleep(64);
+        }
+    }
+    __syncwarp();
 }
 
 __global__ void peer_wait_kernel(uint64_t* flags, int world, int slot, uint64_t epoch) {
@@ -137,6 +165,12 @@ void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint6
                      cudaStream_t s) {
     peer_signal_kernel<<<1, 32, 0, s>>>(f, world, my_rank, slot, epoch);
     SPX_CUDA_LAUNCH();
+    count_launch();
+}
+
+void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
+                      uint64_t epoch, cudaStream_t s) {
+    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot, epoch);
     count_launch();
 }
 

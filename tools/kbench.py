@@ -71,8 +71,13 @@ def attn(iters):
 
 
 def gemm(iters):
-    for M, K, N in [(4680, 1536, 4608), (4680, 1536, 1536), (2340, 1536, 4608), (1170, 1536, 4608),
-                    (585, 1536, 4608), (8192, 8192, 8192)]:
+    shapes = [(4680, 1536, 4608), (4680, 1536, 1536), (2340, 1536, 4608), (1170, 1536, 4608),
+              (585, 1536, 4608), (2340, 1536, 1536), (1170, 1536, 1536), (585, 1536, 1536),
+              (8192, 8192, 8192)]
+    only = os.environ.get("KBENCH_GEMM_SHAPES")  # e.g. "585x1536x4608,1170x1536x1536"
+    if only:
+        shapes = [tuple(int(v) for v in t.split("x")) for t in only.split(",")]
+    for M, K, N in shapes:
         x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
         y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
