@@ -1,4 +1,7 @@
-O=gpurun_out/r01ai; mkdir -p $O
-timeout 900 python -m pytest tests -x -q -m gpu > $O/pytest_gpu.log 2>&1; echo rc=$? >> $O/pytest_gpu.log
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --same-device --steps 2 --warmup 1 --skip-long-video --no-cpu-baseline > $O/bench_p2.json 2> $O/bench_p2.err; echo rc=$? >> $O/bench_p2.err
-tail -2 $O/pytest_gpu.log; tail -1 $O/bench_p2.err; head -c 400 $O/bench_p2.json
+O=gpurun_out/r01ak; mkdir -p $O
+for i in 1 2 3; do for v in base slots4 slots3 s4pfw; do
+  for shp in 4680x4680x12 4680x32760x12 2340x4680x3; do
+    echo -n "$v " >> $O/ab.txt; SPX_LIB=paper_2603_06664_b200/variants/$v.so python tools/kbench.py attn:$shp 30 >> $O/ab.txt 2>&1
+  done
+done; done
+cat $O/ab.txt
