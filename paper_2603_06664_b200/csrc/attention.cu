@@ -10,6 +10,12 @@
 #include <algorithm>
 
 #include <atomic>
+#include <cstdio>
+#include <vector>
+#include <tuple>
+#include <mutex>
+#include <map>
+#include <functional>
 #include <cstdlib>
 
 #include "common.hpp"
@@ -49,8 +55,11 @@ struct AttnParams {
     int rows_per_chunk;
     int64_t out_row_stride;
     int64_t out_batch_stride;
-    // split-KV (v2 kernel): gridDim.z CTAs per (query tile, head)
+    // split-KV (v2 kernel). Cluster modes: gridDim.z CTAs per (query tile, head). Mode 0: a
+    // 1-D grid; tiles (t = head * qt + q_tile) below n_full run unsplit, the rest in `splits`
     int splits;
+    int n_full;
+    int qt;           // query tiles per head (unpadded)
     int heads;
     int q_tiles;
     int* counters;   // [q_tiles][heads], zero between launches
@@ -263,13 +272,32 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int lane = threadIdx.x % 32;
     pdl_trigger();
     span_begin(p.span);
-    const int q_tile = blockIdx.x;
-    const int head = blockIdx.y;
-    const int split = blockIdx.z;
+    int q_tile, head, split, ns;
+    if constexpr (kCluster) {
+        q_tile = blockIdx.x;
+        head = blockIdx.y;
+        split = blockIdx.z;
+        ns = p.splits;
+    } else {  // full tiles first (block order ~ issue order), then the split ones
+        const int b = static_cast<int>(blockIdx.x);
+        int t;
+        if (b < p.n_full) {
+            t = b;
+            split = 0;
+            ns = 1;
+        } else {  // split index outermost: concurrent CTAs share a kv range (L2 reuse)
+            const int k = b - p.n_full;
+            const int nsplit_tiles = p.qt * p.heads - p.n_full;
+            t = p.n_full + k % nsplit_tiles;
+            split = k / nsplit_tiles;
+            ns = p.splits;
+        }
+        q_tile = t % p.qt;
+        head = t / p.qt;
+    }
     // this CTA's share [tb, tb + n_total) of the kv tiles, halved between the warpgroups
-    const int tb = static_cast<int>((static_cast<int64_t>(split) * p.total_tiles) / p.splits);
-    const int n_total =
-        static_cast<int>((static_cast<int64_t>(split + 1) * p.total_tiles) / p.splits) - tb;
+    const int tb = static_cast<int>((static_cast<int64_t>(split) * p.total_tiles) / ns);
+    const int n_total = static_cast<int>((static_cast<int64_t>(split + 1) * p.total_tiles) / ns) - tb;
     const int n0 = (n_total + 1) / 2;
     const int n1 = n_total - n0;
     __shared__ int s_last;
@@ -600,7 +628,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         const uint32_t t_o0 = tmem_base + 256 + lane_off;
         const uint32_t t_o1 = tmem_base + 384 + lane_off;
-        if (p.splits == 1) {
+        if (ns == 1) {
 #pragma unroll 1
             for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
                 uint32_t o0[32], o1[32];
@@ -675,14 +703,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 __threadfence();
                 int* ctr = p.counters + tile;
                 const int prev = atomicAdd(ctr, 1);
-                s_last = prev == p.splits - 1;
+                s_last = prev == ns - 1;
                 if (s_last) *ctr = 0;  // every split has arrived: re-arm for the next launch
             }
             named_bar_sync(1, 256);
             if (s_last) {
                 __threadfence();
                 float lse_max = -INFINITY;
-                for (int z = 0; z < p.splits; ++z) lse_max = fmaxf(lse_max, __ldcg(lse_tile + z * kBQ + r));
+                for (int z = 0; z < ns; ++z) lse_max = fmaxf(lse_max, __ldcg(lse_tile + z * kBQ + r));
                 float acc[D / 2];
                 float wsum;
                 {  // own partial (staging buffer 0)
@@ -702,7 +730,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
                 // the other splits in batches of kMaxOthers (other index o -> split z)
                 uint32_t phase = 0;
-                const int others = p.splits - 1;
+                const int others = ns - 1;
                 for (int o0 = 0; o0 < others; o0 += kMaxOthers) {
                     const int cnt = min(kMaxOthers, others - o0);
                     named_bar_sync(1, 256);  // buffers 1.. are free (previous batch read)
@@ -835,13 +863,63 @@ std::atomic<int> g_forced_splits{[] {  // tuning override: SPX_ATTN_SPLITS=<1..8
 
 void attn_force_splits(int s) { g_forced_splits.store(s, std::memory_order_relaxed); }
 
+namespace {
+// Mixed layout for mode 0: the first n_full (query tile, head) tiles unsplit, the remaining
+// ones in s2 splits, scored by a greedy list-scheduling simulation of the CTAs in block order
+// on sm_count SMs with the same per-CTA costs as choose_splits (full: 3.3 + tiles, split:
+// 9 + tiles / s2, in kv-tile units). E.g. 222 tiles x 37 kv tiles on 148 SMs: 148 full + 74
+// tiles in halves (one full and one half CTA per SM) instead of 1.5 waves of full CTAs.
+struct Layout {
+    int n_full, s2;
+};
+double simulate(int64_t full, int64_t split_ctas, double t_full, double t_split, int sms) {
+    // full CTAs land round-robin (identical durations); split CTAs greedily on the earliest
+    // free SM (min-heap)
+    std::vector<double> busy(static_cast<size_t>(sms));
+    for (int i = 0; i < sms; ++i)
+        busy[static_cast<size_t>(i)] = t_full * static_cast<double>(full / sms + (i < full % sms ? 1 : 0));
+    std::make_heap(busy.begin(), busy.end(), std::greater<double>());
+    for (int64_t i = 0; i < split_ctas; ++i) {
+        std::pop_heap(busy.begin(), busy.end(), std::greater<double>());
+        busy.back() += t_split;
+        std::push_heap(busy.begin(), busy.end(), std::greater<double>());
+    }
+    return *std::max_element(busy.begin(), busy.end());
+}
+Layout choose_layout(int64_t T, int64_t tiles, int sms, int cap) {
+    static std::mutex mu;
+    static std::map<std::tuple<int64_t, int64_t, int, int>, Layout> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(T, tiles, sms, cap);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    Layout best{static_cast<int>(T), 1};
+    double best_t = simulate(T, 0, 3.3 + static_cast<double>(tiles), 0.0, sms);
+    for (int s2 = 2; s2 <= cap; ++s2) {
+        if (tiles / s2 < 2) break;
+        const double ts = 9.0 + static_cast<double>(ceil_div(tiles, s2));
+        // the split part beyond ~2 waves of CTAs never beats fewer, longer splits
+        for (int64_t F = T - 1; F >= std::max<int64_t>(0, T - 2 * sms); --F) {
+            const double t = simulate(F, (T - F) * s2, 3.3 + static_cast<double>(tiles), ts, sms);
+            if (t < best_t * 0.97) {  // a split must win clearly (the model is coarse)
+                best_t = t;
+                best = {static_cast<int>(F), s2};
+            }
+        }
+    }
+    cache[key] = best;
+    return best;
+}
+}  // namespace
+
 int attn_max_splits(const AttnOperands& ops, int sm_count) {
     const int forced = g_forced_splits.load(std::memory_order_relaxed);
     if (forced) return forced;
     // the workspace is sized for the longest kv range the buffers can hold (splits grow
     // with the kv length)
     const int64_t n = ceil_div(static_cast<int64_t>(ops.sq), kBQ) * ops.heads * ops.batch;
-    return choose_splits(n, ceil_div(ops.kv_rows, kBKV), sm_count, 8);
+    const int64_t tiles = ceil_div(ops.kv_rows, kBKV);
+    return std::max(choose_splits(n, tiles, sm_count, 8), choose_layout(n, tiles, sm_count, 8).s2);
 }
 
 size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits) {
@@ -944,13 +1022,35 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         SPX_CUDA(cudaGetDevice(&dev));
         const int64_t n = ceil_div(static_cast<int64_t>(o.sq), kBQ) * o.heads * o.batch;
         const bool forced = g_forced_splits.load(std::memory_order_relaxed) != 0;
-        const int want = forced ? plan.max_splits
-                                : choose_splits(n, p.total_tiles, device_sm_count(dev), plan.max_splits);
-        p.splits = std::max(1, std::min(want, p.total_tiles / 2));
+        static const int mode_env = [] {
+            const char* e = std::getenv("SPX_ATTN_KERNEL");
+            return e && (std::string(e) == "pair" || std::string(e) == "mcast") ? 1 : 0;
+        }();
+        p.qt = static_cast<int>(ceil_div(o.sq, kBQ));
+        if (forced || mode_env || o.head_dim != 128) {  // uniform splits
+            const int want = forced ? plan.max_splits
+                                    : choose_splits(n, p.total_tiles, device_sm_count(dev), plan.max_splits);
+            p.splits = std::max(1, std::min(want, p.total_tiles / 2));
+            p.n_full = p.splits == 1 ? static_cast<int>(n) : 0;
+        } else {
+            Layout lay = choose_layout(n, p.total_tiles, device_sm_count(dev), plan.max_splits);
+            static const char* forced_layout = std::getenv("SPX_ATTN_LAYOUT");  // "F,s2" (tuning)
+            if (forced_layout) {
+                int f = 0, s2 = 1;
+                if (std::sscanf(forced_layout, "%d,%d", &f, &s2) == 2)
+                    lay = {f, std::min(s2, plan.max_splits)};
+            }
+            static const bool verbose = std::getenv("SPX_ATTN_VERBOSE") != nullptr;
+            if (verbose)
+                std::fprintf(stderr, "attention layout: T=%lld tiles=%d -> n_full=%d s2=%d (cap %d)\n",
+                             static_cast<long long>(n), p.total_tiles, lay.n_full, lay.s2, plan.max_splits);
+            p.splits = std::max(1, std::min(lay.s2, p.total_tiles / 2));
+            p.n_full = p.splits == 1 ? static_cast<int>(n) : lay.n_full;
+        }
     }
     p.heads = o.heads;
     p.q_tiles = static_cast<int>((ceil_div(o.sq, kBQ) + 1) & ~1);  // workspace stride (pairs)
-    if (p.splits > 1) {
+    if (p.splits > 1 && p.n_full < p.qt * o.heads) {
         const size_t rows = static_cast<size_t>(p.q_tiles) * kBQ;
         uint8_t* ws = static_cast<uint8_t*>(o.workspace);
         const size_t ctr = (rows / kBQ * o.heads * sizeof(int) + 255) / 256 * 256;
@@ -979,12 +1079,13 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             attn_v2_launch<128, 1>(grid, plan, p, stream);
         else
             attn_v2_launch<128, 2>(grid, plan, p, stream);
-    } else if (o.head_dim == 128) {
-        grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_launch<128, 0>(grid, plan, p, stream);
-    } else {
-        grid.z = static_cast<unsigned>(p.splits);
-        attn_v2_launch<64, 0>(grid, plan, p, stream);
+    } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
+        const int64_t T = static_cast<int64_t>(p.qt) * o.heads;
+        const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
+        if (o.head_dim == 128)
+            attn_v2_launch<128, 0>(g1, plan, p, stream);
+        else
+            attn_v2_launch<64, 0>(g1, plan, p, stream);
     }
     SPX_CUDA_LAUNCH();
     count_launch();
