@@ -289,9 +289,10 @@ def main():
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # attention launches bracketed by CUDA events on the engine stream (profile level 2: two
-    # events per call around the attention kernel, nothing else)
-    _set_profile(eng, 2)
+    # attention launches bracketed by CUDA events on the engine stream (profile level 3: two
+    # events around the attention kernel of every 8th layer call -- a live sample over the
+    # timed region that leaves the launch chaining of the other calls undisturbed)
+    _set_profile(eng, 3)
     tw0 = time.perf_counter()
     ev0.record(stream)
     for _ in range(args.steps):

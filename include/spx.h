@@ -316,7 +316,8 @@ spx_status spx_engine_synchronize(spx_engine* engine);
  * (sp_attention.hpp:92-97); calls = number of profiled layer calls */
 spx_status spx_engine_stage_times(spx_engine* engine, double out_ms[6], int64_t* calls);
 spx_status spx_engine_reset_stage_times(spx_engine* engine);
-/* CUDA-event stage timing for subsequent calls: 0 off, 1 every stage, 2 attention only */
+/* CUDA-event stage timing for subsequent calls: 0 off, 1 every stage, 2 attention only,
+ * 3 attention only on every 8th call (a sample that keeps PDL chaining of the others) */
 spx_status spx_engine_set_profile(spx_engine* engine, int32_t on);
 spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
 /* PEER transport: this rank's exchange buffers as CUDA IPC handles (an opaque blob of

@@ -816,7 +816,7 @@ spx_status spx_engine_reset_stage_times(spx_engine* engine) {
 spx_status spx_engine_set_profile(spx_engine* engine, int32_t on) {
     return guarded([&] {
         require_ptr(engine, "engine");
-        require(on >= 0 && on <= 2, SPX_ERR_CONFIG, "profile level must be 0, 1 or 2");
+        require(on >= 0 && on <= 3, SPX_ERR_CONFIG, "profile level must be 0, 1, 2 or 3");
         engine->e->set_profile(on);
     });
 }

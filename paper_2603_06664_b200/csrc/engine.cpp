@@ -585,7 +585,10 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
     const int64_t slab = Lp_ * Hl_ * D_;
 
     StageEvents* prof = nullptr;
-    if (cfg_.profile) {
+    // level 3: the attention bracket on every 8th call only (a live sample of the kernel's
+    // duration that leaves the PDL chaining of the other calls intact)
+    const bool sampled = cfg_.profile != 3 || (profile_seq_++ % 8) == 0;
+    if (cfg_.profile && sampled) {
         SPX_CUDA(cudaSetDevice(ranks_[0].device));
         if (free_events_.empty()) {
             StageEvents se;
@@ -595,7 +598,7 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         pending_events_.push_back(free_events_.back());
         free_events_.pop_back();
         prof = &pending_events_.back();
-        prof->level = cfg_.profile;
+        prof->level = cfg_.profile == 1 ? 1 : 2;
     }
     auto mark = [&](int li, int k) {
         if (prof && li == 0 && (prof->level == 1 || k == 4 || k == 5))

@@ -115,7 +115,8 @@ class Engine {
     void synchronize();
     void stage_times(double out_ms[6], int64_t* calls);
     void reset_stage_times();
-    // 0 off, 1 every stage (six CUDA-event intervals per call), 2 attention launch only
+    // 0 off, 1 every stage (six CUDA-event intervals per call), 2 attention launch only,
+    // 3 attention launch of every 8th call
     void set_profile(int level) { cfg_.profile = level; }
     spx_comm_stats stats() const { return world_->stats(); }
     // PEER transport: CUDA IPC handles of this rank's exchange buffers, and the mapping of
@@ -178,6 +179,7 @@ class Engine {
     std::vector<StageEvents> free_events_;
     double stage_ms_[6] = {0, 0, 0, 0, 0, 0};
     int64_t profiled_calls_ = 0;
+    int64_t profile_seq_ = 0;
 };
 
 // G (head groups) for P ranks and H heads: the largest divisor of P that divides H
