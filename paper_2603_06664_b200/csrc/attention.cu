@@ -40,6 +40,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 // P_i hand-off to the MMA thread: one arrival per softmax warp (after __syncwarp) instead of
 // one per thread
+// profiling-only variants of the hot loop (SPX_ATTN_EXPERIMENT=2: exponentials on the FMA
+// pipe) are compiled in only with -DSPX_ATTN_PROFILING=1: a runtime branch inside the
+// unrolled exp loop is predicated, i.e. it costs issue slots on every element
+#ifndef SPX_ATTN_PROFILING
+#define SPX_ATTN_PROFILING 0
+#endif
 #ifndef SPX_PFULL_PER_WARP
 #define SPX_PFULL_PER_WARP 0
 #endif
@@ -572,15 +578,18 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 if ((e & 7) >= 8 - SPX_POLY_OF_8) {  // part of the exponentials on the FMA pipe
                     pr = ex2_poly2(x);
                 } else {
+#if SPX_ATTN_PROFILING
                     if (p.experiment == 2) {  // profiling: no MUFU
                         pr.x = fmaf(x.x, 0.03125f, 1.0f);
                         pr.y = fmaf(x.y, 0.03125f, 1.0f);
-                    } else {
+                    } else
+#endif
+                    {
                         pr.x = ex2_approx(x.x);
                         pr.y = ex2_approx(x.y);
                     }
                 }
-                ls[e & 3] = fadd2(ls[e & 3], pr);
+                ls[e & 3] = e < 4 ? pr : fadd2(ls[e & 3], pr);  // (unrolled: no add of 0)
                 pk[e] = pack_bf16x2(pr.x, pr.y);
             }
             {
