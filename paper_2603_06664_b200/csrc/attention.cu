@@ -31,7 +31,6 @@ namespace {
 
 constexpr int kBQ = 128;     // query rows per CTA
 constexpr int kBKV = 128;    // kv rows per tile
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // exponentials computed by the FMA-pipe polynomial, out of every 8 (the rest on MUFU.EX2)
 // (measured on B200: 0 of 8 is fastest -- 0.741 vs 0.764 ms at 4680 x 32760 x 12 with 2 of 8;
 // MUFU.EX2 is not the limit once the MMA issue is warp-uniform)
@@ -524,30 +523,71 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
                 continue;
             }
+            // Exponent offset: the row max of the WG's FIRST tile only. Softmax is invariant to
+            // the offset and P (bf16) / O, l (fp32) have the range for values far above 1, so
+            // later tiles skip the per-tile max (43 3-input max ops per row); the tile's row sum
+            // guards against overflow: if any exp exceeded 2^64 (a logit > offset + 64, in log2
+            // units; rare), the tile is redone with its true max and O, l rescaled.
             uint32_t u[kBKV];
+            auto load_s = [&]() {
 #pragma unroll
-            for (int c = 0; c < kBKV / 32; ++c)
-                tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
-            tmem_ld_wait();
-            if (valid < kBKV) {  // ragged tail tile only: masked logits -> -inf (exp -> 0)
+                for (int c = 0; c < kBKV / 32; ++c)
+                    tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+                tmem_ld_wait();
+                if (valid < kBKV) {  // ragged tail tile only: masked logits -> -inf (exp -> 0)
 #pragma unroll
-                for (int c = 0; c < kBKV; ++c)
-                    if (c >= valid) u[c] = 0xff800000u;
-            }
-            // row max: four independent 3-input max chains
-            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                    for (int c = 0; c < kBKV; ++c)
+                        if (c >= valid) u[c] = 0xff800000u;
+                }
+            };
+            auto row_max = [&]() {  // four independent 3-input max chains
+                float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int c = 0; c < kBKV; c += 8) {
+                for (int c = 0; c < kBKV; c += 8) {
 #pragma unroll
-                for (int k4 = 0; k4 < 4; ++k4)
-                    mq[k4] = fmax3f(mq[k4], __uint_as_float(u[c + 2 * k4]),
-                                    __uint_as_float(u[c + 2 * k4 + 1]));
-            }
-            const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-            const float m_new = fmaxf(m_run, mx * scale);
-            if (j == 0) {
-                m_run = m_new;
-            } else if (__any_sync(0xffffffffu, m_new > m_run + kRescaleThreshold)) {
+                    for (int k4 = 0; k4 < 4; ++k4)
+                        mq[k4] = fmax3f(mq[k4], __uint_as_float(u[c + 2 * k4]),
+                                        __uint_as_float(u[c + 2 * k4 + 1]));
+                }
+                return fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+            };
+            uint32_t pk[kBKV / 2];
+            auto exp_tile = [&]() {  // P = exp2(s scale - m_run), bf16 pairs; returns the sum
+                const float2 sc2 = make_float2(scale, scale);
+                const float2 nm2 = make_float2(-m_run, -m_run);
+                float2 ls[4];
+#pragma unroll
+                for (int e = 0; e < kBKV / 2; ++e) {
+                    const float2 x = ffma2(
+                        make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2,
+                        nm2);
+                    float2 pr;
+                    if ((e & 7) >= 8 - SPX_POLY_OF_8) {  // part of the exponentials on the FMA pipe
+                        pr = ex2_poly2(x);
+                    } else {
+#if SPX_ATTN_PROFILING
+                        if (p.experiment == 2) {  // profiling: no MUFU
+                            pr.x = fmaf(x.x, 0.03125f, 1.0f);
+                            pr.y = fmaf(x.y, 0.03125f, 1.0f);
+                        } else
+#endif
+                        {
+                            pr.x = ex2_approx(x.x);
+                            pr.y = ex2_approx(x.y);
+                        }
+                    }
+                    ls[e & 3] = e < 4 ? pr : fadd2(ls[e & 3], pr);  // (unrolled: no add of 0)
+                    pk[e] = pack_bf16x2(pr.x, pr.y);
+                }
+                const float2 s01 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+                return s01.x + s01.y;
+            };
+            load_s();
+            if (j == 0) m_run = row_max() * scale;
+            float lt = exp_tile();
+            if (j > 0 && __any_sync(0xffffffffu, !(lt < 1.8446744e19f))) {  // 2^64, or inf / NaN
+                load_s();  // S is still in TMEM (P not written yet)
+                const float m_new = fmaxf(m_run, row_max() * scale);
                 mbar_wait(&pv_done[i], (j - 1) & 1);
                 tc_fence_after();
                 const float alpha = ex2_approx(m_run - m_new);
@@ -563,39 +603,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 tmem_st_wait();
                 l_run *= alpha;
                 m_run = m_new;
+                lt = exp_tile();
             }
-            const float2 sc2 = make_float2(scale, scale);
-            const float2 nm2 = make_float2(-m_run, -m_run);
-            float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                            make_float2(0.f, 0.f)};
-            uint32_t pk[kBKV / 2];
-#pragma unroll
-            for (int e = 0; e < kBKV / 2; ++e) {
-                const float2 x = ffma2(
-                    make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2,
-                    nm2);
-                float2 pr;
-                if ((e & 7) >= 8 - SPX_POLY_OF_8) {  // part of the exponentials on the FMA pipe
-                    pr = ex2_poly2(x);
-                } else {
-#if SPX_ATTN_PROFILING
-                    if (p.experiment == 2) {  // profiling: no MUFU
-                        pr.x = fmaf(x.x, 0.03125f, 1.0f);
-                        pr.y = fmaf(x.y, 0.03125f, 1.0f);
-                    } else
-#endif
-                    {
-                        pr.x = ex2_approx(x.x);
-                        pr.y = ex2_approx(x.y);
-                    }
-                }
-                ls[e & 3] = e < 4 ? pr : fadd2(ls[e & 3], pr);  // (unrolled: no add of 0)
-                pk[e] = pack_bf16x2(pr.x, pr.y);
-            }
-            {
-                const float2 s01 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
-                l_run += s01.x + s01.y;
-            }
+            l_run += lt;
 #pragma unroll
             for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_s + c * 16, &pk[c * 16]);
             tmem_st_wait();

@@ -160,3 +160,27 @@ def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H):
     qf, kf, vf = (t.float()[0].transpose(0, 1) for t in (q, k, v))
     ref = torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf
     assert rel_l2(o.float()[0].transpose(0, 1), ref) < 1e-2
+
+
+@pytest.mark.parametrize("skv", [640, 4680])
+def test_attention_offset_guard_on_growing_logits(cuda, skv):
+    """The softmax takes its exponent offset from each warpgroup's first kv tile and skips the
+    per-tile max afterwards; logits that later jump far above that offset (here by ~500 in
+    natural units, > 2^64 after exp) must trip the overflow guard, which redoes the tile with
+    its true max and rescales O and l."""
+    torch = _t()
+    D, H, sq = 128, 2, 256
+    g = torch.Generator(device="cuda").manual_seed(skv)
+    q = (torch.randn(1, sq, H, D, device=cuda, generator=g) * 0.2 + 2.0).to(torch.bfloat16)
+    k = (torch.randn(1, skv, H, D, device=cuda, generator=g) * 0.2).to(torch.bfloat16)
+    k[:, 384:] += 5.0  # kv tiles 3.. : q.k / sqrt(D) ~ 113 above tile 0 (exp2 would overflow fp32)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq, skv,
+                                H, D, _stream()))
+    torch.cuda.synchronize()
+    qf, kf, vf = (t.float()[0].transpose(0, 1) for t in (q, k, v))
+    ref = torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf
+    got = o.float()[0].transpose(0, 1)
+    assert bool(torch.isfinite(got).all())
+    assert rel_l2(got, ref) < 1e-2
