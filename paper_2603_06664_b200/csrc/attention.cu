@@ -648,26 +648,54 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const uint32_t t_o0 = tmem_base + 256 + lane_off;
         const uint32_t t_o1 = tmem_base + 384 + lane_off;
         if (ns == 1) {
+            // rows staged as bf16 in the idle Q smem (16-byte units XOR-swizzled by row), then
+            // copied out by all 256 softmax threads so that each store instruction writes whole
+            // 128/256-byte row segments (the per-row 16-byte stores of a warp hit 32 rows)
+            constexpr uint32_t kRowBytes = D * 2;
+            constexpr uint32_t kU = kRowBytes / 16;
+            const uint32_t s_base = smem_u32(smem);
 #pragma unroll 1
             for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
                 uint32_t o0[32], o1[32];
                 tmem_ld32(t_o0 + c * 32, o0);
                 if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
                 tmem_ld_wait();
-                if (dst) {
-                    float f[32];
+                float f[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        f[e] = __uint_as_float(o0[e]) * w0 +
-                               (n1 > 0 ? __uint_as_float(o1[e]) * w1 : 0.0f);
-                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+                for (int e = 0; e < 32; ++e)
+                    f[e] = __uint_as_float(o0[e]) * w0 + (n1 > 0 ? __uint_as_float(o1[e]) * w1 : 0.0f);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        d4[v] = make_uint4(pack_bf16x2(f[8 * v + 0], f[8 * v + 1]),
-                                           pack_bf16x2(f[8 * v + 2], f[8 * v + 3]),
-                                           pack_bf16x2(f[8 * v + 4], f[8 * v + 5]),
-                                           pack_bf16x2(f[8 * v + 6], f[8 * v + 7]));
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t unit = static_cast<uint32_t>(c * 4 + v);
+                    const uint32_t a = s_base + static_cast<uint32_t>(r) * kRowBytes +
+                                       ((unit ^ (static_cast<uint32_t>(r) & (kU - 1))) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                                 "r"(pack_bf16x2(f[8 * v + 0], f[8 * v + 1])),
+                                 "r"(pack_bf16x2(f[8 * v + 2], f[8 * v + 3])),
+                                 "r"(pack_bf16x2(f[8 * v + 4], f[8 * v + 5])),
+                                 "r"(pack_bf16x2(f[8 * v + 6], f[8 * v + 7]))
+                                 : "memory");
                 }
+            }
+            named_bar_sync(1, 256);
+            const int tid = static_cast<int>(threadIdx.x) - 128;
+#pragma unroll 1
+            for (int idx = tid; idx < kBQ * static_cast<int>(kU); idx += 256) {
+                const int row = idx / static_cast<int>(kU);
+                const uint32_t u = static_cast<uint32_t>(idx) % kU;
+                const int q_row = q_tile * kBQ + row;
+                if (q_row >= p.sq) continue;
+                uint4 w;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                             : "r"(s_base + static_cast<uint32_t>(row) * kRowBytes +
+                                   ((u ^ (static_cast<uint32_t>(row) & (kU - 1))) << 4))
+                             : "memory");
+                const int chunk = q_row / p.rows_per_chunk;
+                bf16* drow = p.out_base[chunk] +
+                             static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
+                             static_cast<int64_t>(head) * D;
+                *reinterpret_cast<uint4*>(drow + u * 8) = w;
             }
         } else {
             // ---- split-KV ----
