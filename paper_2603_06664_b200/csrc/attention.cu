@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int lane = threadIdx.x % 32;
     pdl_trigger();
     span_begin(p.span);
+    if (threadIdx.x == 0) attn_mark(p, 4);  // CTA entry
     int q_tile, head, split, ns;
     if constexpr (kCluster) {
         q_tile = blockIdx.x;
