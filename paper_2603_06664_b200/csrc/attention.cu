@@ -31,11 +31,12 @@ namespace {
 
 constexpr int kBQ = 128;     // query rows per CTA
 constexpr int kBKV = 128;    // kv rows per tile
-// exponentials computed by the FMA-pipe polynomial, out of every 8 (the rest on MUFU.EX2)
-// (measured on B200: 0 of 8 is fastest -- 0.741 vs 0.764 ms at 4680 x 32760 x 12 with 2 of 8;
-// MUFU.EX2 is not the limit once the MMA issue is warp-uniform)
+// exponentials computed by the FMA-pipe polynomial, out of every 8 (the rest on MUFU.EX2).
+// Re-measured once the profiling branch was compiled out of the exp loop (it had been
+// predicated into every element): 3 of 8 0.1080-0.1100 vs 0 of 8 0.1097-0.1111 ms at the
+// Wan chunk (4 of 8 is slower again, 0.1146) -- the MUFU pipe is close to its limit.
 #ifndef SPX_POLY_OF_8
-#define SPX_POLY_OF_8 0
+#define SPX_POLY_OF_8 3  // 3 of every 8 exponentials on the FMA pipe (A/B after the loop cleanup: ~1-1.5 %)
 #endif
 // P_i hand-off to the MMA thread: one arrival per softmax warp (after __syncwarp) instead of
 // one per thread
