@@ -4,7 +4,7 @@ Causal-RoPE SP schedule runs with device-side flag barriers. Several ranks may s
 GPU (the driver time-slices their contexts), which is how the multi-process path is tested
 on a single B200.
 
-usage: python tests/peer_worker.py RANK WORLD PORT OUT_DIR [window_frames]
+usage: python tests/peer_worker.py RANK WORLD PORT OUT_DIR [window_frames|-1] [wan]
 """
 import math
 import os
@@ -27,24 +27,28 @@ def scaled_weights(dim, layers, scale_qk, seed):
     return oracle.round_bf16(w)
 
 
-def make_engine(s, world_size, world, window=None):
+def make_engine(s, world_size, world, window=None, wan=False):
     from oracle import oracle
 
     kw = TINY
     cfg = s.GenerationConfig(grid_per_block=s.GridSpec(kw["frames"], kw["grid_h"], kw["grid_w"]),
                              num_blocks=kw["num_blocks"], layers=kw["layers"], denoise_steps=2,
                              heads=kw["heads"], head_dim=kw["head_dim"], world_size=world_size,
-                             window_frames=window)
-    w = scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 4.0, seed=7)
+                             window_frames=window, qk_norm=wan, adaln=wan)
+    w = scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 1.0 if wan else 4.0, seed=7)
     eng = s.Engine(cfg, world=world, seed_weights=False)
     for l in range(cfg.layers):
         eng.set_layer_weights_bits(l, *[oracle.to_bf16_bits(w[l, m]) for m in range(4)])
+        if wan:  # non-trivial adaLN modulation (zero would make every layer the identity)
+            m = (np.random.default_rng(100 + l).standard_normal((3, kw["heads"] * kw["head_dim"])) * 0.3)
+            eng.set_modulation(l, *m.astype(np.float32))
     return eng
 
 
 def main():
     rank, world_size, port, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4]
-    window = int(sys.argv[5]) if len(sys.argv) > 5 else None
+    window = int(sys.argv[5]) if len(sys.argv) > 5 and int(sys.argv[5]) > 0 else None
+    wan = len(sys.argv) > 6 and sys.argv[6] == "wan"
     import torch
     import torch.distributed as dist
 
@@ -54,7 +58,7 @@ def main():
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world_size)
     world = s.CommWorld.peer(rank, world_size, 0)
-    eng = make_engine(s, world_size, world, window)
+    eng = make_engine(s, world_size, world, window, wan)
     eng.connect_peers(dist.all_gather_object)
     got = eng.generate()  # (blocks, L/P rows of this rank, H, D) bf16 bits
     np.save(os.path.join(out, f"rank{rank}.npy"), got)

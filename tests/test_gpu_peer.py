@@ -23,9 +23,9 @@ def _free_port():
         return so.getsockname()[1]
 
 
-def _run_ranks(world, tmp_path, window=None):
+def _run_ranks(world, tmp_path, window=None, wan=False):
     port = _free_port()
-    args = [str(window)] if window is not None else []
+    args = [str(window if window is not None else -1)] + (["wan"] if wan else [])
     procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "peer_worker.py"), str(r),
                                str(world), str(port), str(tmp_path)] + args,
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
@@ -61,3 +61,14 @@ def test_peer_transport_bit_identical_to_p1(cuda, tmp_path, world, window):
     want = local.stats()
     for st in stats:
         assert list(st) == [want[k] for k in sorted(want)]
+
+
+def test_peer_transport_wan_mode_bit_identical_to_p1(cuda, tmp_path):
+    """QK-RMSNorm + adaLN modulation (seeded per layer) over the PEER transport, P = 4."""
+    import peer_worker
+    from paper_2603_06664_b200 import spattn as s
+
+    slices, _ = _run_ranks(4, tmp_path, wan=True)
+    got = np.concatenate(slices, axis=1)
+    base = peer_worker.make_engine(s, 1, s.CommWorld(1), None, wan=True).generate()
+    assert np.array_equal(got, base)
