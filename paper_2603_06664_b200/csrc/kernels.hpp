@@ -179,19 +179,16 @@ void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const fl
 
 // ---------------------------------------------------------------------------------------
 // PEER transport: device-side rank barrier over IPC-mapped flag words. Each rank owns
-// flags[kPeerSlots][P] (uint64, epoch values). signal: after this stream's prior kernels
-// (whose stores may target peer memory), st.release.sys flags[slot][my_rank] = epoch in
-// every rank's array. wait: spin (ld.acquire.sys) until every entry of flags[slot] >= epoch.
+// flags[kPeerSlots][P] (uint64, epoch values). After this stream's prior kernels (whose
+// stores may target peer memory): st.release.sys flags[slot][my_rank] = epoch in every
+// rank's array, then spin (ld.acquire.sys) until every entry of flags[slot] >= epoch.
 // ---------------------------------------------------------------------------------------
 constexpr int kPeerSlots = 2;
 constexpr int kMaxPeers = 8;
 struct PeerFlags {
     uint64_t* rank_flags[kMaxPeers];  // every rank's flag array (this process's mapping)
 };
-void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint64_t epoch,
-                     cudaStream_t s);
-void peer_wait_run(uint64_t* my_flags, int world, int slot, uint64_t epoch, cudaStream_t s);
-// signal + wait as one PDL-chained 1-warp launch (the engine's default)
+// signal + wait as one PDL-chained 1-warp launch
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
                       uint64_t epoch, cudaStream_t s);
 

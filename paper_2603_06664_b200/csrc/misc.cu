@@ -16,16 +16,7 @@ using namespace sm100;
 
 namespace {
 
-// PEER barrier (see kernels.hpp). One thread per rank.
-__global__ void peer_signal_kernel(PeerFlags f, int world, int my_rank, int slot, uint64_t epoch) {
-    const int r = threadIdx.x;
-    if (r >= world) return;
-    uint64_t* dst = f.rank_flags[r] + slot * world + my_rank;
-    // release at system scope: this stream's earlier kernels (stores into peer memory
-    // included) happen-before the flag as seen by the peer
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
-}
-
+// PEER barrier (see kernels.hpp): one thread per rank.
 // signal + wait in one 1-warp launch, chained with PDL: it starts during the previous
 // kernel's tail, griddepcontrol.wait makes that kernel's stores (peer stores included)
 // complete before the release, and the next kernel's prologue overlaps the spin
@@ -51,19 +42,6 @@ __global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, 
     __syncwarp();
 }
 
-__global__ void peer_wait_kernel(uint64_t* flags, int world, int slot, uint64_t epoch) {
-    const int r = threadIdx.x;
-    if (r < world) {
-        const uint64_t* src = flags + slot * world + r;
-        uint64_t v = 0;
-        for (;;) {
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
-            if (v >= epoch) break;
-            __nanosleep(64);
-        }
-    }
-    __syncwarp();
-}
 
 template <typename T>
 __global__ void copy_box_kernel(T* __restrict__ dst, const T* __restrict__ src, Box4 box,
@@ -161,24 +139,12 @@ __global__ void naive_attention_kernel(const bf16* __restrict__ q, const bf16* _
 
 }  // namespace
 
-void peer_signal_run(const PeerFlags& f, int world, int my_rank, int slot, uint64_t epoch,
-                     cudaStream_t s) {
-    peer_signal_kernel<<<1, 32, 0, s>>>(f, world, my_rank, slot, epoch);
-    SPX_CUDA_LAUNCH();
-    count_launch();
-}
-
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
                       uint64_t epoch, cudaStream_t s) {
     launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot, epoch);
     count_launch();
 }
 
-void peer_wait_run(uint64_t* my_flags, int world, int slot, uint64_t epoch, cudaStream_t s) {
-    peer_wait_kernel<<<1, 32, 0, s>>>(my_flags, world, slot, epoch);
-    SPX_CUDA_LAUNCH();
-    count_launch();
-}
 
 void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s) {
     const int64_t total = box.ext[0] * box.ext[1] * box.ext[2] * box.ext[3];

@@ -1,3 +1,3 @@
-O=gpurun_out/r01bb; mkdir -p $O
-timeout 600 python -m pytest tests/test_gpu_peer.py -x -q > $O/pytest_peer.log 2>&1; echo rc=$? >> $O/pytest_peer.log
-tail -15 $O/pytest_peer.log
+O=gpurun_out/r01bc; mkdir -p $O
+SPX_SPAN_TRACE=1 python tools/span_probe.py > $O/spans.txt 2>&1
+grep kernels_per_call $O/spans.txt
