@@ -49,6 +49,10 @@ struct GemmParams {
     int64_t ldr;
     const float* gate;
     RopeLaunch rope;  // epi_mode 2
+    // epi_mode 2 lookups (host-computed: no integer division in the epilogue)
+    int head_shift;         // log2(head_dim)
+    int8_t head_group[16];  // head -> its head group g
+    int8_t head_slot[16];   // head -> index within the group
     int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation,
                       // 5 = per-tile clock64 timeline of the pair kernel into `trace`
     long long* trace;  // [cta][16 tiles][4]: mma start, mma issued, epilogue start, end
@@ -135,14 +139,16 @@ __device__ __forceinline__ RopeRow rope_row(const RopeLaunch& l, const RopeSmem&
 // memory latency is paid once per slice, not once per pair.
 __device__ __forceinline__ void rope_rotate_chunk(const RopeLaunch& l, const RopeRow& rr, int d0,
                                                   float (&f)[32]) {
-    const int p0 = l.pairs[0], p01 = l.pairs[0] + l.pairs[1];
+    // pair j = j0 + e lies in band T below k0, H below k1, W above (warp-uniform breakpoints);
+    // each band's row base is offset so that base + 8 e addresses pair j
+    const int j0 = d0 / 2;
+    const int k0 = l.pairs[0] - j0, k1 = l.pairs[0] + l.pairs[1] - j0;
+    const uint32_t tb = rr.t + 8u * j0, hb = rr.h - 8u * k0, wb = rr.w - 8u * k1;
     float2 cs[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-        const int j = d0 / 2 + e;
-        const uint32_t at = rr.t + 8u * j, ah = rr.h + 8u * (j - p0), aw = rr.w + 8u * (j - p01);
-        const uint32_t a = j < p0 ? at : (j < p01 ? ah : aw);
-        cs[e] = lds_f2(a);
+        const uint32_t base = e < k0 ? tb : (e < k1 ? hb : wb);
+        cs[e] = lds_f2(base + 8u * e);
     }
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -164,15 +170,13 @@ struct ChunkDst {
 __device__ __forceinline__ ChunkDst chunk_dst(const GemmParams& p, int col0) {
     if (p.epi_mode != 2) return {-1, 0, 1, 0, col0, p.ldo};
     const RopeLaunch& l = p.rope;
-    const int C = l.heads * l.head_dim;
-    const int which = col0 / C;
+    const int C = l.heads << p.head_shift;
+    const int which = (col0 >= C) + (col0 >= 2 * C);
     const int c = col0 - which * C;
-    const int head = c / l.head_dim;
-    const int d0 = c - head * l.head_dim;
-    const int hpg = l.heads / l.groups;
-    const int g = head / hpg;
-    return {which, g, which == 0 ? 1 : l.dst.copies, d0, (head - g * hpg) * l.head_dim + d0,
-            l.dst_row_stride};
+    const int head = c >> p.head_shift;
+    const int d0 = c & ((1 << p.head_shift) - 1);
+    return {which, p.head_group[head], which == 0 ? 1 : l.dst.copies, d0,
+            (static_cast<int64_t>(p.head_slot[head]) << p.head_shift) + d0, l.dst_row_stride};
 }
 
 __device__ __forceinline__ bf16* chunk_base(const GemmParams& p, const ChunkDst& d, int cp) {
@@ -731,6 +735,15 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
                 "gemm: rope epilogue needs 3C outputs, C % BN == 0, D % 32 == 0, no QK-norm");
         p.epi_mode = 2;
         p.rope = *rope;
+        require(rope->heads <= 16 && (rope->head_dim & (rope->head_dim - 1)) == 0, SPX_ERR_UNSUPPORTED,
+                "gemm: rope epilogue needs <= 16 heads and a power-of-two head_dim");
+        p.head_shift = 0;
+        while ((1 << p.head_shift) < rope->head_dim) ++p.head_shift;
+        const int hpg = rope->heads / rope->groups;
+        for (int h = 0; h < rope->heads; ++h) {
+            p.head_group[h] = static_cast<int8_t>(h / hpg);
+            p.head_slot[h] = static_cast<int8_t>(h % hpg);
+        }
     }
     static const int experiment = [] {
         const char* e = std::getenv("SPX_GEMM_EXPERIMENT");
