@@ -485,3 +485,48 @@ def test_generation_report_matches_reference_layout(cuda):
     assert rep["profile"]["ledger"]["rounds"] == st["rounds"]
     assert rep["profile"]["ledger"]["bytes_sent_at_width"] == 2 * st["elements_sent"]
     assert rep["profile"]["stage_order"][:2] == ["qkv", "rope"]
+
+
+@pytest.mark.parametrize("world,adaln", [(1, False), (2, False), (2, True)])
+def test_layer_call_api_matches_generate(cuda, world, adaln):
+    """optimized_sp_self_attention (spx_engine_layer, sp_attention.hpp:118-130) on caller
+    buffers: layer by layer over one block it reproduces generate()'s block output bit for
+    bit (same kernels, external x / y, adaLN residual taken from the caller's x)."""
+    import torch
+
+    s = spattn()
+    kw = dict(TINY, num_blocks=1)
+    dim = kw["heads"] * kw["head_dim"]
+    w = _scaled_weights(dim, kw["layers"], 1.0, seed=12)
+    cfg = cfg_from(kw, steps=1, world=world, adaln=adaln)
+    mod = _modulation(dim, kw["layers"], seed=13)
+    rng = np.random.default_rng(14)
+    noise = oracle.to_bf16_bits(oracle.round_bf16(rng.standard_normal((1, 192, dim)) * 0.2))
+
+    def engine():
+        e = _engine_with_weights(cfg, w)
+        if adaln:
+            for l in range(kw["layers"]):
+                e.set_modulation(l, mod[l, 0], mod[l, 1], mod[l, 2])
+        return e
+
+    ref = engine().generate_block(0, noise)  # (rows, H, D) bits
+    eng = engine()
+    rows = 192 // world
+    xs = [torch.from_numpy(noise[0, r * rows:(r + 1) * rows].view(np.int16).copy()).to(cuda)
+          .view(torch.bfloat16) for r in range(world)]
+    for l in range(kw["layers"]):
+        xs = eng.optimized_sp_self_attention(l, 0, 0, xs)
+    got = np.concatenate([x.view(torch.int16).cpu().numpy().view(np.uint16) for x in xs])
+    assert np.array_equal(got.reshape(ref.shape), ref)
+
+
+def test_reset_cache_replays_a_video(cuda):
+    """reset_cache (a new video, generator.cpp:69-81): the same blocks generated again after a
+    reset give the same outputs; without the reset block 0 would see the old cache."""
+    s = spattn()
+    eng = s.Engine(cfg_from(TINY, steps=2, world=2))
+    first = eng.generate()
+    eng.reset_cache()
+    again = eng.generate()
+    assert np.array_equal(first, again)
