@@ -396,6 +396,7 @@ def main():
         "wan_block": wan_block,
         "rope_microbench": rope_mb,
         "clocks": clocks, "gpu_launches": launches, "ledger": eng.stats(),
+        "exchange": exchange_summary(eng.stats(), world_size, args, ms_per_chunk),
     }
 
     if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
@@ -420,6 +421,23 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def exchange_summary(ledger, world_size, args, ms_per_chunk):
+    """Sequence<->head exchange traffic per rank and layer call (row (e), NVLink roofline):
+    bf16 elements crossing a rank boundary from the ledger (sender side, summed over ranks)."""
+    if world_size == 1:
+        return {"bytes_per_call_per_rank": 0, "note": "P = 1: no exchange"}
+    calls = max(1, ledger["rounds"] // 2)
+    per_rank = ledger["elements_sent"] * 2 / calls / world_size
+    return {"bytes_per_call_per_rank": per_rank,
+            "calls": calls, "transport": args.transport,
+            "nvlink_GBs_per_direction": 900.0,
+            "nvlink_time_floor_us": per_rank / 900e9 * 1e6,
+            "note": ("PEER: the stores are issued by the QKV-GEMM and attention epilogues into "
+                     "the peers' buffers (no separate transfer to time); the floor is bytes / "
+                     "NVLink bandwidth per layer call" if args.transport == "peer" else
+                     "NCCL: one grouped send/recv round per exchange")}
 
 
 def _set_profile(eng, level):
