@@ -141,10 +141,14 @@ struct SmemV2 {
     // (128 kv rows x D/2), so a ring slot is half as large and the ring twice as deep
     static constexpr uint32_t kTileBytes = kPair ? kBKV * D : kBKV * D * 2;
     static constexpr uint32_t kSlots = (D == 128 ? kSlotsV2 : 2 * kSlotsV2) * (kPair ? 2 : 1);
+    // persistent mode: two Q buffers (the next unit's Q lands while this one's epilogue
+    // stages its output rows in the other)
+    static constexpr uint32_t kQBytes = kBQ * D * 2;
     static constexpr uint32_t kOffQ = 0;
-    static constexpr uint32_t kOffRing = kOffQ + kBQ * D * 2;
+    static constexpr uint32_t kOffRing = kOffQ + (kMode == 3 ? 2 : 1) * kQBytes;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
-    static constexpr uint32_t kNumBars = 1 + 2 * kSlots + 7;  // + the split-merge load barrier
+    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done[2], merge, o_free, q_empty[2]
+    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 6 + 1 + 1 + 2;
     static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
@@ -154,6 +158,14 @@ __device__ __forceinline__ void setmaxnreg_dec56() {
 }
 __device__ __forceinline__ void setmaxnreg_inc224() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+}
+__device__ __forceinline__ int opaque_i32(int x) {
+    asm volatile("" : "+r"(x));
+    return x;
+}
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+    asm volatile("" : "+r"(x));
+    return x;
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
@@ -252,6 +264,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     constexpr bool kPair = kMode == 1;
     constexpr bool kMcast = kMode == 2;
     constexpr bool kCluster = kPair || kMcast;
+    // kMode 3 (persistent): gridDim.x <= SMs CTAs walk the unsplit (query tile, head) units
+    // u = blockIdx.x + k gridDim.x. The producer and the MMA thread run into unit k + 1 while
+    // the softmax warpgroups finish unit k: the next Q lands in the other Q buffer, the first
+    // S tiles are computed into the free S columns, and only the first PV waits for the
+    // epilogue to have read O0|O1 out (o_free). Hides the per-CTA prologue, the Q load and
+    // first-tile latency and the CTA turnover of the one-CTA-per-unit grid.
+    constexpr bool kPersist = kMode == 3;
     using L = SmemV2<D, kMode>;
     static_assert(!kCluster || D == 128, "clustered attention is D = 128 only");
     const int cta = kCluster ? static_cast<int>(cluster_ctarank()) : 0;
@@ -263,14 +282,16 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint8_t* sQ = smem + L::kOffQ;
     uint8_t* ring = smem + L::kOffRing;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-    uint64_t* q_full = bars;
-    uint64_t* slot_full = bars + 1;
+    uint64_t* q_full = bars;                 // [2] (persistent: per Q buffer)
+    uint64_t* slot_full = bars + 2;
     uint64_t* slot_empty = slot_full + kSlots;
     uint64_t* s_full = slot_empty + kSlots;  // [2]
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* pv_done = p_full + 2;          // [2]
     uint64_t* merge_bar = pv_done + 2;       // split-KV: other splits' partials landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 3);
+    uint64_t* o_free = merge_bar + 1;        // persistent: O0|O1 read out by all 8 softmax warps
+    uint64_t* q_empty = o_free + 1;          // [2] persistent: Q buffer's staged rows stored
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 2);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
 
@@ -302,6 +323,17 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         q_tile = t % p.qt;
         head = t / p.qt;
     }
+    // persistent: this CTA's units (all unsplit); one pass otherwise
+    const int n_units = kPersist ? p.qt * p.heads : 1;
+#define my_units (kPersist ? (n_units - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / \
+                                  static_cast<int>(gridDim.x) : 1)
+    // persistent: (q_tile, head) of this CTA's k-th unit
+#define enter_unit(k)                                                                   \
+    if constexpr (kPersist) {                                                           \
+        const int u_ = static_cast<int>(blockIdx.x) + (k) * static_cast<int>(gridDim.x); \
+        q_tile = u_ % p.qt;                                                             \
+        head = u_ / p.qt;                                                               \
+    }
     // this CTA's share [tb, tb + n_total) of the kv tiles, halved between the warpgroups
     const int tb = static_cast<int>((static_cast<int64_t>(split) * p.total_tiles) / ns);
     const int n_total = static_cast<int>((static_cast<int64_t>(split + 1) * p.total_tiles) / ns) - tb;
@@ -313,7 +345,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         tma_prefetch_desc(&map_q);
         tma_prefetch_desc(&map_k);
         tma_prefetch_desc(&map_v);
-        mbar_init(q_full, 1);
+        mbar_init(&q_full[0], 1);
+        mbar_init(&q_full[1], 1);
+        mbar_init(o_free, 8);
+        mbar_init(&q_empty[0], 8);
+        mbar_init(&q_empty[1], 8);
         for (uint32_t s = 0; s < kSlots; ++s) {
             mbar_init(&slot_full[s], 1);
             mbar_init(&slot_empty[s], kMcast ? 2 : 1);
@@ -345,18 +381,31 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
 
     if (warp < 4) {
         setmaxnreg_dec56();
+        // values the producer / MMA roles need, re-derived after the register drop (params,
+        // shared memory) instead of carried across it: in the persistent form ptxas otherwise
+        // parks them in local memory and reloads them on the MMA issue path
+        const int rn0 = kPersist ? (p.total_tiles + 1) / 2 : n0;
+        const int rn1 = kPersist ? p.total_tiles - rn0 : n1;
+        const int rtb = kPersist ? 0 : tb;
+        const uint32_t rtmem = kPersist ? *reinterpret_cast<volatile uint32_t*>(tmem_slot) : tmem_base;
         if (warp == 0 && lane == 0) {
             // ---------------- TMA producer: the MMA consumption order ----------------
-            if (leader) mbar_arrive_expect_tx(q_full, (kPair ? 2 : 1) * kBQ * D * 2);
+            uint32_t t = 0;
+#pragma unroll 1
+            for (int k = 0; k < my_units; ++k) {
+            enter_unit(k)
+            const int qb = kPersist ? (k & 1) : 0;
+            if (kPersist && k >= 2) mbar_wait(&q_empty[qb], ((k - 2) >> 1) & 1);
+            if (leader) mbar_arrive_expect_tx(&q_full[qb], (kPair ? 2 : 1) * kBQ * D * 2);
 #pragma unroll
             for (int c = 0; c < (int)L::kChunks; ++c) {
                 if constexpr (kPair)
                     tma_load_3d_pair(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head,
                                      q_tile * kBQ);
                 else
-                    tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
+                    tma_load_3d(sQ + qb * L::kQBytes + c * (kBQ * 128), &map_q, &q_full[qb], c * 64,
+                                head, q_tile * kBQ);
             }
-            uint32_t t = 0;
             auto load = [&](bool is_v, int g) {
                 const uint32_t slot = t % kSlots;
                 const uint32_t ph = (t / kSlots) & 1;
@@ -364,7 +413,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 if (leader)
                     mbar_arrive_expect_tx(&slot_full[slot], (kPair ? 2 : 1) * L::kTileBytes);
                 int row, valid;
-                kv_tile_coords(p, tb + g, row, valid);
+                kv_tile_coords(p, rtb + g, row, valid);
                 uint8_t* dst = ring + slot * L::kTileBytes;
                 if constexpr (kMcast) {  // my 64 kv rows of the tile -> both CTAs' slot
 #pragma unroll
@@ -389,15 +438,16 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 ++t;
             };
             load(false, 0);
-            if (n1 > 0) load(false, n0);
-            for (int j = 0; j < n0; ++j) {
+            if (rn1 > 0) load(false, rn0);
+            for (int j = 0; j < rn0; ++j) {
                 load(true, j);
-                if (j + 1 < n0) load(false, j + 1);
-                if (j < n1) {
-                    load(true, n0 + j);
-                    if (j + 1 < n1) load(false, n0 + j + 1);
+                if (j + 1 < rn0) load(false, j + 1);
+                if (j < rn1) {
+                    load(true, rn0 + j);
+                    if (j + 1 < rn1) load(false, rn0 + j + 1);
                 }
             }
+            }  // units
             if constexpr (kCluster) {  // drain: every multicast release has landed
                 for (uint32_t k = 0; k < kSlots; ++k, ++t)
                     mbar_wait(&slot_empty[t % kSlots], ((t / kSlots) & 1) ^ 1);
@@ -423,7 +473,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 else
                     commit(bar);
             };
-            const uint32_t q_addr = smem_u32(sQ);
+            uint32_t q_addr = smem_u32(sQ);
+            uint32_t unit_k = 0;  // persistent: this CTA's unit index (o_free, p_full phases)
             const uint32_t ring_addr = smem_u32(ring);
             uint32_t t = 0;
             auto take = [&]() {
@@ -442,12 +493,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                         const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
                         const uint32_t koff = (kk >> 2) * kKChunk + (kk & 3) * 32;
                         if constexpr (kPair)
-                            umma_bf16_ss_pair(tmem_base + i * 128,
+                            umma_bf16_ss_pair(rtmem + i * 128,
                                               make_desc_sw128(q_addr + qoff, 16, 1024),
                                               make_desc_sw128(k_addr + koff, 16, 1024), idesc_s,
                                               kk > 0);
                         else
-                            umma_bf16_ss(tmem_base + i * 128,
+                            umma_bf16_ss(rtmem + i * 128,
                                          make_desc_sw128(q_addr + qoff, 16, 1024),
                                          make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
                     }
@@ -458,22 +509,27 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             };
             auto issue_pv = [&](int i, int j) {
                 const uint32_t slot = take();
+                // p_full completes once per tile of slot i: cumulative over the units
+                const uint32_t nth = unit_k * static_cast<uint32_t>(i == 0 ? rn0 : rn1) + j;
                 if constexpr (kPair)
                     mbar_wait_cluster(&p_full[i], j & 1);
                 else if (p.experiment != 3)  // 3: profiling, MMA stream without softmax
-                    mbar_wait(&p_full[i], j & 1);
+                    mbar_wait(&p_full[i], nth & 1);
+                // the first PV of a unit overwrites O_i: the previous unit's epilogue has read
+                // O0|O1 out
+                if (kPersist && j == 0 && unit_k > 0) mbar_wait(o_free, (unit_k - 1) & 1);
                 tc_fence_after();
                 const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
                 if (issuer) {
 #pragma unroll
                     for (int kk = 0; kk < kBKV / 16; ++kk) {
                         if constexpr (kPair)
-                            umma_bf16_ts_pair(tmem_base + 256 + i * 128,
-                                              tmem_base + i * 128 + kk * 8,
+                            umma_bf16_ts_pair(rtmem + 256 + i * 128,
+                                              rtmem + i * 128 + kk * 8,
                                               make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
                                               idesc_o, (j | kk) != 0);
                         else
-                            umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                            umma_bf16_ts(rtmem + 256 + i * 128, rtmem + i * 128 + kk * 8,
                                          make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
                                          idesc_o, (j | kk) != 0);
                     }
@@ -482,16 +538,21 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
                 __syncwarp();
             };
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            issue_s(0);
-            if (n1 > 0) issue_s(1);
-            for (int j = 0; j < n0; ++j) {
-                issue_pv(0, j);
-                if (j + 1 < n0) issue_s(0);
-                if (j < n1) {
-                    issue_pv(1, j);
-                    if (j + 1 < n1) issue_s(1);
+#pragma unroll 1
+            for (int k = 0; k < my_units; ++k, ++unit_k) {
+                const int qb = kPersist ? (k & 1) : 0;
+                q_addr = smem_u32(sQ) + qb * L::kQBytes;
+                mbar_wait(&q_full[qb], kPersist ? ((k >> 1) & 1) : 0);
+                tc_fence_after();
+                issue_s(0);
+                if (rn1 > 0) issue_s(1);
+                for (int j = 0; j < rn0; ++j) {
+                    issue_pv(0, j);
+                    if (j + 1 < rn0) issue_s(0);
+                    if (j < rn1) {
+                        issue_pv(1, j);
+                        if (j + 1 < rn1) issue_s(1);
+                    }
                 }
             }
         }
@@ -507,12 +568,18 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const int n = i == 0 ? n0 : n1;
         const int g0 = tb + (i == 0 ? 0 : n0);
         const float scale = p.scale_log2;
+        // (loop state kept minimal: the softmax runs at the register limit; the unit's
+        // coordinates are derived again for the epilogue)
+#pragma unroll 1
+        for (int k = 0; k < my_units; ++k) {
+        // s_full / pv_done complete once per tile of this slot: cumulative over the units
+#define nb (static_cast<uint32_t>(k) * static_cast<uint32_t>(n))
         float m_run = -INFINITY;
         float l_run = 0.0f;
         for (int j = 0; j < (p.experiment == 3 ? 0 : n); ++j) {
             int row, valid;
             kv_tile_coords(p, g0 + j, row, valid);
-            mbar_wait(&s_full[i], j & 1);
+            mbar_wait(&s_full[i], (nb + j) & 1);
             tc_fence_after();
             if (p.experiment == 1) {  // profiling: MMA/TMA/barrier skeleton only
                 tc_fence_before();
@@ -590,7 +657,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             if (j > 0 && __any_sync(0xffffffffu, !(lt < 1.8446744e19f))) {  // 2^64, or inf / NaN
                 load_s();  // S is still in TMEM (P not written yet)
                 const float m_new = fmaxf(m_run, row_max() * scale);
-                mbar_wait(&pv_done[i], (j - 1) & 1);
+                mbar_wait(&pv_done[i], (nb + j - 1) & 1);
                 tc_fence_after();
                 const float alpha = ex2_approx(m_run - m_new);
 #pragma unroll 1
@@ -621,10 +688,19 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             }
         }
         if (n > 0) {
-            mbar_wait(&pv_done[i], (n - 1) & 1);
+            mbar_wait(&pv_done[i], (nb + n - 1) & 1);
             tc_fence_after();
         }
+#undef nb
+        {  // epilogue. Persistent: the lane-derived values are re-derived opaquely, so that
+           // the compiler cannot hoist the epilogue's address math out of the unit loop (it
+           // would stay live across the softmax loop, which runs at the register limit)
+        const int r = opaque_i32(q * 32 + lane);
+        const uint32_t lane_off = static_cast<uint32_t>(r & ~31) << 16;
+        const uint32_t tmem_base = opaque_u32(*tmem_slot);
         if (threadIdx.x == 128) attn_mark(p, 1);
+        enter_unit(k)
+        const int qb = kPersist ? (k & 1) : 0;
         st_m[i * 128 + r] = m_run;
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
@@ -649,13 +725,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         const uint32_t t_o0 = tmem_base + 256 + lane_off;
         const uint32_t t_o1 = tmem_base + 384 + lane_off;
-        if (ns == 1) {
+        if (kPersist || ns == 1) {  // (persistent units are never split)
             // rows staged as bf16 in the idle Q smem (16-byte units XOR-swizzled by row), then
             // copied out by all 256 softmax threads so that each store instruction writes whole
             // 128/256-byte row segments (the per-row 16-byte stores of a warp hit 32 rows)
             constexpr uint32_t kRowBytes = D * 2;
             constexpr uint32_t kU = kRowBytes / 16;
-            const uint32_t s_base = smem_u32(smem);
+            const uint32_t s_base = smem_u32(smem) + qb * L::kQBytes;  // this unit's Q buffer
 #pragma unroll 1
             for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
                 uint32_t o0[32], o1[32];
@@ -679,6 +755,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                  : "memory");
                 }
             }
+            if constexpr (kPersist) {  // O0|O1 read out: the next unit's first PV may overwrite
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(o_free);
+            }
             named_bar_sync(1, 256);
             const int tid = static_cast<int>(threadIdx.x) - 128;
 #pragma unroll 1
@@ -698,6 +779,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                              static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
                              static_cast<int64_t>(head) * D;
                 *reinterpret_cast<uint4*>(drow + u * 8) = w;
+            }
+            if constexpr (kPersist) {  // staged rows consumed: the Q buffer may be refilled
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&q_empty[qb]);
             }
         } else {
             // ---- split-KV ----
@@ -827,6 +912,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
             }
         }
+        }  // epilogue
+        }  // units
     }
     if (threadIdx.x == 128) attn_mark(p, 3);
     tc_fence_before();
@@ -844,6 +931,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
 }
 
+#undef my_units
+#undef enter_unit
+
 template <int D, int kMode>
 void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
     static bool done[64] = {};
@@ -855,7 +945,7 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
                                       static_cast<int>(SmemV2<D, kMode>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kMode != 0) {
+    if constexpr (kMode == 1 || kMode == 2) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kThreadsV2);
@@ -1130,11 +1220,31 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             attn_v2_launch<128, 2>(grid, plan, p, stream);
     } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
         const int64_t T = static_cast<int64_t>(p.qt) * o.heads;
-        const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
-        if (o.head_dim == 128)
-            attn_v2_launch<128, 0>(g1, plan, p, stream);
-        else
-            attn_v2_launch<64, 0>(g1, plan, p, stream);
+        int dev = 0;
+        SPX_CUDA(cudaGetDevice(&dev));
+        const int sms = device_sm_count(dev);
+        // persistent form (opt-in, SPX_ATTN_PERSIST=1) when every unit is unsplit and there
+        // is more than one wave of them. Measured slower on B200 (tools/kbench.py, same box):
+        // 0.113 vs 0.1096 ms at the Wan chunk, 0.743 vs 0.701 ms at 32760 keys -- the steady
+        // state loses more (ncu: tensor pipe 64 vs 72 % active, L2 read sectors +15 %) than
+        // the hidden prologue / first-tile / epilogue latency gains
+        static const bool persist_env = [] {
+            const char* e = std::getenv("SPX_ATTN_PERSIST");
+            return e && std::atoi(e) == 1;
+        }();
+        if (persist_env && p.experiment != 5 && p.n_full == T && T > sms) {
+            const dim3 gp(static_cast<unsigned>(sms));
+            if (o.head_dim == 128)
+                attn_v2_launch<128, 3>(gp, plan, p, stream);
+            else
+                attn_v2_launch<64, 3>(gp, plan, p, stream);
+        } else {
+            const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
+            if (o.head_dim == 128)
+                attn_v2_launch<128, 0>(g1, plan, p, stream);
+            else
+                attn_v2_launch<64, 0>(g1, plan, p, stream);
+        }
     }
     SPX_CUDA_LAUNCH();
     count_launch();

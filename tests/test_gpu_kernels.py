@@ -184,3 +184,49 @@ def test_attention_offset_guard_on_growing_logits(cuda, skv):
     got = o.float()[0].transpose(0, 1)
     assert bool(torch.isfinite(got).all())
     assert rel_l2(got, ref) < 1e-2
+
+
+_PERSIST_CHILD = r"""
+import sys, torch
+from paper_2603_06664_b200._lib import check, lib
+q, k, v = torch.load(sys.argv[1])
+q, k, v = q.cuda(), k.cuda(), v.cuda()
+o = torch.empty_like(q)
+_, sq, H, D = q.shape
+check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq,
+                          k.shape[1], H, D, torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+torch.save(o.cpu(), sys.argv[2])
+"""
+
+
+@pytest.mark.parametrize("sq,skv,H,D", [(4680, 4680, 12, 128), (2560, 1000, 16, 64)])
+def test_attention_persistent_opt_in_bit_identical(cuda, tmp_path, sq, skv, H, D):
+    """the opt-in persistent form (SPX_ATTN_PERSIST=1: CTAs walk several (query tile, head)
+    units, the next unit's Q load and first S tiles overlap this unit's epilogue) runs the
+    same per-unit arithmetic as the one-CTA-per-unit grid: outputs are bit-identical"""
+    import os
+    import subprocess
+    import sys
+
+    torch = _t()
+    g = torch.Generator(device="cuda").manual_seed(sq + H)
+    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq, skv,
+                                H, D, _stream()))
+    torch.cuda.synchronize()
+    torch.save((q.cpu(), k.cpu(), v.cpu()), tmp_path / "in.pt")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPX_ATTN_PERSIST="1", SPX_ATTN_VERBOSE="1",
+               PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(tmp_path / "in.pt"),
+                        str(tmp_path / "out.pt")], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    if D == 128:  # the layout line (D = 128 path): every unit unsplit, i.e. the persistent form ran
+        assert "n_full=%d" % (((sq + 127) // 128) * H) in r.stderr
+    o_p = torch.load(tmp_path / "out.pt")
+    assert torch.equal(o_p, o.cpu())
