@@ -325,8 +325,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
     // persistent: this CTA's units (all unsplit); one pass otherwise
     const int n_units = kPersist ? p.qt * p.heads : 1;
-#define my_units (kPersist ? (n_units - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / \
-                                  static_cast<int>(gridDim.x) : 1)
+    const int my_units = kPersist ? (n_units - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                                        static_cast<int>(gridDim.x)
+                                  : 1;
     // persistent: (q_tile, head) of this CTA's k-th unit
 #define enter_unit(k)                                                                   \
     if constexpr (kPersist) {                                                           \
@@ -573,7 +574,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
 #pragma unroll 1
         for (int k = 0; k < my_units; ++k) {
         // s_full / pv_done complete once per tile of this slot: cumulative over the units
-#define nb (static_cast<uint32_t>(k) * static_cast<uint32_t>(n))
+        const uint32_t nb = static_cast<uint32_t>(k) * static_cast<uint32_t>(n);
         float m_run = -INFINITY;
         float l_run = 0.0f;
         for (int j = 0; j < (p.experiment == 3 ? 0 : n); ++j) {
@@ -691,7 +692,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_wait(&pv_done[i], (nb + n - 1) & 1);
             tc_fence_after();
         }
-#undef nb
         {  // epilogue. Persistent: the lane-derived values are re-derived opaquely, so that
            // the compiler cannot hoist the epilogue's address math out of the unit loop (it
            // would stay live across the softmax loop, which runs at the register limit)
@@ -931,7 +931,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
 }
 
-#undef my_units
 #undef enter_unit
 
 template <int D, int kMode>

@@ -64,7 +64,7 @@ def main():
     check(lib().spx_engine_synchronize(eng._h))
     check(lib().spx_engine_set_profile(eng._h, 0))
     stages, calls = eng.stage_times()
-    if os.environ.get("SPX_GEMM_EXPERIMENT") == "5":  # last pair-GEMM launch's tile timeline
+    if os.environ.get("SPX_GEMM_EXPERIMENT") in ("5", "7"):  # last traced GEMM launch: tile timeline (7: the O-projection)
         import numpy as np
 
         tr = np.zeros(1024 * 16 * 4, dtype=np.int64)
