@@ -83,5 +83,35 @@ def main():
     print({k: round(v, 3) for k, v in res.items()})
 
 
+
+
+def enqueue_cost():
+    """host cost of enqueueing one chunk (GPU idle at the start, no sync inside)"""
+    F, Hg, Wg, H, D, layers, steps = 3, 30, 52, 12, 128, 30, 4
+    L, C = F * Hg * Wg, H * D
+    cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(F, Hg, Wg), num_blocks=1,
+                                  layers=layers, denoise_steps=steps, heads=H, head_dim=D,
+                                  world_size=1, seed=0, profile=False)
+    eng = spattn.Engine(cfg, world=spattn.CommWorld(1, [0]))
+    noise = torch.randn(steps, L, C, device="cuda").to(torch.bfloat16)
+    out = torch.empty(L, C, device="cuda", dtype=torch.bfloat16)
+    nptr, optr = ptr_array([noise.data_ptr()]), ptr_array([out.data_ptr()])
+    for _ in range(3):
+        check(lib().spx_engine_generate_block_device(eng._h, 0, nptr, optr))
+    check(lib().spx_engine_synchronize(eng._h))
+    res = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        check(lib().spx_engine_generate_block_device(eng._h, 0, nptr, optr))
+        t1 = time.perf_counter()
+        check(lib().spx_engine_synchronize(eng._h))
+        t2 = time.perf_counter()
+        res.append((round((t1 - t0) * 1e3, 3), round((t2 - t0) * 1e3, 3)))
+    print({"enqueue_ms, enqueue+sync_ms": res})
+
+
 if __name__ == "__main__":
-    main()
+    if "--enqueue" in sys.argv:
+        enqueue_cost()
+    else:
+        main()
