@@ -54,6 +54,8 @@ def timeit(fn, iters):
 
 ATTN_SHAPES = [(4680, 4680, 12), (4680, 32760, 12), (2340, 4680, 6), (1170, 4680, 3),
                (2340, 4680, 3), (4680, 14040, 12)]
+if os.environ.get("KBENCH_ATTN_SHAPES"):  # e.g. "4680x4680x6,4680x4680x3" (per-rank shapes)
+    ATTN_SHAPES = [tuple(int(v) for v in t.split("x")) for t in os.environ["KBENCH_ATTN_SHAPES"].split(",")]
 
 
 def attn(iters):
