@@ -147,8 +147,9 @@ struct SmemV2 {
     static constexpr uint32_t kOffQ = 0;
     static constexpr uint32_t kOffRing = kOffQ + (kMode == 3 ? 2 : 1) * kQBytes;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
-    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done[2], merge, o_free, q_empty[2]
-    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 6 + 1 + 1 + 2;
+    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done[2], merge, o_free, q_empty[2],
+    // xfer_free
+    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 6 + 1 + 1 + 2 + 1;
     static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
@@ -271,6 +272,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     // epilogue to have read O0|O1 out (o_free). Hides the per-CTA prologue, the Q load and
     // first-tile latency and the CTA turnover of the one-CTA-per-unit grid.
     constexpr bool kPersist = kMode == 3;
+    // kMode 5: every (query tile, head) in exactly 2 kv splits, the two CTAs of a 2-CTA
+    // cluster. Split 1 bulk-copies its normalised fp32 partial and log-sum-exp straight into
+    // split 0's shared memory (DSMEM) and split 0 merges: no workspace round trip through L2,
+    // no completion wait + atomic on the critical path.
+    constexpr bool kSplitPair = kMode == 5;
     using L = SmemV2<D, kMode>;
     static_assert(!kCluster || D == 128, "clustered attention is D = 128 only");
     const int cta = kCluster ? static_cast<int>(cluster_ctarank()) : 0;
@@ -291,7 +297,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint64_t* merge_bar = pv_done + 2;       // split-KV: other splits' partials landed
     uint64_t* o_free = merge_bar + 1;        // persistent: O0|O1 read out by all 8 softmax warps
     uint64_t* q_empty = o_free + 1;          // [2] persistent: Q buffer's staged rows stored
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 2);
+    uint64_t* xfer_free = q_empty + 2;       // mode 5, split 1: the merging CTA's buffers are free
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfer_free + 1);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
 
@@ -306,6 +313,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         head = blockIdx.y;
         split = blockIdx.z;
         ns = p.splits;
+    } else if constexpr (kSplitPair) {
+        const int t = static_cast<int>(blockIdx.x) >> 1;
+        split = static_cast<int>(cluster_ctarank());
+        ns = 2;
+        q_tile = t % p.qt;
+        head = t / p.qt;
     } else {  // full tiles first (block order ~ issue order), then the split ones
         const int b = static_cast<int>(blockIdx.x);
         int t;
@@ -361,6 +374,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_init(&pv_done[i], 1);
         }
         mbar_init(merge_bar, 1);
+        mbar_init(xfer_free, 1);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -370,7 +384,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tmem_alloc<512>(tmem_slot);
     }
     tc_fence_before();
-    if constexpr (kCluster)
+    if constexpr (kCluster || kSplitPair)
         cluster_sync_all();
     else
         __syncthreads();
@@ -784,6 +798,91 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&q_empty[qb]);
             }
+        } else if constexpr (kSplitPair) {
+            // ---- 2 splits merged through DSMEM ----
+            // Both CTAs stage their normalised fp32 partial (128 rows x D, 16-byte units
+            // XOR-swizzled by row) at offset 0 of their own smem. Split 0 keeps its lse in
+            // registers and receives split 1's partial at offset kPartBytes and its lse at
+            // 2 kPartBytes (ring smem, idle once the PVs are done), then merges.
+            constexpr uint32_t kUnits = D / 4;
+            constexpr uint32_t kPartBytes = kBQ * D * 4;
+            static_assert(2 * kPartBytes + 1024 <= L::kOffBar, "mode 5: two partials + lse in smem");
+            const uint32_t s_base = smem_u32(smem);
+            auto unit_addr = [&](uint32_t buf, int row, uint32_t u) {
+                return s_base + buf * kPartBytes + static_cast<uint32_t>(row) * (kUnits * 16) +
+                       ((u ^ (static_cast<uint32_t>(row) & (kUnits - 1))) << 4);
+            };
+            const float lse_own = mm + __log2f(l0 * a0 + l1 * a1);
+            if (split == 0 && threadIdx.x == 128) {
+                // the partner may write our buffer 1 and lse slot now (our MMAs are done)
+                mbar_arrive_expect_tx(merge_bar, kPartBytes + kBQ * 4);
+                mbar_arrive_remote(peer_smem_addr(xfer_free, 1));
+            }
+#pragma unroll 1
+            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+                uint32_t o0[32], o1[32];
+                tmem_ld32(t_o0 + c * 32, o0);
+                if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
+                tmem_ld_wait();
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    float f[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        f[e] = __uint_as_float(o0[4 * v + e]) * w0 +
+                               (n1 > 0 ? __uint_as_float(o1[4 * v + e]) * w1 : 0.0f);
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     unit_addr(0, r, static_cast<uint32_t>(c * 8 + v))),
+                                 "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3])
+                                 : "memory");
+                }
+            }
+            if (split == 1) {
+                if (i == 0)
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(s_base + 2 * kPartBytes + kBQ * 4 + r * 4),
+                                 "f"(lse_own)
+                                 : "memory");
+                fence_proxy_async_smem();  // generic-proxy smem writes -> the bulk copies' reads
+                named_bar_sync(1, 256);
+                if (threadIdx.x == 128) {
+                    attn_mark(p, 2);
+                    mbar_wait_cluster(xfer_free, 0);
+                    const uint32_t mb = peer_smem_addr(merge_bar, 0);
+                    bulk_copy_to_peer(peer_smem_addr(smem + kPartBytes, 0), s_base, kPartBytes, mb);
+                    bulk_copy_to_peer(peer_smem_addr(smem + 2 * kPartBytes, 0), s_base + 2 * kPartBytes + kBQ * 4,
+                                      kBQ * 4, mb);
+                }
+            } else {
+                named_bar_sync(1, 256);  // both warpgroups staged their halves of every row
+                mbar_wait(merge_bar, 0);
+                if (threadIdx.x == 128) attn_mark(p, 6);
+                float lse1;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lse1) : "r"(s_base + 2 * kPartBytes + r * 4));
+                const float lm = fmaxf(lse_own, lse1);
+                const float wa = ex2_approx(lse_own - lm), wb = ex2_approx(lse1 - lm);
+                const float inv_w = 1.0f / (wa + wb);
+                const float ca = wa * inv_w, cb = wb * inv_w;
+                if (dst) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + i * (D / 2));
+#pragma unroll
+                    for (int v = 0; v < D / 16; ++v) {
+                        float4 x0, x1, y0, y1;
+                        const uint32_t u0 = static_cast<uint32_t>(i * (D / 8) + 2 * v);
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w) : "r"(unit_addr(0, r, u0)));
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w) : "r"(unit_addr(0, r, u0 + 1)));
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(y0.x), "=f"(y0.y), "=f"(y0.z), "=f"(y0.w) : "r"(unit_addr(1, r, u0)));
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(y1.x), "=f"(y1.y), "=f"(y1.z), "=f"(y1.w) : "r"(unit_addr(1, r, u0 + 1)));
+                        d4[v] = make_uint4(pack_bf16x2(ca * x0.x + cb * y0.x, ca * x0.y + cb * y0.y),
+                                           pack_bf16x2(ca * x0.z + cb * y0.z, ca * x0.w + cb * y0.w),
+                                           pack_bf16x2(ca * x1.x + cb * y1.x, ca * x1.y + cb * y1.y),
+                                           pack_bf16x2(ca * x1.z + cb * y1.z, ca * x1.w + cb * y1.w));
+                    }
+                }
+            }
         } else {
             // ---- split-KV ----
             // Each split CTA stages its normalised fp32 partial (128 rows x D) in the now idle
@@ -841,6 +940,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 if (s_last) *ctr = 0;  // every split has arrived: re-arm for the next launch
             }
             named_bar_sync(1, 256);
+            if (threadIdx.x == 128) attn_mark(p, 5);  // split arrival counted
             if (s_last) {
                 __threadfence();
                 float lse_max = -INFINITY;
@@ -881,6 +981,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                         }
                     }
                     mbar_wait(merge_bar, phase);
+                    if (threadIdx.x == 128) attn_mark(p, 6);  // other partials landed
                     phase ^= 1;
                     for (int b = 0; b < cnt; ++b) {
                         const int z = o0 + b < split ? o0 + b : o0 + b + 1;
@@ -917,7 +1018,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
     if (threadIdx.x == 128) attn_mark(p, 3);
     tc_fence_before();
-    if constexpr (kCluster)
+    if constexpr (kCluster || kSplitPair)  // mode 5: split 1's smem is read by its bulk copy
         cluster_sync_all();
     else
         __syncthreads();
@@ -944,7 +1045,7 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
                                       static_cast<int>(SmemV2<D, kMode>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kMode == 1 || kMode == 2) {
+    if constexpr (kMode == 1 || kMode == 2 || kMode == 5) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kThreadsV2);
@@ -961,7 +1062,8 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
         cfg.numAttrs = 2;
         // pair and multicast modes both load 64-row K boxes; multicast also 64-row V boxes
         SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q,
-                                    plan.map_k_pair, kMode == 2 ? plan.map_v_half : plan.map_v, p));
+                                    kMode == 5 ? plan.map_k : plan.map_k_pair,
+                                    kMode == 2 ? plan.map_v_half : plan.map_v, p));
     } else {
         launch_pdl(attn_fwd_v2_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV2<D, kMode>::kBytes,
                    stream, plan.map_q, plan.map_k, plan.map_v, p);
@@ -1231,7 +1333,18 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             const char* e = std::getenv("SPX_ATTN_PERSIST");
             return e && std::atoi(e) == 1;
         }();
-        if (persist_env && p.experiment != 5 && p.n_full == T && T > sms) {
+        static const bool pair_merge = [] {  // SPX_ATTN_SPLIT_PAIR=0: the workspace merge
+            const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
+            return !(e && std::atoi(e) == 0);
+        }();
+        if (pair_merge && p.n_full == 0 && p.splits == 2 && p.experiment != 5) {
+            // every tile in 2 splits: the two CTAs of a cluster merge through DSMEM
+            const dim3 g2(static_cast<unsigned>(2 * T));
+            if (o.head_dim == 128)
+                attn_v2_launch<128, 5>(g2, plan, p, stream);
+            else
+                attn_v2_launch<64, 5>(g2, plan, p, stream);
+        } else if (persist_env && p.experiment != 5 && p.n_full == T && T > sms) {
             const dim3 gp(static_cast<unsigned>(sms));
             if (o.head_dim == 128)
                 attn_v2_launch<128, 3>(gp, plan, p, stream);

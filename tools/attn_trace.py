@@ -23,13 +23,13 @@ for _ in range(3):
 torch.cuda.synchronize()
 tr = np.zeros(1024 * 64, dtype=np.int64)
 check(lib().spx_debug_gemm_trace(tr.ctypes.data, tr.size))
-tr = tr.reshape(1024, 64)[:, :5]
+tr = tr.reshape(1024, 64)[:, :7]
 n = int((tr[:, 0] != 0).sum())
 t = tr[:n].astype(np.float64) / 1965.0  # us at 1965 MHz (SM clock cycles)
 rel = t - t[:, :1]
 print(json.dumps({"entry_to_prologue_end_us(mean,max)": [round(float((t[:, 0] - t[:, 4]).mean()), 2),
                                                          round(float((t[:, 0] - t[:, 4]).max()), 2)]}))
 print(json.dumps({"shape": sys.argv[1], "ctas": n,
-                  "mean_us[loop_end, partial_done, cta_end]": [round(float(x), 2) for x in
+                  "mean_us[loop_end, partial_done, cta_end, entry, counted, merge_loaded]": [round(float(x), 2) for x in
                                                               np.where(tr[:n, 1:] != 0, rel[:, 1:], np.nan).mean(0)],
                   "max_us": [round(float(x), 2) for x in np.nanmax(np.where(tr[:n, 1:] != 0, rel[:, 1:], np.nan), 0)]}))
