@@ -6,7 +6,13 @@
 // order-invariant, so the ring's two chronological segments are visited in storage order.
 //
 // The kernel (attn_fwd_v2_kernel below): one CTA = one 128-row query tile of one head, its kv
-// range split between two softmax warpgroups that ping-pong against one MMA thread.
+// range split between two softmax warpgroups that ping-pong against one MMA thread. Template
+// modes (host selection in attn_run):
+//   0  default: 1-D grid, unsplit tiles first, then split-KV tiles merged through a workspace
+//   5  default when every tile has exactly 2 splits: the splits are a 2-CTA cluster, merged
+//      through DSMEM
+//   1, 2, 3  opt-in experiments measured slower on B200 (CTA-pair MMAs, K/V multicast, a
+//      persistent form); kept for the record and covered by tests
 #include <algorithm>
 
 #include <atomic>
