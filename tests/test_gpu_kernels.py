@@ -230,3 +230,33 @@ def test_attention_persistent_opt_in_bit_identical(cuda, tmp_path, sq, skv, H, D
         assert "n_full=%d" % (((sq + 127) // 128) * H) in r.stderr
     o_p = torch.load(tmp_path / "out.pt")
     assert torch.equal(o_p, o.cpu())
+
+
+@pytest.mark.parametrize("kernel", ["pair", "mcast"])
+@pytest.mark.parametrize("sq,skv,H", [(512, 1000, 2), (300, 4680, 3)])
+def test_attention_opt_in_cluster_modes(cuda, tmp_path, kernel, sq, skv, H):
+    """the opt-in cluster variants (SPX_ATTN_KERNEL=pair: CTA-pair MMAs; mcast: K/V multicast
+    across a CTA pair; measured slower, kept for the record) against fp32 attention, incl. a
+    ragged query tile count (padding CTA of the pair) and kv tail"""
+    import os
+    import subprocess
+    import sys
+
+    torch = _t()
+    D = 128
+    g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
+    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
+    torch.save((q.cpu(), k.cpu(), v.cpu()), tmp_path / "in.pt")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPX_ATTN_KERNEL=kernel,
+               PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(tmp_path / "in.pt"),
+                        str(tmp_path / "out.pt")], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    o = torch.load(tmp_path / "out.pt").cuda()
+    qf, kf, vf = (t.float().transpose(1, 2) for t in (q, k, v))
+    ref = (torch.softmax(qf @ kf.transpose(-1, -2) / math.sqrt(D), dim=-1) @ vf).transpose(1, 2)
+    assert rel_l2(o.float(), ref) < 1e-2
