@@ -352,6 +352,7 @@ void Engine::build_plans() {
             q.M = static_cast<int>(Lp_);
             q.N = static_cast<int>(3 * C_);
             q.K = static_cast<int>(C_);
+            q.b_constant = true;  // weights: uploaded synchronously, never written by a kernel
             gemm_plan(&rs.qkv_plan[l], q, sms);
 
             GemmOperands o{};
@@ -373,6 +374,7 @@ void Engine::build_plans() {
             o.M = static_cast<int>(Lp_);
             o.N = static_cast<int>(C_);
             o.K = static_cast<int>(C_);
+            o.b_constant = true;
             gemm_plan(&rs.o_plan[l], o, sms);
 
             AttnOperands a{};

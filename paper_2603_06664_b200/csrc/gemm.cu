@@ -53,6 +53,7 @@ struct GemmParams {
     int head_shift;         // log2(head_dim)
     int8_t head_group[16];  // head -> its head group g
     int8_t head_slot[16];   // head -> index within the group
+    int b_early;      // stages whose B tile the producer loaded before griddepcontrol.wait
     int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation,
                       // 5 = per-tile clock64 timeline of the pair kernel into `trace`
     long long* trace;  // [cta][16 tiles][4]: mma start, mma issued, epilogue start, end
@@ -296,6 +297,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tempty[a], kEpiWarps);  // one arrival per epilogue warp
         }
         fence_mbar_init();
+        // B (weights) of this CTA's first tile: not produced by the previous kernel, so it
+        // streams in while that kernel drains; A follows after the PDL wait
+        if (static_cast<int>(blockIdx.x) < num_tiles) {
+            const int n0 = (static_cast<int>(blockIdx.x) / p.num_m_tiles) * BN;
+            for (int kt = 0; kt < p.b_early; ++kt) {
+                mbar_arrive_expect_tx(&full[kt], kABytes + kBBytes);
+                tma_load_2d(sB + kt * kBBytes, &map_b, &full[kt], kt * kBK, n0);
+            }
+        }
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
     // the previous kernel's outputs (A operand, destinations, a per-call RoPE table) are
@@ -318,11 +328,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = (tile / p.num_m_tiles) * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
+                    const bool early = tile == static_cast<int>(blockIdx.x) && kt < p.b_early;
+                    if (!early) mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
                     const int k0 = kt * kBK;
                     tma_load_3d(sA + stage * kABytes, &map_a, &full[stage], k0 % p.k_inner, m0,
                                 k0 / p.k_inner);
-                    tma_load_2d(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
+                    if (!early) tma_load_2d(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -762,6 +773,15 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     if ((experiment == 5 && rope) || experiment == 7) p.trace = gemm_trace_buffer();
     p.experiment = p.trace ? 5 : (experiment == 5 || experiment == 7 ? 0 : experiment);
     p.span = span_slot();
+    // the pair kernel's B halves complete on the leader's barrier (initialised cluster-wide
+    // only after its prologue sync): early B loads are a single-CTA-kernel feature
+    static const bool early_env = [] {  // SPX_GEMM_EARLY_B=0 turns it off (A/B)
+        const char* e = std::getenv("SPX_GEMM_EARLY_B");
+        return !(e && std::atoi(e) == 0);
+    }();
+    p.b_early = (early_env && o.b_constant && !plan.pair)
+                    ? std::min(p.K / kBK, plan.bn == 192 && p.epi_mode != 2 ? 5 : kStages)
+                    : 0;
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         launch_pdl(gemm_bf16_tn_pair_kernel<256>, dim3(plan.grid), dim3(kThreads),

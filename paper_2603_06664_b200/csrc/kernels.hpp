@@ -33,6 +33,9 @@ struct GemmOperands {
     const bf16* residual = nullptr;
     int64_t residual_row_stride = 0;
     const float* gate = nullptr;
+    // B is not written by the kernel launched just before (e.g. weights): its first pipeline
+    // stages are loaded before griddepcontrol.wait, overlapping the previous kernel's tail
+    bool b_constant = false;
 };
 
 struct GemmPlan {
