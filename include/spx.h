@@ -262,8 +262,10 @@ typedef struct spx_engine_config {
                                          the QKV projection (K1), x + gate * W_o o in the
                                          O-projection epilogue (extension, no reference
                                          counterpart; per-layer shift/scale/gate) */
-    int32_t l2_prefetch;              /* 1 (default): the attention kernel warms the next
-                                         projections' weights into L2 (bulk prefetch) */
+    int32_t l2_prefetch;              /* 1: the attention kernel warms the next projections'
+                                         weights into L2 (bulk prefetch); 0 (default) since
+                                         the weight-tile-early GEMM pipelines made it a net
+                                         loss under the power cap */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */

@@ -438,7 +438,7 @@ class GenerationConfig:
     profile: bool = False
     fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
     adaln: bool = False  # Wan adaLN modulation + gated residual (extension, default off)
-    l2_prefetch: bool = True  # attention warms the next projections' weights into L2
+    l2_prefetch: bool = False  # attention warms the next projections' weights into L2 (opt-in)
     ablation: AblationFlags = field(default_factory=AblationFlags.all_on)
 
     def block_len(self):

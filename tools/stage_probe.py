@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--chunks", type=int, default=5)
     ap.add_argument("--label", default="")
     ap.add_argument("--wan", action="store_true", help="Wan mode: QK-RMSNorm + adaLN modulation")
-    ap.add_argument("--no-prefetch", action="store_true", help="no L2 weight prefetch in attention")
+    ap.add_argument("--prefetch", action="store_true", help="L2 weight prefetch in attention (opt-in)")
     args = ap.parse_args()
     F, Hg, Wg, H, D, layers, steps = 3, 30, 52, 12, 128, 30, 4
     L, C = F * Hg * Wg, H * D
@@ -32,7 +32,7 @@ def main():
                                   layers=layers, denoise_steps=steps, heads=H, head_dim=D,
                                   world_size=args.P, seed=0, profile=False,
                                   fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=args.wan,
-                                  adaln=args.wan, l2_prefetch=not args.no_prefetch)
+                                  adaln=args.wan, l2_prefetch=args.prefetch)
     eng = spattn.Engine(cfg, world=world)
     Lp = L // args.P
     noise = [torch.randn(steps, Lp, C, device="cuda").mul_(D ** -0.5).to(torch.bfloat16)
