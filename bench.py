@@ -177,6 +177,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
 
     import torch
 
@@ -188,6 +190,13 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world_size != args.gpus:
         world_size = args.gpus if world_size == 1 and args.gpus == 1 else world_size
+    few_gpus = world_size > 1 and torch.cuda.device_count() < world_size and not args.same_device
+    if few_gpus:  # N ranks, fewer GPUs: every rank on cuda:0 (a path check, said in the line)
+        if args.transport != "peer":
+            raise SystemExit(f"--gpus {world_size} on {torch.cuda.device_count()} GPU(s) needs "
+                             "the PEER transport (ranks share cuda:0)")
+        args.same_device = True
+        args.same_device_auto = True
     device = 0 if args.same_device else local_rank
     torch.cuda.set_device(device)
     dist = None
@@ -379,7 +388,14 @@ def main():
                    "global_batch": 1, "seq_len": L, "parallelism": f"sp{world_size}",
                    "transport": (args.transport if world_size > 1 else "none") +
                                 (" (same device: path check, not a scaling number)" if args.same_device else ""),
+                   "same_device": bool(args.same_device),
+                   **({"same_device_reason": f"{torch.cuda.device_count()} visible GPU(s) for "
+                                             f"{world_size} ranks: every rank time-slices cuda:0"}
+                      if getattr(args, "same_device_auto", False) else {}),
                    "head_groups": eng.head_groups, "query_splits": eng.query_splits,
+                   "kv_cache": "C2 = the first chunk of a video: each timed chunk re-denoises block "
+                               "0, which attends its own 3 frames (4680 keys); chunks that attend "
+                               "longer caches are in video_5s (C3) and video_60s (C5)",
                    "l2": "inputs larger than L2: 566 MB of weights + 58 MB KV ring stream per chunk"},
         "e2e": {"value": e2e_fps, "unit": "latent frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "first_frame_latency_ms": e2e_s / args.steps * 1e3},
@@ -423,6 +439,20 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def spawn_ranks(args):
+    """--gpus N without a torchrun environment: launch the N ranks ourselves (one process per
+    GPU, rendezvous on 127.0.0.1) and forward rank 0's line; exit status = the worst rank's."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 def exchange_summary(ledger, world_size, args, ms_per_chunk):

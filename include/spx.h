@@ -10,7 +10,8 @@
  *   - every call returns spx_status; on failure spx_last_error() holds a message
  *     (thread-local). No C++ exception crosses the ABI;
  *   - "stream" arguments are cudaStream_t passed as void* (NULL = legacy default stream);
- *   - allocation happens only in *_create calls, never in the per-layer hot path.
+ *   - allocation happens only in *_create calls (and spx_world_reserve), never in the
+ *     per-layer hot path.
  */
 #ifndef SPX_H_
 #define SPX_H_
@@ -128,8 +129,9 @@ spx_status spx_attention(const void* q, const void* k, const void* v, void* o, i
  * ------------------------------------------------------------------------------------- */
 typedef struct spx_kv_ring spx_kv_ring;
 
-/* window_frames < 0 -> unlimited; capacity_frames <= 0 -> derived (window rounded up to a
- * multiple of 3 frames, or 64 frames when unlimited) */
+/* window_frames < 0 -> unlimited; capacity_frames <= 0 -> derived: the window itself, or 64
+ * frames when unlimited (an update that would need more than the capacity raises
+ * SPX_ERR_RANGE; pass capacity_frames explicitly for longer unlimited caches) */
 spx_status spx_kv_ring_create(int device, int64_t tokens_per_frame, int64_t window_frames,
                               int64_t capacity_frames, int64_t heads, int64_t head_dim,
                               spx_kv_ring** out);
@@ -186,12 +188,17 @@ spx_status spx_world_synchronize(spx_world* world);
 spx_status spx_world_stats(const spx_world* world, spx_comm_stats* out);
 spx_status spx_world_reset_stats(spx_world* world);
 
+/* NCCL transport: size the staging buffer of the standalone collectives up front (bytes;
+ * all_to_all needs 2 x P x its per-rank input, fused_all_to_all 6 x P x one tensor's,
+ * all_gather P x its input). Without it the first call of a larger size allocates once. */
+spx_status spx_world_reserve(spx_world* world, int64_t bytes);
 /* all_to_all(rank, x, scatter, gather) (collectives.cpp:203-235); shape = per-rank input
  * (B, S, H, D); elem_bytes in {1,2,4,8}; out holds the per-rank result */
 spx_status spx_all_to_all(spx_world* world, void* const* in, void* const* out,
                           const int64_t shape[4], int32_t elem_bytes, int32_t scatter_axis,
                           int32_t gather_axis);
-/* fused_all_to_all(rank, q, k, v) (collectives.cpp:237-276): one invocation, one round */
+/* fused_all_to_all(rank, q, k, v) (collectives.cpp:237-276): one invocation, one round --
+ * on NCCL one group, one message per peer carrying the q, k and v chunks */
 spx_status spx_fused_all_to_all(spx_world* world, void* const* q_in, void* const* k_in,
                                 void* const* v_in, void* const* q_out, void* const* k_out,
                                 void* const* v_out, const int64_t shape[4], int32_t elem_bytes,
@@ -310,6 +317,11 @@ spx_status spx_engine_generate_block(spx_engine* engine, int64_t block, const ui
  * out_dev[local rank] receives (L/P, H, D); asynchronous on the world's streams */
 spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
                                             const void* const* noise_dev, void* const* out_dev);
+/* one denoise step of a block (the per-step body of generate, generator.cpp:94-110):
+ * KvCache::update of the block, then every layer on x_local[local rank] (device bf16
+ * (L/P, H, D)) into y_local[local rank]; asynchronous on the world's streams */
+spx_status spx_engine_denoise_step(spx_engine* engine, int64_t block, int64_t step,
+                                   const void* const* x_local, void* const* y_local);
 /* generate(cfg): every block; out_host: (num_blocks, rows_local, H, D) bf16 */
 spx_status spx_engine_generate(spx_engine* engine, uint16_t* out_host);
 spx_status spx_engine_synchronize(spx_engine* engine);
@@ -327,6 +339,20 @@ spx_status spx_engine_stats(const spx_engine* engine, spx_comm_stats* out);
  * order (any host channel: torch.distributed, MPI, a file) and passes them to _import. */
 spx_status spx_engine_ipc_export(spx_engine* engine, void* out, int64_t capacity, int64_t* bytes);
 spx_status spx_engine_ipc_import(spx_engine* engine, const void* blobs, int64_t bytes_per_rank);
+
+/* verify_stream(cfg, tol) (proj/src/generator.cpp:149-177, generator.hpp:65-83): runs cfg on a
+ * LOCAL world of world_size ranks (devices[r], NULL = all on the current device) and the
+ * P = 1 optimized path (= the reference pipeline at P = 1, true start frames) with the same
+ * seeded weights and noise, and reports per block the max |variant - expected| over the bf16
+ * outputs. blocks[] needs num_blocks entries; ledger (optional) = the variant's CommStats. */
+typedef struct spx_verify_block {
+    int64_t block;
+    double max_abs_dev;
+    int32_t pass;
+} spx_verify_block;
+spx_status spx_verify_stream(const spx_engine_config* cfg, int32_t world_size, const int* devices,
+                             double tolerance, spx_verify_block* blocks, int64_t max_blocks,
+                             int32_t* pass, spx_comm_stats* ledger);
 
 /* ---------------------------------------------------------------------------------------
  * Debug / GPU-oracle kernels (fp32 SIMT; tests only)

@@ -1,0 +1,236 @@
+"""GPU fp64 ORACLE -- test infrastructure only (tests/ and nothing else; the product path never
+imports it). A torch float64 restatement of the reference P = 1 path on a CUDA device, for
+the Wan-shape configurations the CPU oracle cannot finish (one Wan layer call takes 6 minutes
+on the CPU reference):
+
+  reference_self_attention   proj/src/sp_attention.cpp:317-348  (QKV -> global RoPE -> cache
+                                                                  -> SDPA -> W_o)
+  project_tokens             proj/src/sp_attention.cpp:51-75    (y = W x, W [out][in])
+  rotate_rows                proj/src/rope.cpp:78-131            (interleaved pairs, bands T|H|W)
+  KvCache::update / read     proj/src/kv_cache.cpp:18-67         (pop same block, append, evict)
+  scaled_dot_product_attention proj/src/tensor.cpp:161-209       (max-subtracted softmax, no mask)
+  generate                   proj/src/generator.cpp:50-147       (steps do not chain)
+
+plus the Wan-mode extensions the CPU oracle (oracle/spattn_oracle.cpp) restates: QK-RMSNorm
+and the adaLN modulation + gated residual. Everything is float64; the RoPE tables, seeded
+weights and noise come from the CPU oracle (liboracle: the reference's own RNG and std::pow /
+cos / sin), so only the summation order of the matmuls differs from the CPU oracle. It is
+pinned to the CPU oracle at the shapes that one finishes (tests/test_gpu_wan_parity.py:
+relative difference <= 1e-12).
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+import numpy as np
+
+from . import oracle
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class RopeRows:
+    """cos/sin of every (row, pair) of a block starting at frame `start` (P = 1 positions:
+    i_g = i, t = start + i / HW, h = (i mod HW) / W_g, w = i mod W_g; rope.cpp:97-101), built from
+    the reference's table values (precompute_frequencies, rope.cpp:21-64)."""
+
+    def __init__(self, grid, max_frames, head_dim, base=10000.0, split=None, device="cuda"):
+        torch = _torch()
+        F, Hg, Wg = grid
+        self.grid = grid
+        sp = tuple(split) if split else oracle.band_split(head_dim)
+        self.split = sp
+        ext = (max_frames, Hg, Wg)
+        tabs = []
+        for band in range(3):
+            c = np.empty((ext[band], sp[band]))
+            s = np.empty((ext[band], sp[band]))
+            for m in range(ext[band]):
+                for j in range(sp[band]):
+                    c[m, j], s[m, j] = oracle.table_at(head_dim, band, m, j, base, split)
+            tabs.append((torch.from_numpy(c).to(device), torch.from_numpy(s).to(device)))
+        self.tabs = tabs
+        self.max_frames = max_frames
+        self.device = device
+        self._cache = {}
+
+    def rows(self, start):
+        if start in self._cache:
+            return self._cache[start]
+        torch = _torch()
+        F, Hg, Wg = self.grid
+        hw = Hg * Wg
+        if start + F > self.max_frames:
+            raise ValueError("block frames exceed the table")  # RangeError (rope.cpp:86-94)
+        i = torch.arange(F * hw, device=self.device)
+        pos = (start + i // hw, (i % hw) // Wg, i % Wg)
+        cos = torch.cat([self.tabs[b][0][pos[b]] for b in range(3)], dim=1)
+        sin = torch.cat([self.tabs[b][1][pos[b]] for b in range(3)], dim=1)
+        self._cache[start] = (cos, sin)
+        return cos, sin
+
+
+def rope(x, cos, sin):
+    """x (L, H, D) float64: (a, b) -> (a c - b s, a s + b c) on pairs (2j, 2j+1)."""
+    a = x[..., 0::2]
+    b = x[..., 1::2]
+    c = cos[:, None, :]
+    s = sin[:, None, :]
+    out = _torch().empty_like(x)
+    out[..., 0::2] = a * c - b * s
+    out[..., 1::2] = a * s + b * c
+    return out
+
+
+def sdpa(q, k, v, head_chunk=4):
+    """q (Sq, H, D), k/v (Skv, H, D) float64 -> (Sq, H, D): softmax(q k^T / sqrt(D)) v, no mask."""
+    torch = _torch()
+    D = q.shape[-1]
+    out = torch.empty_like(q)
+    for h0 in range(0, q.shape[1], head_chunk):
+        h1 = min(q.shape[1], h0 + head_chunk)
+        qh = q[:, h0:h1].transpose(0, 1)
+        kh = k[:, h0:h1].transpose(0, 1)
+        vh = v[:, h0:h1].transpose(0, 1)
+        logits = torch.matmul(qh, kh.transpose(1, 2)) / math.sqrt(D)
+        w = torch.softmax(logits, dim=-1)
+        del logits
+        out[:, h0:h1] = torch.matmul(w, vh).transpose(0, 1)
+        del w
+    return out
+
+
+def rms_norm(x, w, eps):
+    """x (L, C): x / sqrt(mean(x^2) + eps) * w (the oracle's rms_norm, spattn_oracle.cpp)."""
+    torch = _torch()
+    r = 1.0 / torch.sqrt((x * x).sum(dim=1, keepdim=True) / x.shape[1] + eps)
+    return x * r * (w[None, :] if w is not None else 1.0)
+
+
+def layernorm_modulate(x, shift, scale, eps):
+    mean = x.mean(dim=1, keepdim=True)
+    var = ((x - mean) ** 2).mean(dim=1, keepdim=True)
+    return (x - mean) / _torch().sqrt(var + eps) * (1.0 + scale[None, :]) + shift[None, :]
+
+
+class FrameCache:
+    """KvCache (kv_cache.cpp:18-67): frames tagged by block index; update pops the trailing
+    frames of the same block, appends the block's frames, evicts from the front while more
+    than `window` frames are held; read() is the chronological concatenation."""
+
+    def __init__(self, hw, window=None):
+        self.hw = hw
+        self.window = window
+        self.frames = []  # (block, k (hw, H, D), v)
+
+    def update(self, block, k, v):
+        while self.frames and self.frames[-1][0] == block:
+            self.frames.pop()
+        F = k.shape[0] // self.hw
+        for f in range(F):
+            sl = slice(f * self.hw, (f + 1) * self.hw)
+            self.frames.append((block, k[sl], v[sl]))
+        if self.window is not None:
+            while len(self.frames) > self.window:
+                self.frames.pop(0)
+
+    def read(self):
+        torch = _torch()
+        return (torch.cat([f[1] for f in self.frames]), torch.cat([f[2] for f in self.frames]))
+
+
+class ReferenceModel:
+    """generate() of the reference P = 1 pipeline (generator.cpp:50-147) in float64 on a GPU.
+
+    weights: (layers, 4, C, C) numpy [q|k|v|o] ([out][in]) or None (the reference's seeded init
+    AttentionLayerParams::seeded, derive_seed(seed, 0x20, layer)); round_inputs: round weights
+    and noise to bf16 first (the device path's inputs). qk_norm / modulation: the Wan-mode
+    extensions (modulation (layers, 3, C) [shift | scale | gate])."""
+
+    def __init__(self, frames, grid_h, grid_w, heads, head_dim, layers, num_blocks, steps,
+                 window=None, seed=0, base=10000.0, split=None, weights=None, round_inputs=True,
+                 qk_norm=False, norm_weights=None, modulation=None, norm_eps=1e-6,
+                 force_start_frame_zero=False, device="cuda"):
+        torch = _torch()
+        self.grid = (frames, grid_h, grid_w)
+        self.H, self.D = heads, head_dim
+        self.C = heads * head_dim
+        self.L = frames * grid_h * grid_w
+        self.layers, self.num_blocks, self.steps = layers, num_blocks, steps
+        self.window, self.seed = window, seed
+        self.round_inputs = round_inputs
+        self.device = device
+        self.force0 = force_start_frame_zero
+        self.table = RopeRows(self.grid, num_blocks * frames, head_dim, base, split, device)
+        W = []
+        for l in range(layers):
+            w = weights[l] if weights is not None else oracle.layer_weights(seed, l, self.C)
+            if round_inputs:
+                w = oracle.round_bf16(w)
+            W.append(torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)).to(device))
+        self.W = W
+        self.qk_norm = qk_norm
+        self.norm_eps = norm_eps
+        self.norm_w = None
+        if qk_norm and norm_weights is not None:
+            self.norm_w = torch.from_numpy(np.asarray(norm_weights, dtype=np.float64)).to(device)
+        self.mod = None
+        if modulation is not None:
+            self.mod = torch.from_numpy(np.asarray(modulation, dtype=np.float64)).to(device)
+        self.reset()
+
+    def reset(self):
+        hw = self.grid[1] * self.grid[2]
+        self.caches = [FrameCache(hw, self.window) for _ in range(self.layers)]
+
+    def noise(self, block, step):
+        x = oracle.block_noise(self.seed, block, step, (self.L, self.H, self.D))
+        if self.round_inputs:
+            x = oracle.round_bf16(x)
+        return _torch().from_numpy(x.reshape(self.L, self.C)).to(self.device)
+
+    def layer(self, l, block, start, x):
+        """reference_self_attention (sp_attention.cpp:317-348) on x (L, C) float64."""
+        W = self.W[l]
+        L, H, D = self.L, self.H, self.D
+        xin = x
+        if self.mod is not None:
+            m = self.mod[l]
+            xin = layernorm_modulate(x, m[0], m[1], self.norm_eps)
+        q, k, v = (xin @ W[m].t() for m in range(3))
+        if self.qk_norm:
+            nq = self.norm_w[l, 0] if self.norm_w is not None else None
+            nk = self.norm_w[l, 1] if self.norm_w is not None else None
+            q = rms_norm(q, nq, self.norm_eps)
+            k = rms_norm(k, nk, self.norm_eps)
+        cos, sin = self.table.rows(start)
+        q = rope(q.reshape(L, H, D), cos, sin)
+        k = rope(k.reshape(L, H, D), cos, sin)
+        cache = self.caches[l]
+        cache.update(block, k, v.reshape(L, H, D))
+        kk, vv = cache.read()
+        o = sdpa(q, kk, vv).reshape(L, self.C)
+        y = o @ W[3].t()
+        if self.mod is not None:
+            return x + self.mod[l, 2][None, :] * y
+        return y
+
+    def block(self, b, noise=None):
+        """one block: steps x layers calls (generator.cpp:89-115); noise: optional
+        callable(step) -> (L, C) float64 tensor (default: the reference's seeded draws)."""
+        start = 0 if self.force0 else b * self.grid[0]
+        x = None
+        for s in range(self.steps):
+            x = noise(s) if noise is not None else self.noise(b, s)
+            for l in range(self.layers):
+                x = self.layer(l, b, start, x)
+        return x
+
+    def generate(self):
+        """(num_blocks, L, C) float64 numpy (generate, generator.cpp:50-147)."""
+        return np.stack([self.block(b).cpu().numpy() for b in range(self.num_blocks)])

@@ -90,6 +90,12 @@ class EngineConfig(ctypes.Structure):
                 ("l2_prefetch", c_int32)]
 
 
+class VerifyBlock(ctypes.Structure):
+    """spx_verify_block: VerificationReport::BlockCheck (proj/include/spattn/generator.hpp:68-73)."""
+
+    _fields_ = [("block", c_int64), ("max_abs_dev", c_double), ("pass_", c_int32)]
+
+
 # (name, restype, argtypes); restype None for void
 _SIGS = [
     ("spx_abi_version", c_int, []),
@@ -136,6 +142,7 @@ _SIGS = [
     ("spx_world_synchronize", c_int, [c_void_p]),
     ("spx_world_stats", c_int, [c_void_p, POINTER(CommStats)]),
     ("spx_world_reset_stats", c_int, [c_void_p]),
+    ("spx_world_reserve", c_int, [c_void_p, c_int64]),
     ("spx_all_to_all", c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_int64),
                                c_int32, c_int32, c_int32]),
     ("spx_fused_all_to_all", c_int, [c_void_p] + [POINTER(c_void_p)] * 6 + [POINTER(c_int64), c_int32,
@@ -160,6 +167,9 @@ _SIGS = [
     ("spx_engine_generate_block", c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     ("spx_engine_generate_block_device", c_int, [c_void_p, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
     ("spx_engine_generate", c_int, [c_void_p, c_void_p]),
+    ("spx_engine_denoise_step", c_int, [c_void_p, c_int64, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
+    ("spx_verify_stream", c_int, [POINTER(EngineConfig), c_int32, POINTER(c_int), c_double,
+                                  POINTER(VerifyBlock), c_int64, POINTER(c_int32), POINTER(CommStats)]),
     ("spx_engine_synchronize", c_int, [c_void_p]),
     ("spx_engine_stage_times", c_int, [c_void_p, POINTER(c_double), POINTER(c_int64)]),
     ("spx_engine_reset_stage_times", c_int, [c_void_p]),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -599,13 +600,21 @@ spx_status spx_world_reset_stats(spx_world* world) {
     });
 }
 
+spx_status spx_world_reserve(spx_world* world, int64_t bytes) {
+    return guarded([&] {
+        require_ptr(world, "world");
+        require(bytes >= 0, SPX_ERR_CONFIG, "bytes must be >= 0");
+        world->w->reserve(static_cast<size_t>(bytes));
+    });
+}
+
 spx_status spx_all_to_all(spx_world* world, void* const* in, void* const* out,
                           const int64_t shape[4], int32_t elem_bytes, int32_t scatter_axis,
                           int32_t gather_axis) {
     return guarded([&] {
         require_ptr(world, "world");
         require(in && out && shape, SPX_ERR_CONFIG, "null argument");
-        world->w->all_to_all(in, out, shape, elem_bytes, scatter_axis, gather_axis, false);
+        world->w->all_to_all(in, out, shape, elem_bytes, scatter_axis, gather_axis);
     });
 }
 
@@ -782,6 +791,63 @@ spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
     return guarded([&] {
         require(engine && noise_dev && out_dev, SPX_ERR_CONFIG, "null argument");
         engine->e->generate_block_device(block, noise_dev, out_dev);
+    });
+}
+
+spx_status spx_engine_denoise_step(spx_engine* engine, int64_t block, int64_t step,
+                                   const void* const* x_local, void* const* y_local) {
+    return guarded([&] {
+        require(engine && x_local && y_local, SPX_ERR_CONFIG, "null argument");
+        engine->e->denoise_step(block, step, x_local, y_local);
+    });
+}
+
+spx_status spx_verify_stream(const spx_engine_config* cfg, int32_t world_size, const int* devices,
+                             double tolerance, spx_verify_block* blocks, int64_t max_blocks,
+                             int32_t* pass, spx_comm_stats* ledger) {
+    return guarded([&] {
+        require(cfg && blocks && pass, SPX_ERR_CONFIG, "null argument");
+        require(max_blocks >= cfg->num_blocks, SPX_ERR_SHAPE,
+                "blocks[] holds " + std::to_string(max_blocks) + " entries, the run has " +
+                    std::to_string(cfg->num_blocks) + " blocks");
+        // the variant: cfg on a LOCAL world of world_size ranks (devices may repeat)
+        const int64_t L = cfg->frames * cfg->grid_h * cfg->grid_w;
+        const size_t per_block = static_cast<size_t>(L * cfg->heads * cfg->head_dim);
+        std::vector<uint16_t> got(per_block * static_cast<size_t>(cfg->num_blocks));
+        std::vector<uint16_t> want(got.size());
+        {
+            World w(world_size, devices);
+            Engine e(&w, *cfg);
+            e.seed_weights();
+            e.generate(got.data());
+            if (ledger) *ledger = w.stats();
+        }
+        // the expected run: the P = 1 optimized path (= the reference pipeline at P = 1) with
+        // the correct start frames (verify_stream, generator.cpp:149-177)
+        {
+            spx_engine_config rc = *cfg;
+            rc.ablation = SPX_ABLATION_ALL;
+            rc.force_start_frame_zero = 0;
+            const int dev0 = devices ? devices[0] : current_device();
+            World w(1, &dev0);
+            Engine e(&w, rc);
+            e.seed_weights();
+            e.generate(want.data());
+        }
+        bool all = true;
+        for (int64_t b = 0; b < cfg->num_blocks; ++b) {
+            double mx = 0.0;
+            for (size_t i = 0; i < per_block; ++i) {
+                const size_t k = static_cast<size_t>(b) * per_block + i;
+                const double d = std::fabs(bf16_to_f64(got[k]) - bf16_to_f64(want[k]));
+                if (!(d <= mx)) mx = d;  // NaN propagates as a failure
+            }
+            blocks[b].block = b;
+            blocks[b].max_abs_dev = mx;
+            blocks[b].pass = mx <= tolerance ? 1 : 0;
+            all = all && blocks[b].pass;
+        }
+        *pass = all ? 1 : 0;
     });
 }
 

@@ -8,11 +8,10 @@
 // The kernel (attn_fwd_v2_kernel below): one CTA = one 128-row query tile of one head, its kv
 // range split between two softmax warpgroups that ping-pong against one MMA thread. Template
 // modes (host selection in attn_run):
-//   0  default: 1-D grid, unsplit tiles first, then split-KV tiles merged through a workspace
-//   5  default when every tile has exactly 2 splits: the splits are a 2-CTA cluster, merged
-//      through DSMEM
-//   1, 2, 3  opt-in experiments measured slower on B200 (CTA-pair MMAs, K/V multicast, a
-//      persistent form); kept for the record and covered by tests
+//   0  1-D grid, unsplit tiles first, then split-KV tiles merged through a workspace
+//   5  every tile in exactly 2 splits: the splits are a 2-CTA cluster, merged through DSMEM
+// (Round 1 also measured CTA-pair MMAs, K/V multicast across a CTA pair and a persistent form;
+// all were slower on B200 and are gone from this file -- DESIGN.md section 5 has the numbers.)
 #include <algorithm>
 
 #include <atomic>
@@ -141,21 +140,15 @@ constexpr int kSlotsV2 = SPX_ATTN_SLOTS;
 
 template <int D, int kMode = 0>
 struct SmemV2 {
-    static constexpr bool kPair = kMode == 1;
     static constexpr uint32_t kChunks = D / 64;
-    // pair: each CTA holds half of every K tile (64 kv rows x D) and half of every V tile
-    // (128 kv rows x D/2), so a ring slot is half as large and the ring twice as deep
-    static constexpr uint32_t kTileBytes = kPair ? kBKV * D : kBKV * D * 2;
-    static constexpr uint32_t kSlots = (D == 128 ? kSlotsV2 : 2 * kSlotsV2) * (kPair ? 2 : 1);
-    // persistent mode: two Q buffers (the next unit's Q lands while this one's epilogue
-    // stages its output rows in the other)
+    static constexpr uint32_t kTileBytes = kBKV * D * 2;
+    static constexpr uint32_t kSlots = D == 128 ? kSlotsV2 : 2 * kSlotsV2;
     static constexpr uint32_t kQBytes = kBQ * D * 2;
     static constexpr uint32_t kOffQ = 0;
-    static constexpr uint32_t kOffRing = kOffQ + (kMode == 3 ? 2 : 1) * kQBytes;
+    static constexpr uint32_t kOffRing = kOffQ + kQBytes;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
-    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done[2], merge, o_free, q_empty[2],
-    // xfer_free
-    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 6 + 1 + 1 + 2 + 1;
+    // q_full, slot_full/empty[kSlots], s_full/p_full/pv_done[2], merge, xfer_free
+    static constexpr uint32_t kNumBars = 1 + 2 * kSlots + 6 + 1 + 1;
     static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
@@ -250,43 +243,17 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
         __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// kPair (D = 128 only; opt-in, see attn_run): a 2-CTA cluster = two adjacent query tiles of one head. The leader's
-// MMA thread issues M = 256 pair MMAs: S = Q K^T with each CTA supplying its own 128 query
-// rows and half of the K tile's 128 kv rows; O += P V with P read from each CTA's TMEM and
-// each CTA supplying half of V's head-dim columns. Per SM the K/V fill traffic and the SMEM
-// operand reads of the MMAs halve. Barriers that collect both CTAs (q_full, slot_full,
-// p_full) live in the leader; commits multicast to both CTAs.
-//
-// kMode 2 (kMcast, D = 128): a 2-CTA cluster = two adjacent query tiles of one head with
-// private MMA/softmax pipelines; only the K/V stream is shared. Each CTA's producer loads
-// half of every K/V tile (64 kv rows) with .multicast::cluster into BOTH CTAs' ring slot,
-// so every K/V byte leaves L2 once per 256 query rows (the single-CTA kernel is bounded by
-// the ~11 TB/s L2 -> SM TMA stream: 1430 TFLOP/s with the softmax switched off). A slot is
-// refilled only when both CTAs' MMAs have released it (multicast commits, count 2).
+// kMode 5: every (query tile, head) in exactly 2 kv splits, the two CTAs of a 2-CTA cluster.
+// Split 1 bulk-copies its normalised fp32 partial and log-sum-exp straight into split 0's
+// shared memory (DSMEM) and split 0 merges: no workspace round trip through L2, no completion
+// wait + atomic on the critical path.
 template <int D, int kMode>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    constexpr bool kPair = kMode == 1;
-    constexpr bool kMcast = kMode == 2;
-    constexpr bool kCluster = kPair || kMcast;
-    // kMode 3 (persistent): gridDim.x <= SMs CTAs walk the unsplit (query tile, head) units
-    // u = blockIdx.x + k gridDim.x. The producer and the MMA thread run into unit k + 1 while
-    // the softmax warpgroups finish unit k: the next Q lands in the other Q buffer, the first
-    // S tiles are computed into the free S columns, and only the first PV waits for the
-    // epilogue to have read O0|O1 out (o_free). Hides the per-CTA prologue, the Q load and
-    // first-tile latency and the CTA turnover of the one-CTA-per-unit grid.
-    constexpr bool kPersist = kMode == 3;
-    // kMode 5: every (query tile, head) in exactly 2 kv splits, the two CTAs of a 2-CTA
-    // cluster. Split 1 bulk-copies its normalised fp32 partial and log-sum-exp straight into
-    // split 0's shared memory (DSMEM) and split 0 merges: no workspace round trip through L2,
-    // no completion wait + atomic on the critical path.
     constexpr bool kSplitPair = kMode == 5;
     using L = SmemV2<D, kMode>;
-    static_assert(!kCluster || D == 128, "clustered attention is D = 128 only");
-    const int cta = kCluster ? static_cast<int>(cluster_ctarank()) : 0;
-    const bool leader = !kPair || cta == 0;
     constexpr uint32_t kSlots = L::kSlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -294,16 +261,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint8_t* sQ = smem + L::kOffQ;
     uint8_t* ring = smem + L::kOffRing;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-    uint64_t* q_full = bars;                 // [2] (persistent: per Q buffer)
-    uint64_t* slot_full = bars + 2;
+    uint64_t* q_full = bars;
+    uint64_t* slot_full = bars + 1;
     uint64_t* slot_empty = slot_full + kSlots;
     uint64_t* s_full = slot_empty + kSlots;  // [2]
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* pv_done = p_full + 2;          // [2]
     uint64_t* merge_bar = pv_done + 2;       // split-KV: other splits' partials landed
-    uint64_t* o_free = merge_bar + 1;        // persistent: O0|O1 read out by all 8 softmax warps
-    uint64_t* q_empty = o_free + 1;          // [2] persistent: Q buffer's staged rows stored
-    uint64_t* xfer_free = q_empty + 2;       // mode 5, split 1: the merging CTA's buffers are free
+    uint64_t* xfer_free = merge_bar + 1;     // mode 5, split 1: the merging CTA's buffers are free
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfer_free + 1);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
@@ -314,12 +279,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     span_begin(p.span);
     if (threadIdx.x == 0) attn_mark(p, 4);  // CTA entry
     int q_tile, head, split, ns;
-    if constexpr (kCluster) {
-        q_tile = blockIdx.x;
-        head = blockIdx.y;
-        split = blockIdx.z;
-        ns = p.splits;
-    } else if constexpr (kSplitPair) {
+    if constexpr (kSplitPair) {
         const int t = static_cast<int>(blockIdx.x) >> 1;
         split = static_cast<int>(cluster_ctarank());
         ns = 2;
@@ -342,18 +302,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         q_tile = t % p.qt;
         head = t / p.qt;
     }
-    // persistent: this CTA's units (all unsplit); one pass otherwise
-    const int n_units = kPersist ? p.qt * p.heads : 1;
-    const int my_units = kPersist ? (n_units - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
-                                        static_cast<int>(gridDim.x)
-                                  : 1;
-    // persistent: (q_tile, head) of this CTA's k-th unit
-#define enter_unit(k)                                                                   \
-    if constexpr (kPersist) {                                                           \
-        const int u_ = static_cast<int>(blockIdx.x) + (k) * static_cast<int>(gridDim.x); \
-        q_tile = u_ % p.qt;                                                             \
-        head = u_ / p.qt;                                                               \
-    }
     // this CTA's share [tb, tb + n_total) of the kv tiles, halved between the warpgroups
     const int tb = static_cast<int>((static_cast<int64_t>(split) * p.total_tiles) / ns);
     const int n_total = static_cast<int>((static_cast<int64_t>(split + 1) * p.total_tiles) / ns) - tb;
@@ -365,32 +313,23 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         tma_prefetch_desc(&map_q);
         tma_prefetch_desc(&map_k);
         tma_prefetch_desc(&map_v);
-        mbar_init(&q_full[0], 1);
-        mbar_init(&q_full[1], 1);
-        mbar_init(o_free, 8);
-        mbar_init(&q_empty[0], 8);
-        mbar_init(&q_empty[1], 8);
+        mbar_init(q_full, 1);
         for (uint32_t s = 0; s < kSlots; ++s) {
             mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_empty[s], kMcast ? 2 : 1);
+            mbar_init(&slot_empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], (kPair ? 2 : 1) * (SPX_PFULL_PER_WARP ? 4 : 128));
+            mbar_init(&p_full[i], SPX_PFULL_PER_WARP ? 4 : 128);
             mbar_init(&pv_done[i], 1);
         }
         mbar_init(merge_bar, 1);
         mbar_init(xfer_free, 1);
         fence_mbar_init();
     }
-    if (warp == 2) {
-        if constexpr (kPair)
-            tmem_alloc_pair<512>(tmem_slot);
-        else
-            tmem_alloc<512>(tmem_slot);
-    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
-    if constexpr (kCluster || kSplitPair)
+    if constexpr (kSplitPair)
         cluster_sync_all();
     else
         __syncthreads();
@@ -402,100 +341,45 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
 
     if (warp < 4) {
         setmaxnreg_dec56();
-        // values the producer / MMA roles need, re-derived after the register drop (params,
-        // shared memory) instead of carried across it: in the persistent form ptxas otherwise
-        // parks them in local memory and reloads them on the MMA issue path
-        const int rn0 = kPersist ? (p.total_tiles + 1) / 2 : n0;
-        const int rn1 = kPersist ? p.total_tiles - rn0 : n1;
-        const int rtb = kPersist ? 0 : tb;
-        const uint32_t rtmem = kPersist ? *reinterpret_cast<volatile uint32_t*>(tmem_slot) : tmem_base;
         if (warp == 0 && lane == 0) {
             // ---------------- TMA producer: the MMA consumption order ----------------
             uint32_t t = 0;
-#pragma unroll 1
-            for (int k = 0; k < my_units; ++k) {
-            enter_unit(k)
-            const int qb = kPersist ? (k & 1) : 0;
-            if (kPersist && k >= 2) mbar_wait(&q_empty[qb], ((k - 2) >> 1) & 1);
-            if (leader) mbar_arrive_expect_tx(&q_full[qb], (kPair ? 2 : 1) * kBQ * D * 2);
+            mbar_arrive_expect_tx(q_full, kBQ * D * 2);
 #pragma unroll
-            for (int c = 0; c < (int)L::kChunks; ++c) {
-                if constexpr (kPair)
-                    tma_load_3d_pair(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head,
-                                     q_tile * kBQ);
-                else
-                    tma_load_3d(sQ + qb * L::kQBytes + c * (kBQ * 128), &map_q, &q_full[qb], c * 64,
-                                head, q_tile * kBQ);
-            }
+            for (int c = 0; c < (int)L::kChunks; ++c)
+                tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
             auto load = [&](bool is_v, int g) {
                 const uint32_t slot = t % kSlots;
                 const uint32_t ph = (t / kSlots) & 1;
                 mbar_wait(&slot_empty[slot], ph ^ 1);
-                if (leader)
-                    mbar_arrive_expect_tx(&slot_full[slot], (kPair ? 2 : 1) * L::kTileBytes);
+                mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
                 int row, valid;
-                kv_tile_coords(p, rtb + g, row, valid);
+                kv_tile_coords(p, tb + g, row, valid);
                 uint8_t* dst = ring + slot * L::kTileBytes;
-                if constexpr (kMcast) {  // my 64 kv rows of the tile -> both CTAs' slot
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-                        tma_load_3d_mcast(dst + c * (kBKV * 128) + cta * (64 * 128),
-                                          is_v ? &map_v : &map_k, &slot_full[slot], c * 64, head,
-                                          row + cta * 64, 0x3);
-                } else if constexpr (kPair) {
-                    if (is_v)  // V half: all 128 kv rows, head-dim columns [64 cta, 64 cta + 64)
-                        tma_load_3d_pair(dst, &map_v, &slot_full[slot], cta * 64, head, row);
-                    else       // K half: kv rows [64 cta, 64 cta + 64), all head-dim columns
-#pragma unroll
-                        for (int c = 0; c < 2; ++c)
-                            tma_load_3d_pair(dst + c * (64 * 128), &map_k, &slot_full[slot],
-                                             c * 64, head, row + cta * 64);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < (int)L::kChunks; ++c)
-                        tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k,
-                                    &slot_full[slot], c * 64, head, row);
-                }
+                for (int c = 0; c < (int)L::kChunks; ++c)
+                    tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
+                                c * 64, head, row);
                 ++t;
             };
             load(false, 0);
-            if (rn1 > 0) load(false, rn0);
-            for (int j = 0; j < rn0; ++j) {
+            if (n1 > 0) load(false, n0);
+            for (int j = 0; j < n0; ++j) {
                 load(true, j);
-                if (j + 1 < rn0) load(false, j + 1);
-                if (j < rn1) {
-                    load(true, rn0 + j);
-                    if (j + 1 < rn1) load(false, rn0 + j + 1);
+                if (j + 1 < n0) load(false, j + 1);
+                if (j < n1) {
+                    load(true, n0 + j);
+                    if (j + 1 < n1) load(false, n0 + j + 1);
                 }
             }
-            }  // units
-            if constexpr (kCluster) {  // drain: every multicast release has landed
-                for (uint32_t k = 0; k < kSlots; ++k, ++t)
-                    mbar_wait(&slot_empty[t % kSlots], ((t / kSlots) & 1) ^ 1);
-            }
-        } else if (warp == 1 && leader) {
+        } else if (warp == 1) {
             // ---------------- MMA issuer ----------------
             // The whole warp runs the control flow (waits, slot and descriptor arithmetic stay
             // warp-uniform, in uniform registers); one elected lane issues the tcgen05 ops.
             const bool issuer = elect_one();
-            constexpr uint32_t kM = kPair ? 2 * kBQ : kBQ;
-            constexpr uint32_t idesc_s = make_idesc_bf16(kM, kBKV, false, false);
-            constexpr uint32_t idesc_o = make_idesc_bf16(kM, D, false, true);
-            constexpr uint32_t kKChunk = kPair ? 64 * 128 : kBKV * 128;  // K chunk stride
-            auto commit = [&](uint64_t* bar) {
-                if constexpr (kPair)
-                    umma_commit_pair(bar, 0x3);
-                else
-                    umma_commit(bar);
-            };
-            auto release = [&](uint64_t* bar) {  // a ring slot: both CTAs' producers refill it
-                if constexpr (kMcast)
-                    umma_commit_mcast(bar, 0x3);
-                else
-                    commit(bar);
-            };
-            uint32_t q_addr = smem_u32(sQ);
-            uint32_t unit_k = 0;  // persistent: this CTA's unit index (o_free, p_full phases)
+            constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
+            const uint32_t q_addr = smem_u32(sQ);
             const uint32_t ring_addr = smem_u32(ring);
             uint32_t t = 0;
             auto take = [&]() {
@@ -511,69 +395,42 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 if (issuer) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                        const uint32_t koff = (kk >> 2) * kKChunk + (kk & 3) * 32;
-                        if constexpr (kPair)
-                            umma_bf16_ss_pair(rtmem + i * 128,
-                                              make_desc_sw128(q_addr + qoff, 16, 1024),
-                                              make_desc_sw128(k_addr + koff, 16, 1024), idesc_s,
-                                              kk > 0);
-                        else
-                            umma_bf16_ss(rtmem + i * 128,
-                                         make_desc_sw128(q_addr + qoff, 16, 1024),
-                                         make_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0);
+                        const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                        umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
+                                     make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
                     }
-                    commit(&s_full[i]);
-                    release(&slot_empty[slot]);
+                    umma_commit(&s_full[i]);
+                    umma_commit(&slot_empty[slot]);
                 }
                 __syncwarp();
             };
             auto issue_pv = [&](int i, int j) {
                 const uint32_t slot = take();
-                // p_full completes once per tile of slot i: cumulative over the units
-                const uint32_t nth = unit_k * static_cast<uint32_t>(i == 0 ? rn0 : rn1) + j;
-                if constexpr (kPair)
-                    mbar_wait_cluster(&p_full[i], j & 1);
-                else if (p.experiment != 3)  // 3: profiling, MMA stream without softmax
-                    mbar_wait(&p_full[i], nth & 1);
-                // the first PV of a unit overwrites O_i: the previous unit's epilogue has read
-                // O0|O1 out
-                if (kPersist && j == 0 && unit_k > 0) mbar_wait(o_free, (unit_k - 1) & 1);
+                if (p.experiment != 3)  // 3: profiling, MMA stream without softmax
+                    mbar_wait(&p_full[i], j & 1);
                 tc_fence_after();
                 const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
                 if (issuer) {
 #pragma unroll
-                    for (int kk = 0; kk < kBKV / 16; ++kk) {
-                        if constexpr (kPair)
-                            umma_bf16_ts_pair(rtmem + 256 + i * 128,
-                                              rtmem + i * 128 + kk * 8,
-                                              make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                              idesc_o, (j | kk) != 0);
-                        else
-                            umma_bf16_ts(rtmem + 256 + i * 128, rtmem + i * 128 + kk * 8,
-                                         make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                         idesc_o, (j | kk) != 0);
-                    }
-                    commit(&pv_done[i]);
-                    release(&slot_empty[slot]);
+                    for (int kk = 0; kk < kBKV / 16; ++kk)
+                        umma_bf16_ts(tmem_base + 256 + i * 128, tmem_base + i * 128 + kk * 8,
+                                     make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                     idesc_o, (j | kk) != 0);
+                    umma_commit(&pv_done[i]);
+                    umma_commit(&slot_empty[slot]);
                 }
                 __syncwarp();
             };
-#pragma unroll 1
-            for (int k = 0; k < my_units; ++k, ++unit_k) {
-                const int qb = kPersist ? (k & 1) : 0;
-                q_addr = smem_u32(sQ) + qb * L::kQBytes;
-                mbar_wait(&q_full[qb], kPersist ? ((k >> 1) & 1) : 0);
-                tc_fence_after();
-                issue_s(0);
-                if (rn1 > 0) issue_s(1);
-                for (int j = 0; j < rn0; ++j) {
-                    issue_pv(0, j);
-                    if (j + 1 < rn0) issue_s(0);
-                    if (j < rn1) {
-                        issue_pv(1, j);
-                        if (j + 1 < rn1) issue_s(1);
-                    }
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            issue_s(0);
+            if (n1 > 0) issue_s(1);
+            for (int j = 0; j < n0; ++j) {
+                issue_pv(0, j);
+                if (j + 1 < n0) issue_s(0);
+                if (j < n1) {
+                    issue_pv(1, j);
+                    if (j + 1 < n1) issue_s(1);
                 }
             }
         }
@@ -589,28 +446,17 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const int n = i == 0 ? n0 : n1;
         const int g0 = tb + (i == 0 ? 0 : n0);
         const float scale = p.scale_log2;
-        // (loop state kept minimal: the softmax runs at the register limit; the unit's
-        // coordinates are derived again for the epilogue)
-#pragma unroll 1
-        for (int k = 0; k < my_units; ++k) {
-        // s_full / pv_done complete once per tile of this slot: cumulative over the units
-        const uint32_t nb = static_cast<uint32_t>(k) * static_cast<uint32_t>(n);
         float m_run = -INFINITY;
         float l_run = 0.0f;
         for (int j = 0; j < (p.experiment == 3 ? 0 : n); ++j) {
             int row, valid;
             kv_tile_coords(p, g0 + j, row, valid);
-            mbar_wait(&s_full[i], (nb + j) & 1);
+            mbar_wait(&s_full[i], j & 1);
             tc_fence_after();
             if (p.experiment == 1) {  // profiling: MMA/TMA/barrier skeleton only
                 tc_fence_before();
                 if (SPX_PFULL_PER_WARP) __syncwarp();
-                if (!SPX_PFULL_PER_WARP || lane == 0) {
-                    if constexpr (kPair)
-                        mbar_arrive_leader(&p_full[i]);
-                    else
-                        mbar_arrive(&p_full[i]);
-                }
+                if (!SPX_PFULL_PER_WARP || lane == 0) mbar_arrive(&p_full[i]);
                 continue;
             }
             // Exponent offset: the row max of the WG's FIRST tile only. Softmax is invariant to
@@ -678,7 +524,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             if (j > 0 && __any_sync(0xffffffffu, !(lt < 1.8446744e19f))) {  // 2^64, or inf / NaN
                 load_s();  // S is still in TMEM (P not written yet)
                 const float m_new = fmaxf(m_run, row_max() * scale);
-                mbar_wait(&pv_done[i], (nb + j - 1) & 1);
+                mbar_wait(&pv_done[i], (j - 1) & 1);
                 tc_fence_after();
                 const float alpha = ex2_approx(m_run - m_new);
 #pragma unroll 1
@@ -701,26 +547,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tmem_st_wait();
             tc_fence_before();
             if (SPX_PFULL_PER_WARP) __syncwarp();
-            if (!SPX_PFULL_PER_WARP || lane == 0) {
-                if constexpr (kPair)
-                    mbar_arrive_leader(&p_full[i]);
-                else
-                    mbar_arrive(&p_full[i]);
-            }
+            if (!SPX_PFULL_PER_WARP || lane == 0) mbar_arrive(&p_full[i]);
         }
         if (n > 0) {
-            mbar_wait(&pv_done[i], (nb + n - 1) & 1);
+            mbar_wait(&pv_done[i], (n - 1) & 1);
             tc_fence_after();
         }
-        {  // epilogue. Persistent: the lane-derived values are re-derived opaquely, so that
-           // the compiler cannot hoist the epilogue's address math out of the unit loop (it
-           // would stay live across the softmax loop, which runs at the register limit)
-        const int r = opaque_i32(q * 32 + lane);
-        const uint32_t lane_off = static_cast<uint32_t>(r & ~31) << 16;
-        const uint32_t tmem_base = opaque_u32(*tmem_slot);
+        // ---------------- epilogue ----------------
         if (threadIdx.x == 128) attn_mark(p, 1);
-        enter_unit(k)
-        const int qb = kPersist ? (k & 1) : 0;
         st_m[i * 128 + r] = m_run;
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
@@ -745,13 +579,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         }
         const uint32_t t_o0 = tmem_base + 256 + lane_off;
         const uint32_t t_o1 = tmem_base + 384 + lane_off;
-        if (kPersist || ns == 1) {  // (persistent units are never split)
+        if (ns == 1) {
             // rows staged as bf16 in the idle Q smem (16-byte units XOR-swizzled by row), then
             // copied out by all 256 softmax threads so that each store instruction writes whole
             // 128/256-byte row segments (the per-row 16-byte stores of a warp hit 32 rows)
             constexpr uint32_t kRowBytes = D * 2;
             constexpr uint32_t kU = kRowBytes / 16;
-            const uint32_t s_base = smem_u32(smem) + qb * L::kQBytes;  // this unit's Q buffer
+            const uint32_t s_base = smem_u32(smem);
 #pragma unroll 1
             for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
                 uint32_t o0[32], o1[32];
@@ -775,11 +609,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                  : "memory");
                 }
             }
-            if constexpr (kPersist) {  // O0|O1 read out: the next unit's first PV may overwrite
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(o_free);
-            }
             named_bar_sync(1, 256);
             const int tid = static_cast<int>(threadIdx.x) - 128;
 #pragma unroll 1
@@ -799,10 +628,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                              static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
                              static_cast<int64_t>(head) * D;
                 *reinterpret_cast<uint4*>(drow + u * 8) = w;
-            }
-            if constexpr (kPersist) {  // staged rows consumed: the Q buffer may be refilled
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&q_empty[qb]);
             }
         } else if constexpr (kSplitPair) {
             // ---- 2 splits merged through DSMEM ----
@@ -1019,26 +844,19 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
             }
         }
-        }  // epilogue
-        }  // units
     }
     if (threadIdx.x == 128) attn_mark(p, 3);
     tc_fence_before();
-    if constexpr (kCluster || kSplitPair)  // mode 5: split 1's smem is read by its bulk copy
+    if constexpr (kSplitPair)  // mode 5: split 1's smem is read by its bulk copy
         cluster_sync_all();
     else
         __syncthreads();
     span_end(p.span);
     if (warp == 2) {
         tc_fence_after();
-        if constexpr (kPair)
-            tmem_dealloc_pair<512>(tmem_base);
-        else
-            tmem_dealloc<512>(tmem_base);
+        tmem_dealloc<512>(tmem_base);
     }
 }
-
-#undef enter_unit
 
 template <int D, int kMode>
 void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
@@ -1051,7 +869,7 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
                                       static_cast<int>(SmemV2<D, kMode>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kMode == 1 || kMode == 2 || kMode == 5) {
+    if constexpr (kMode == 5) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kThreadsV2);
@@ -1066,10 +884,8 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
         attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-        // pair and multicast modes both load 64-row K boxes; multicast also 64-row V boxes
-        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q,
-                                    kMode == 5 ? plan.map_k : plan.map_k_pair,
-                                    kMode == 2 ? plan.map_v_half : plan.map_v, p));
+        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q, plan.map_k,
+                                    plan.map_v, p));
     } else {
         launch_pdl(attn_fwd_v2_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV2<D, kMode>::kBytes,
                    stream, plan.map_q, plan.map_k, plan.map_v, p);
@@ -1204,14 +1020,7 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count) {
                                      static_cast<uint64_t>(ops.heads) * ops.head_dim * 2};
         require(make_tma_map_bf16(&plan->map_k, ops.k, 3, dims, strides, box, err, sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
-        const uint32_t box_half[3] = {64, 1, 64};
-        require(make_tma_map_bf16(&plan->map_k_pair, ops.k, 3, dims, strides, box_half, err,
-                                  sizeof(err)),
-                SPX_ERR_ALIGNMENT, err);
         require(make_tma_map_bf16(&plan->map_v, ops.v, 3, dims, strides, box, err, sizeof(err)),
-                SPX_ERR_ALIGNMENT, err);
-        require(make_tma_map_bf16(&plan->map_v_half, ops.v, 3, dims, strides, box_half, err,
-                                  sizeof(err)),
                 SPX_ERR_ALIGNMENT, err);
     }
     attn_set_segments(plan, ops.seg_start, ops.seg_len, ops.num_segs);
@@ -1268,12 +1077,8 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         SPX_CUDA(cudaGetDevice(&dev));
         const int64_t n = ceil_div(static_cast<int64_t>(o.sq), kBQ) * o.heads * o.batch;
         const bool forced = g_forced_splits.load(std::memory_order_relaxed) != 0;
-        static const int mode_env = [] {
-            const char* e = std::getenv("SPX_ATTN_KERNEL");
-            return e && (std::string(e) == "pair" || std::string(e) == "mcast") ? 1 : 0;
-        }();
         p.qt = static_cast<int>(ceil_div(o.sq, kBQ));
-        if (forced || mode_env || o.head_dim != 128) {  // uniform splits
+        if (forced || o.head_dim != 128) {  // uniform splits
             const int want = forced ? plan.max_splits
                                     : choose_splits(n, p.total_tiles, device_sm_count(dev), plan.max_splits);
             p.splits = std::max(1, std::min(want, p.total_tiles / 2));
@@ -1305,40 +1110,8 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
         p.ws_lse = reinterpret_cast<float*>(ws + ctr);
         p.ws_o = reinterpret_cast<float*>(ws + ctr + lse);
     }
-    dim3 grid(static_cast<unsigned>(ceil_div(o.sq, kBQ)), static_cast<unsigned>(o.heads),
-              static_cast<unsigned>(o.batch));
-    // D = 128 kernel: 0 single CTA (default); opt-in, both measured slower on B200:
-    //   1 CTA-pair MMAs (SPX_ATTN_KERNEL=pair): 4680x4680x12 0.225 vs 0.135 ms -- every
-    //     S -> P -> PV hand-off crosses SMs with only two S buffers to hide it;
-    //   2 K/V multicast across a CTA pair (SPX_ATTN_KERNEL=mcast): 0.182 ms, and 0.87 vs
-    //     0.66 ms for the bare MMA stream at 32760 keys -- the ring fill is not the limit.
-    static const int mode128 = [] {
-        const char* e = std::getenv("SPX_ATTN_KERNEL");
-        if (e && std::string(e) == "pair") return 1;
-        if (e && std::string(e) == "mcast") return 2;
-        return 0;
-    }();
-    if (o.head_dim == 128 && mode128 != 0) {
-        grid.x = (grid.x + 1) & ~1u;  // whole CTA pairs; the padding tile's rows are all >= sq
-        grid.z = static_cast<unsigned>(p.splits);
-        if (mode128 == 1)
-            attn_v2_launch<128, 1>(grid, plan, p, stream);
-        else
-            attn_v2_launch<128, 2>(grid, plan, p, stream);
-    } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
+    {
         const int64_t T = static_cast<int64_t>(p.qt) * o.heads;
-        int dev = 0;
-        SPX_CUDA(cudaGetDevice(&dev));
-        const int sms = device_sm_count(dev);
-        // persistent form (opt-in, SPX_ATTN_PERSIST=1) when every unit is unsplit and there
-        // is more than one wave of them. Measured slower on B200 (tools/kbench.py, same box):
-        // 0.113 vs 0.1096 ms at the Wan chunk, 0.743 vs 0.701 ms at 32760 keys -- the steady
-        // state loses more (ncu: tensor pipe 64 vs 72 % active, L2 read sectors +15 %) than
-        // the hidden prologue / first-tile / epilogue latency gains
-        static const bool persist_env = [] {
-            const char* e = std::getenv("SPX_ATTN_PERSIST");
-            return e && std::atoi(e) == 1;
-        }();
         static const bool pair_merge = [] {  // SPX_ATTN_SPLIT_PAIR=0: the workspace merge
             const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
             return !(e && std::atoi(e) == 0);
@@ -1350,13 +1123,7 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 attn_v2_launch<128, 5>(g2, plan, p, stream);
             else
                 attn_v2_launch<64, 5>(g2, plan, p, stream);
-        } else if (persist_env && p.experiment != 5 && p.n_full == T && T > sms) {
-            const dim3 gp(static_cast<unsigned>(sms));
-            if (o.head_dim == 128)
-                attn_v2_launch<128, 3>(gp, plan, p, stream);
-            else
-                attn_v2_launch<64, 3>(gp, plan, p, stream);
-        } else {
+        } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
             const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
             if (o.head_dim == 128)
                 attn_v2_launch<128, 0>(g1, plan, p, stream);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <functional>
@@ -144,6 +145,7 @@ Engine::~Engine() {
         for (StageEvents& se : *set)
             for (cudaEvent_t e : se.ev) cudaEventDestroy(e);
     if (noise_pinned_) cudaFreeHost(noise_pinned_);
+    if (peer_error_host_) cudaFreeHost(peer_error_host_);
 }
 
 int Engine::local_of(int rank) const { return world_->local_index(rank); }
@@ -257,7 +259,19 @@ void Engine::peer_barrier(RankState& rs, int slot) {
     const uint64_t e = ++epoch_[slot];
     PeerFlags f{};
     for (int r = 0; r < P_; ++r) f.rank_flags[r] = peers_[static_cast<size_t>(r)].flags;
-    peer_barrier_run(f, rs.flags, static_cast<int>(P_), rs.rank, slot, e, rs.stream);
+    peer_barrier_run(f, rs.flags, static_cast<int>(P_), rs.rank, slot, e, peer_timeout_ns_,
+                     peer_error_dev_, rs.stream);
+}
+
+void Engine::check_peer_error() {
+    if (!peer_error_host_) return;
+    const int e = *reinterpret_cast<volatile int*>(peer_error_host_);
+    if (e == 0) return;
+    *reinterpret_cast<volatile int*>(peer_error_host_) = 0;
+    throw Error(SPX_ERR_COLLECTIVE,
+                "PEER barrier timed out waiting for rank " + std::to_string(e - 1) + " (after " +
+                    std::to_string(peer_timeout_ns_ / 1000000) +
+                    " ms; a rank died or left the collective order, collectives.cpp:42-52)");
 }
 
 void Engine::allocate() {
@@ -307,8 +321,17 @@ void Engine::allocate() {
                               Wg_ * table_->pairs(2);
             rs.tab_scratch = dev_alloc<float2>(rs, static_cast<size_t>(n));
         }
-        if (world_->transport() == SPX_TRANSPORT_PEER)
+        if (world_->transport() == SPX_TRANSPORT_PEER) {
             rs.flags = dev_alloc<uint64_t>(rs, static_cast<size_t>(kPeerSlots * P_));
+            SPX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&peer_error_host_), sizeof(int),
+                                   cudaHostAllocMapped));
+            *peer_error_host_ = 0;
+            SPX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&peer_error_dev_),
+                                              peer_error_host_, 0));
+            const char* t = std::getenv("SPX_PEER_TIMEOUT_MS");
+            const long long ms = t ? std::max(1LL, std::atoll(t)) : 60000LL;
+            peer_timeout_ns_ = static_cast<uint64_t>(ms) * 1000000ull;
+        }
         if (nccl) {
             rs.q_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
             rs.k_send = dev_alloc<bf16>(rs, static_cast<size_t>(G_) * slab);
@@ -458,6 +481,8 @@ void Engine::seed_weights() {
 void Engine::set_modulation(int64_t layer, const float* shift, const float* scale,
                             const float* gate) {
     require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    // kernels still in flight may read this layer's weights: drain the engine streams first
+    synchronize();
     require(shift && scale && gate, SPX_ERR_CONFIG, "null modulation vector");
     for (auto& kv : weights_) {
         SPX_CUDA(cudaSetDevice(kv.first));
@@ -466,11 +491,14 @@ void Engine::set_modulation(int64_t layer, const float* shift, const float* scal
         SPX_CUDA(cudaMemcpy(m + C_, scale, C_ * 4, cudaMemcpyHostToDevice));
         SPX_CUDA(cudaMemcpy(m + 2 * C_, gate, C_ * 4, cudaMemcpyHostToDevice));
     }
+    sync_weight_devices();
 }
 
 void Engine::set_layer_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk,
                                const uint16_t* wv, const uint16_t* wo) {
     require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    // kernels still in flight may read this layer's weights: drain the engine streams first
+    synchronize();
     const size_t mat = static_cast<size_t>(C_ * C_);
     for (auto& kv : weights_) {
         SPX_CUDA(cudaSetDevice(kv.first));
@@ -480,14 +508,28 @@ void Engine::set_layer_weights(int64_t layer, const uint16_t* wq, const uint16_t
         SPX_CUDA(cudaMemcpy(base + 2 * mat, wv, mat * 2, cudaMemcpyHostToDevice));
         SPX_CUDA(cudaMemcpy(kv.second.wo + layer * mat, wo, mat * 2, cudaMemcpyHostToDevice));
     }
+    sync_weight_devices();
 }
 
 void Engine::set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk) {
     require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    // kernels still in flight may read this layer's weights: drain the engine streams first
+    synchronize();
     for (auto& kv : weights_) {
         SPX_CUDA(cudaSetDevice(kv.first));
         SPX_CUDA(cudaMemcpy(kv.second.norm_q + layer * C_, wq, C_ * 2, cudaMemcpyHostToDevice));
         SPX_CUDA(cudaMemcpy(kv.second.norm_k + layer * C_, wk, C_ * 2, cudaMemcpyHostToDevice));
+    }
+    sync_weight_devices();
+}
+
+// the setters copy with cudaMemcpy on the legacy stream (a pageable H2D may return before its
+// DMA lands, and the engine streams are non-blocking): finish the copies on every weight
+// device before any later kernel can read them
+void Engine::sync_weight_devices() {
+    for (auto& kv : weights_) {
+        SPX_CUDA(cudaSetDevice(kv.first));
+        SPX_CUDA(cudaDeviceSynchronize());
     }
 }
 
@@ -847,16 +889,42 @@ void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_s
     begin_block(block);
     for (int64_t step = 0; step < cfg_.denoise_steps; ++step) {
         load_step(step);  // fresh noise into x[0] of every local rank (steps do not chain)
-        for (int64_t l = 0; l < cfg_.layers; ++l) {
-            std::vector<const GemmPlan*> qv, ov;
-            std::vector<const bf16*> xv;
-            for (RankState& rs : ranks_) {
-                qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
-                ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
-                xv.push_back(rs.x[l % 2]);
-            }
-            run_layer(l, start, qv, ov, xv);
+        run_step(start);
+    }
+}
+
+// the layers of one denoise step on x[0] of every local rank (output in x[layers % 2])
+void Engine::run_step(int64_t start) {
+    for (int64_t l = 0; l < cfg_.layers; ++l) {
+        std::vector<const GemmPlan*> qv, ov;
+        std::vector<const bf16*> xv;
+        for (RankState& rs : ranks_) {
+            qv.push_back(&rs.qkv_plan[static_cast<size_t>(l)]);
+            ov.push_back(&rs.o_plan[static_cast<size_t>(l)]);
+            xv.push_back(rs.x[l % 2]);
         }
+        run_layer(l, start, qv, ov, xv);
+    }
+}
+
+void Engine::denoise_step(int64_t block, int64_t step, const void* const* x, void* const* y) {
+    require(block >= 0 && block < cfg_.num_blocks, SPX_ERR_RANGE, "block out of range");
+    require(step >= 0 && step < cfg_.denoise_steps, SPX_ERR_RANGE,
+            "denoise step " + std::to_string(step) + " out of range [0, " +
+                std::to_string(cfg_.denoise_steps) + ")");
+    const size_t slice_bytes = static_cast<size_t>(Lp_ * C_) * sizeof(bf16);
+    begin_block(block);  // KvCache::update of this step (the block's slots are overwritten)
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        SPX_CUDA(cudaMemcpyAsync(rs.x[0], x[rs.local], slice_bytes, cudaMemcpyDeviceToDevice,
+                                 rs.stream));
+    }
+    run_step(cfg_.force_start_frame_zero ? 0 : block * F_);
+    const int fin = static_cast<int>(cfg_.layers % 2);
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        SPX_CUDA(cudaMemcpyAsync(y[rs.local], rs.x[fin], slice_bytes, cudaMemcpyDeviceToDevice,
+                                 rs.stream));
     }
 }
 
@@ -964,6 +1032,7 @@ void Engine::generate(uint16_t* out_host) {
 
 void Engine::synchronize() {
     world_->synchronize();
+    check_peer_error();
     harvest_events();
 }
 

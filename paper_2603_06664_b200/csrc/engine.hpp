@@ -112,6 +112,9 @@ class Engine {
     // (steps, L/P, C) bf16, out_dev[local] receives (L/P, C)
     void generate_block_device(int64_t block, const void* const* noise_dev, void* const* out_dev);
     void generate(uint16_t* out_host);
+    // one denoise step of a block (generator.cpp:94-110): x[local] (L/P, C) device bf16 in,
+    // y[local] after every layer; asynchronous on the world's streams
+    void denoise_step(int64_t block, int64_t step, const void* const* x, void* const* y);
     void synchronize();
     void stage_times(double out_ms[6], int64_t* calls);
     void reset_stage_times();
@@ -127,6 +130,7 @@ class Engine {
   private:
     void allocate();
     void run_block(int64_t block, const std::function<void(int64_t)>& load_step);
+    void run_step(int64_t start_frame);
     void build_plans();
     // x_in[local]: the layer input (the K1 source with cfg.adaln; otherwise the QKV plans'
     // A operand already points at it)
@@ -143,6 +147,8 @@ class Engine {
     bf16* ring_k_of(int rank, int64_t layer) const;
     bf16* ring_v_of(int rank, int64_t layer) const;
     void peer_barrier(RankState& rs, int slot);
+    void check_peer_error();
+    void sync_weight_devices();  // throws SPX_ERR_COLLECTIVE after a timed-out PEER barrier
 
     World* world_;
     spx_engine_config cfg_;
@@ -174,6 +180,9 @@ class Engine {
     std::vector<void*> ipc_opened_;
     bool peers_ready_ = false;
     uint64_t epoch_[2] = {0, 0};
+    int* peer_error_host_ = nullptr;  // host-mapped: 1 + the rank a PEER barrier timed out on
+    int* peer_error_dev_ = nullptr;
+    uint64_t peer_timeout_ns_ = 0;
     // profiling
     std::vector<StageEvents> pending_events_;
     std::vector<StageEvents> free_events_;

@@ -99,9 +99,7 @@ struct AttnOperands {
 struct AttnPlan {
     CUtensorMap map_q;
     CUtensorMap map_k;
-    CUtensorMap map_k_pair;  // 64-row boxes: each CTA of a pair loads half of a K tile
     CUtensorMap map_v;
-    CUtensorMap map_v_half;  // 64-row boxes (K/V multicast mode)
     AttnOperands ops;
     int max_splits = 1;
 };
@@ -191,9 +189,11 @@ constexpr int kMaxPeers = 8;
 struct PeerFlags {
     uint64_t* rank_flags[kMaxPeers];  // every rank's flag array (this process's mapping)
 };
-// signal + wait as one PDL-chained 1-warp launch
+// signal + wait as one PDL-chained 1-warp launch. The wait is bounded: after timeout_ns it
+// stores 1 + (the first missing rank) into *error_word (host-mapped) and returns, so a dead or
+// diverged peer surfaces as SPX_ERR_COLLECTIVE instead of a hung stream.
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
-                      uint64_t epoch, cudaStream_t s);
+                      uint64_t epoch, uint64_t timeout_ns, int* error_word, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // Kd: naive fp32 SIMT reference kernels (GPU oracle at shapes the CPU oracle cannot reach).

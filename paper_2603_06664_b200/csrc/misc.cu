@@ -21,7 +21,7 @@ namespace {
 // kernel's tail, griddepcontrol.wait makes that kernel's stores (peer stores included)
 // complete before the release, and the next kernel's prologue overlaps the spin
 __global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, int my_rank, int slot,
-                                    uint64_t epoch) {
+                                    uint64_t epoch, uint64_t timeout_ns, int* error_word) {
     pdl_trigger();
     pdl_wait();
     const int r = threadIdx.x;
@@ -30,12 +30,23 @@ __global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, 
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
     }
     __syncwarp();
-    if (r < world) {
+    // an earlier barrier of this engine already timed out: do not wait again
+    const bool failed = *reinterpret_cast<volatile int*>(error_word) != 0;
+    if (r < world && !failed) {
+        // bounded spin (the reference raises CollectiveError instead of hanging on a rank that
+        // never enters, collectives.cpp:42-52, 88-102): past the deadline the wait gives up,
+        // records the missing rank in the host-visible error word and lets the stream drain;
+        // the host turns the word into SPX_ERR_COLLECTIVE at the next synchronisation
         const uint64_t* src = my_flags + slot * world + r;
+        const uint64_t t0 = globaltimer_ns();
         uint64_t v = 0;
-        for (;;) {
+        for (uint32_t it = 0;; ++it) {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
             if (v >= epoch) break;
+            if ((it & 255u) == 255u && globaltimer_ns() - t0 > timeout_ns) {
+                atomicExch(error_word, 1 + r);
+                break;
+            }
             __nanosleep(64);
         }
     }
@@ -140,8 +151,9 @@ __global__ void naive_attention_kernel(const bf16* __restrict__ q, const bf16* _
 }  // namespace
 
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
-                      uint64_t epoch, cudaStream_t s) {
-    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot, epoch);
+                      uint64_t epoch, uint64_t timeout_ns, int* error_word, cudaStream_t s) {
+    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot, epoch,
+               timeout_ns, error_word);
     count_launch();
 }
 

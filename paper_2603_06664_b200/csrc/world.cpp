@@ -187,6 +187,10 @@ World::~World() {
         if (lr.ev) cudaEventDestroy(lr.ev);
         if (lr.stream) cudaStreamDestroy(lr.stream);
     }
+    if (stage_) {
+        cudaSetDevice(local_[0].device);
+        cudaFree(stage_);
+    }
     if (comm_ && nccl().ok) nccl().comm_destroy(static_cast<ncclComm_t>(comm_));
 }
 
@@ -272,8 +276,33 @@ void World::reset_stats() {
 // ---------------------------------------------------------------------------------------
 // byte-moving collectives
 // ---------------------------------------------------------------------------------------
-void World::all_to_all(void* const* in, void* const* out, const int64_t shape[4],
-                       int elem_bytes, int scatter_axis, int gather_axis, bool fused_member) {
+// Staging for the NCCL byte movers: one device buffer per world, grown (after draining the
+// stream) only when a call needs more than any earlier one; spx_world_reserve sizes it up front
+// so that the collectives allocate nothing on the hot path.
+uint8_t* World::staging(size_t bytes) {
+    if (bytes <= stage_bytes_) return static_cast<uint8_t*>(stage_);
+    const LocalRank& me = local_[0];
+    SPX_CUDA(cudaSetDevice(me.device));
+    SPX_CUDA(cudaStreamSynchronize(me.stream));
+    if (stage_) SPX_CUDA(cudaFree(stage_));
+    stage_ = nullptr;
+    stage_bytes_ = 0;
+    SPX_CUDA(cudaMalloc(&stage_, bytes));
+    stage_bytes_ = bytes;
+    return static_cast<uint8_t*>(stage_);
+}
+
+void World::reserve(size_t bytes) {
+    if (transport_ == SPX_TRANSPORT_NCCL) staging(bytes);
+}
+
+// n tensors of one per-rank shape, all chunk j of every tensor -> rank j (gather offset = the
+// source rank), in ONE round: LOCAL copies straight between the ranks' buffers; NCCL packs
+// [peer][tensor][chunk] into the staging buffer and posts one group of (P-1) sends + (P-1)
+// receives, one message per peer carrying all n tensors' chunks.
+void World::exchange(int n, void* const* const* ins, void* const* const* outs,
+                     const int64_t shape[4], int elem_bytes, int scatter_axis, int gather_axis,
+                     const char* what) {
     require(transport_ != SPX_TRANSPORT_PEER, SPX_ERR_UNSUPPORTED,
             "standalone collectives need the LOCAL or NCCL transport (PEER is engine-only)");
     validate_shape(shape);
@@ -282,20 +311,22 @@ void World::all_to_all(void* const* in, void* const* out, const int64_t shape[4]
     validate_axis(gather_axis);
     const int P = world_size_;
     require(shape[scatter_axis] % P == 0, SPX_ERR_PARTITION,
-            "all_to_all scatter extent " + std::to_string(shape[scatter_axis]) +
+            std::string(what) + " scatter extent " + std::to_string(shape[scatter_axis]) +
                 " not divisible by world size " + std::to_string(P));
     int64_t piece[4] = {shape[0], shape[1], shape[2], shape[3]};
     piece[scatter_axis] = shape[scatter_axis] / P;
     int64_t oshape[4] = {piece[0], piece[1], piece[2], piece[3]};
     oshape[gather_axis] *= P;
-    int64_t in_str[4], out_str[4];
+    int64_t in_str[4], out_str[4], piece_str[4];
     strides_of(shape, in_str);
     strides_of(oshape, out_str);
-    Box4 box{};
+    strides_of(piece, piece_str);
+    Box4 box{}, pack{}, unpack{};
     for (int a = 0; a < 4; ++a) {
-        box.ext[a] = piece[a];
-        box.src_str[a] = in_str[a];
-        box.dst_str[a] = out_str[a];
+        box.ext[a] = pack.ext[a] = unpack.ext[a] = piece[a];
+        box.src_str[a] = pack.src_str[a] = in_str[a];
+        box.dst_str[a] = unpack.dst_str[a] = out_str[a];
+        pack.dst_str[a] = unpack.src_str[a] = piece_str[a];
     }
     const size_t eb = static_cast<size_t>(elem_bytes);
     // chunk j of rank i -> rank j, placed at gather offset i
@@ -306,77 +337,63 @@ void World::all_to_all(void* const* in, void* const* out, const int64_t shape[4]
         join_all();
         for (int j = 0; j < P; ++j) {
             SPX_CUDA(cudaSetDevice(local_[j].device));
-            for (int i = 0; i < P; ++i) {
-                copy_box_run(static_cast<uint8_t*>(out[j]) + dst_off(i),
-                             static_cast<const uint8_t*>(in[i]) + src_off(j), box, elem_bytes,
-                             local_[j].stream);
-            }
+            for (int t = 0; t < n; ++t)
+                for (int i = 0; i < P; ++i)
+                    copy_box_run(static_cast<uint8_t*>(outs[t][j]) + dst_off(i),
+                                 static_cast<const uint8_t*>(ins[t][i]) + src_off(j), box,
+                                 elem_bytes, local_[j].stream);
         }
         join_all();
-    } else {
-        const LocalRank& me = local_[0];
-        const int r = me.rank;
-        SPX_CUDA(cudaSetDevice(me.device));
-        const int64_t pn = numel(piece);
-        const size_t pbytes = static_cast<size_t>(pn) * eb;
-        uint8_t* tmp = nullptr;
-        SPX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 2 * P * pbytes, me.stream));
-        uint8_t* sendb = tmp;
-        uint8_t* recvb = tmp + P * pbytes;
-        int64_t piece_str[4];
-        strides_of(piece, piece_str);
-        Box4 pack{}, unpack{};
-        for (int a = 0; a < 4; ++a) {
-            pack.ext[a] = unpack.ext[a] = piece[a];
-            pack.src_str[a] = in_str[a];
-            pack.dst_str[a] = piece_str[a];
-            unpack.src_str[a] = piece_str[a];
-            unpack.dst_str[a] = out_str[a];
-        }
+        return;
+    }
+    const LocalRank& me = local_[0];
+    const int r = me.rank;
+    SPX_CUDA(cudaSetDevice(me.device));
+    const size_t pbytes = static_cast<size_t>(numel(piece)) * eb;  // one chunk of one tensor
+    const size_t msg = static_cast<size_t>(n) * pbytes;             // everything for one peer
+    uint8_t* sendb = staging(2 * static_cast<size_t>(P) * msg);
+    uint8_t* recvb = sendb + static_cast<size_t>(P) * msg;
+    for (int t = 0; t < n; ++t) {
         for (int j = 0; j < P; ++j) {
-            if (j == r) {
-                copy_box_run(static_cast<uint8_t*>(out[0]) + dst_off(r),
-                             static_cast<const uint8_t*>(in[0]) + src_off(r), box, elem_bytes,
+            const uint8_t* src = static_cast<const uint8_t*>(ins[t][0]) + src_off(j);
+            if (j == r)
+                copy_box_run(static_cast<uint8_t*>(outs[t][0]) + dst_off(r), src, box, elem_bytes,
                              me.stream);
-            } else {
-                copy_box_run(sendb + j * pbytes, static_cast<const uint8_t*>(in[0]) + src_off(j),
-                             pack, elem_bytes, me.stream);
-            }
+            else
+                copy_box_run(sendb + j * msg + t * pbytes, src, pack, elem_bytes, me.stream);
         }
-        group_start();
-        for (int j = 0; j < P; ++j) {
-            if (j == r) continue;
-            send(sendb + j * pbytes, pbytes, j, me.stream);
-            recv(recvb + j * pbytes, pbytes, j, me.stream);
-        }
-        group_end();
+    }
+    group_start();
+    for (int j = 0; j < P; ++j) {
+        if (j == r) continue;
+        send(sendb + j * msg, msg, j, me.stream);
+        recv(recvb + j * msg, msg, j, me.stream);
+    }
+    group_end();
+    for (int t = 0; t < n; ++t)
         for (int i = 0; i < P; ++i) {
             if (i == r) continue;
-            copy_box_run(static_cast<uint8_t*>(out[0]) + dst_off(i), recvb + i * pbytes, unpack,
-                         elem_bytes, me.stream);
+            copy_box_run(static_cast<uint8_t*>(outs[t][0]) + dst_off(i), recvb + i * msg + t * pbytes,
+                         unpack, elem_bytes, me.stream);
         }
-        SPX_CUDA(cudaFreeAsync(tmp, me.stream));
-    }
-    const int64_t cross = static_cast<int64_t>(P) * (P - 1) * numel(piece);
-    if (!fused_member) add_stats(0, 1, 0, cross, 1);
+}
+
+void World::all_to_all(void* const* in, void* const* out, const int64_t shape[4],
+                       int elem_bytes, int scatter_axis, int gather_axis) {
+    void* const* ins[1] = {in};
+    void* const* outs[1] = {out};
+    exchange(1, ins, outs, shape, elem_bytes, scatter_axis, gather_axis, "all_to_all");
+    const int P = world_size_;
+    add_stats(0, 1, 0, static_cast<int64_t>(P - 1) * numel(shape), 1);
 }
 
 void World::fused_all_to_all(void* const* const ins[3], void* const* const outs[3],
                              const int64_t shape[4], int elem_bytes, int scatter_axis,
                              int gather_axis) {
-    validate_shape(shape);
-    validate_axis(scatter_axis);
-    require(shape[scatter_axis] % world_size_ == 0, SPX_ERR_PARTITION,
-            "fused_all_to_all scatter extent " + std::to_string(shape[scatter_axis]) +
-                " not divisible by world size " + std::to_string(world_size_));
-    // one invocation, one round: the three tensors ride the same exchange
-    int64_t cross = 0;
-    for (int t = 0; t < 3; ++t) {
-        all_to_all(ins[t], outs[t], shape, elem_bytes, scatter_axis, gather_axis, true);
-        cross += static_cast<int64_t>(world_size_) * (world_size_ - 1) * numel(shape) /
-                 world_size_;
-    }
-    add_stats(0, 0, 1, cross, 1);
+    // one invocation, one round: the three tensors ride the same exchange (one NCCL group)
+    exchange(3, ins, outs, shape, elem_bytes, scatter_axis, gather_axis, "fused_all_to_all");
+    const int P = world_size_;
+    add_stats(0, 0, 1, 3 * static_cast<int64_t>(P - 1) * numel(shape), 1);
 }
 
 void World::all_gather(void* const* in, void* const* out, const int64_t shape[4],
@@ -413,8 +430,7 @@ void World::all_gather(void* const* in, void* const* out, const int64_t shape[4]
         const LocalRank& me = local_[0];
         SPX_CUDA(cudaSetDevice(me.device));
         const size_t bytes = static_cast<size_t>(numel(shape)) * eb;
-        uint8_t* recvb = nullptr;
-        SPX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&recvb), P * bytes, me.stream));
+        uint8_t* recvb = staging(static_cast<size_t>(P) * bytes);
         group_start();
         for (int j = 0; j < P; ++j) {
             if (j == me.rank) continue;
@@ -429,7 +445,6 @@ void World::all_gather(void* const* in, void* const* out, const int64_t shape[4]
             copy_box_run(static_cast<uint8_t*>(out[0]) + dst_off(i), src, box, elem_bytes,
                          me.stream);
         }
-        SPX_CUDA(cudaFreeAsync(recvb, me.stream));
     }
     add_stats(1, 0, 0, static_cast<int64_t>(P) * (P - 1) * numel(shape), 1);
 }

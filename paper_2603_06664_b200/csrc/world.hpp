@@ -67,14 +67,22 @@ class World {
 
     // byte-moving collectives on (B, S, H, D) tensors of any element width
     void all_to_all(void* const* in, void* const* out, const int64_t shape[4], int elem_bytes,
-                    int scatter_axis, int gather_axis, bool fused_member);
+                    int scatter_axis, int gather_axis);
     void fused_all_to_all(void* const* const ins[3], void* const* const outs[3],
                           const int64_t shape[4], int elem_bytes, int scatter_axis,
                           int gather_axis);
     void all_gather(void* const* in, void* const* out, const int64_t shape[4], int elem_bytes,
                     int axis);
 
+    // pre-size the NCCL staging buffer (bytes) so that no collective allocates
+    void reserve(size_t bytes);
+
   private:
+    void exchange(int n, void* const* const* ins, void* const* const* outs, const int64_t shape[4],
+                  int elem_bytes, int scatter_axis, int gather_axis, const char* what);
+    uint8_t* staging(size_t bytes);
+    void* stage_ = nullptr;
+    size_t stage_bytes_ = 0;
     int world_size_ = 1;
     int transport_ = SPX_TRANSPORT_LOCAL;
     std::vector<LocalRank> local_;

@@ -572,9 +572,25 @@ class Engine:
         nz = None
         if noise_bits is not None:
             nz = np.ascontiguousarray(noise_bits, dtype=np.uint16)
+            want = self.cfg.denoise_steps * self.cfg.block_len() * self.cfg.heads * self.cfg.head_dim
+            if nz.size != want:
+                raise ShapeError(f"noise_bits holds {nz.size} values, expected denoise_steps x L x H x D"
+                                 f" = {want} (the full block at every step)")
         check(lib().spx_engine_generate_block(self._h, block, nz.ctypes.data if nz is not None else None,
                                               out.ctypes.data))
         return out
+
+    def denoise_step(self, block, step, x_locals):
+        """one denoise step of `block` (generator.cpp:94-110) on every local rank: x_locals are
+        (L/P, H, D) bf16 CUDA tensors (noise), returns the last layer's outputs."""
+        torch = _torch()
+        ys = [torch.empty_like(x) for x in x_locals]
+        torch.cuda.synchronize()
+        check(lib().spx_engine_denoise_step(self._h, block, step,
+                                            ptr_array([_bf16(x).data_ptr() for x in x_locals]),
+                                            ptr_array([y.data_ptr() for y in ys])))
+        check(lib().spx_engine_synchronize(self._h))
+        return ys
 
     def generate(self) -> np.ndarray:
         rows = self.local_len * self.local_ranks
@@ -595,6 +611,43 @@ class Engine:
         s = _lib.CommStats()
         check(lib().spx_engine_stats(self._h, ctypes.byref(s)))
         return s.as_dict()
+
+
+@dataclass
+class BlockCheck:
+    block: int
+    max_abs_dev: float
+    passed: bool
+
+
+@dataclass
+class VerificationReport:
+    """VerificationReport (proj/include/spattn/generator.hpp:66-80)."""
+
+    config: "GenerationConfig"
+    tolerance: float
+    blocks: list
+    ledger: dict
+    passed: bool
+
+
+def verify_stream(cfg: "GenerationConfig", tolerance: float = 1e-10,
+                  devices: Optional[Sequence[int]] = None) -> VerificationReport:
+    """verify_stream(cfg, tol) (generator.cpp:149-177) on the device: cfg's schedule at
+    cfg.world_size ranks (a LOCAL world; devices may repeat) against the P = 1 optimized path
+    (the reference pipeline at P = 1, true start frames) on the same seeded weights and noise;
+    per-block max |deviation| of the bf16 outputs. The reference's 1e-10 default is met exactly
+    by the schedules that keep the P = 1 arithmetic (every partition: bit-identical outputs)."""
+    c = cfg.to_c()
+    n = cfg.num_blocks
+    blocks = (_lib.VerifyBlock * n)()
+    ok = ctypes.c_int32()
+    st = _lib.CommStats()
+    devs = None if devices is None else (ctypes.c_int * len(devices))(*devices)
+    check(lib().spx_verify_stream(ctypes.byref(c), cfg.world_size, devs, tolerance, blocks, n,
+                                  ctypes.byref(ok), ctypes.byref(st)))
+    checks = [BlockCheck(int(b.block), float(b.max_abs_dev), bool(b.pass_)) for b in blocks]
+    return VerificationReport(cfg, tolerance, checks, st.as_dict(), bool(ok.value))
 
 
 def tensor_checksum(x: np.ndarray) -> str:

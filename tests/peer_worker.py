@@ -4,7 +4,9 @@ Causal-RoPE SP schedule runs with device-side flag barriers. Several ranks may s
 GPU (the driver time-slices their contexts), which is how the multi-process path is tested
 on a single B200.
 
-usage: python tests/peer_worker.py RANK WORLD PORT OUT_DIR [window_frames|-1] [wan]
+usage: python tests/peer_worker.py RANK WORLD PORT OUT_DIR [window_frames|-1] [wan|stall]
+  stall: ranks > 0 map the buffers and then never enter the layer calls; rank 0 must get a
+         CollectiveError from the bounded PEER barrier (SPX_PEER_TIMEOUT_MS) instead of hanging
 """
 import math
 import os
@@ -49,6 +51,7 @@ def main():
     rank, world_size, port, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4]
     window = int(sys.argv[5]) if len(sys.argv) > 5 and int(sys.argv[5]) > 0 else None
     wan = len(sys.argv) > 6 and sys.argv[6] == "wan"
+    stall = len(sys.argv) > 6 and sys.argv[6] == "stall"
     import torch
     import torch.distributed as dist
 
@@ -60,6 +63,19 @@ def main():
     world = s.CommWorld.peer(rank, world_size, 0)
     eng = make_engine(s, world_size, world, window, wan)
     eng.connect_peers(dist.all_gather_object)
+    if stall:
+        if rank == 0:
+            try:
+                eng.generate()
+                outcome = "no error"
+            except s.CollectiveError as e:
+                outcome = "CollectiveError: " + str(e)
+            with open(os.path.join(out, "stall.txt"), "w") as f:
+                f.write(outcome)
+        dist.barrier()
+        del eng
+        dist.destroy_process_group()
+        return
     got = eng.generate()  # (blocks, L/P rows of this rank, H, D) bf16 bits
     np.save(os.path.join(out, f"rank{rank}.npy"), got)
     stats = eng.stats()

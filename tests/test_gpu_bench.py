@@ -55,3 +55,15 @@ def test_bench_reference_arm_line():
         pytest.skip(d["unavailable"])
     assert d["unit"] == "latent frames/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_two_ranks_spawns_itself():
+    """--gpus 2 without torchrun: bench.py launches its two ranks itself (PEER transport; both
+    on cuda:0 here, a path check) and rank 0 prints the whole-job line with the exchange."""
+    d = _run("--gpus", "2", "--same-device", "--no-cpu-baseline")
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "sp2"
+    assert d["config"]["same_device"] is True
+    ex = d["exchange"]
+    # Ulysses at P = 2: q, k, v, o -- each rank sends half of each (L/2, C) slab to its peer
+    assert ex["bytes_per_call_per_rank"] == 4 * (4680 // 2) * 1536 * 2 // 2
+    assert d["value"] > 0 and d["e2e"]["value"] > 0

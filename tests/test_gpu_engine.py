@@ -530,3 +530,55 @@ def test_reset_cache_replays_a_video(cuda):
     eng.reset_cache()
     again = eng.generate()
     assert np.array_equal(first, again)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_verify_stream_product_api(cuda, world):
+    """spx_verify_stream / spattn.verify_stream (generator.cpp:149-177): the SP schedule at P
+    ranks against the P = 1 path on the same seeded inputs; every partition keeps the P = 1
+    arithmetic, so the reference's 1e-10 tolerance holds with deviation 0, and the ledger is
+    the variant run's."""
+    s = spattn()
+    rep = s.verify_stream(cfg_from(TINY, world=world), tolerance=1e-10)
+    assert rep.passed and len(rep.blocks) == TINY["num_blocks"]
+    assert all(b.max_abs_dev == 0.0 and b.passed for b in rep.blocks)
+    calls = TINY["num_blocks"] * 2 * TINY["layers"]
+    assert rep.ledger["fused_all_to_all"] == calls and rep.ledger["rounds"] == 2 * calls
+
+
+def test_verify_stream_catches_the_start_frame_fault(cuda):
+    """force_start_frame_zero (test_generator.cpp:115-124): block 0 coincides with the correct
+    run, every later block deviates and fails the check."""
+    s = spattn()
+    rep = s.verify_stream(cfg_from(TINY, world=2, force_start_frame_zero=True), tolerance=1e-10)
+    assert not rep.passed
+    assert rep.blocks[0].passed and rep.blocks[0].max_abs_dev == 0.0
+    assert all(not b.passed and b.max_abs_dev > 0 for b in rep.blocks[1:])
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_denoise_step_api_matches_generate_block(cuda, world):
+    """spx_engine_denoise_step: the per-step body of generate (generator.cpp:94-110) on caller
+    buffers; the block's steps in order reproduce generate_block's output bit for bit."""
+    import torch
+
+    s = spattn()
+    kw = dict(TINY, num_blocks=2)
+    cfg = cfg_from(kw, steps=3, world=world)
+    L, C = 192, kw["heads"] * kw["head_dim"]
+    rng = np.random.default_rng(6)
+    noise = [oracle.to_bf16_bits(oracle.round_bf16(rng.standard_normal((3, L, C)) * 0.1))
+             for _ in range(2)]
+    a = s.Engine(cfg)
+    want = [a.generate_block(b, noise[b]) for b in range(2)]
+    e = s.Engine(cfg)
+    rows = L // world
+    for b in range(2):
+        for st in range(3):
+            xs = [torch.from_numpy(noise[b][st, r * rows:(r + 1) * rows].view(np.int16).copy()).to(cuda)
+                  .view(torch.bfloat16) for r in range(world)]
+            ys = e.denoise_step(b, st, xs)
+        got = np.concatenate([y.view(torch.int16).cpu().numpy().view(np.uint16) for y in ys])
+        assert np.array_equal(got.reshape(want[b].shape), want[b]), b
+    with pytest.raises(s.RangeError):
+        e.denoise_step(0, 3, xs)

@@ -42,7 +42,7 @@ def rel_l2(a, b):
 
 @pytest.mark.parametrize("M,K,N", [(192, 256, 768), (300, 256, 256), (4680, 1536, 4608),
                                    (585, 1536, 1536), (1170, 1536, 4608)])
-def test_project_tokens_matches_fp32(cuda, M, K, N):
+def test_project_tokens_matches_fp32(cuda, M, K, N, parity_log):
     torch = _t()
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
@@ -51,8 +51,10 @@ def test_project_tokens_matches_fp32(cuda, M, K, N):
     _check(_lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(), M, K, N, _stream()))
     torch.cuda.synchronize()
     ref = x.float() @ w.float().t()
-    # bf16 output rounding: |err| <= 2^-8 |y|
-    assert rel_l2(y.float(), ref) < 4e-3
+    # bf16 output rounding: |err| <= 2^-8 |y|; rel-L2 bar 3e-3
+    e = rel_l2(y.float(), ref)
+    parity_log(rel_l2=e, max_abs_over_max=float((y.float() - ref).abs().max() / ref.abs().max()), bar=3e-3)
+    assert e < 3e-3
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
@@ -75,13 +77,13 @@ def test_project_tokens_every_tile_variant(cuda, variant, M, K, N):
         _check(_lib().spx_debug_set_gemm_variant(-1))
     ref = x.float() @ w.float().t()
     assert bool(torch.isfinite(y.float()).all())
-    assert rel_l2(y.float(), ref) < 4e-3
+    assert rel_l2(y.float(), ref) < 3e-3
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
 @pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),
                                         (4680, 4680, 12, 128), (1170, 9360, 3, 128)])
-def test_attention_matches_fp32(cuda, sq, skv, H, D):
+def test_attention_matches_fp32(cuda, sq, skv, H, D, parity_log):
     torch = _t()
     g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
     # O(1) logits (well-conditioned softmax), as in the tolerance tier of SURVEY 8c
@@ -95,7 +97,9 @@ def test_attention_matches_fp32(cuda, sq, skv, H, D):
     qf, kf, vf = (t.float().transpose(1, 2) for t in (q, k, v))
     ref = torch.softmax(qf @ kf.transpose(-1, -2) / math.sqrt(D), dim=-1) @ vf
     ref = ref.transpose(1, 2)
-    assert rel_l2(o.float(), ref) < 1e-2
+    e = rel_l2(o.float(), ref)
+    parity_log(rel_l2=e, bar=5e-3)
+    assert e < 5e-3  # SURVEY 8c K6 bar (bf16 P, fp32 O / l, one bf16 output rounding)
 
 
 def test_attention_matches_simt_kernel(cuda):
@@ -112,7 +116,7 @@ def test_attention_matches_simt_kernel(cuda):
     _check(_lib().spx_debug_naive_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), ref.data_ptr(),
                                             1, sq, skv, H, D, _stream()))
     torch.cuda.synchronize()
-    assert rel_l2(o.float(), ref) < 1e-2
+    assert rel_l2(o.float(), ref) < 5e-3
 
 
 @pytest.mark.parametrize("grid,P,start", [((3, 30, 52), 8, 18), ((3, 8, 8), 2, 3), ((3, 4, 4), 4, 0)])
@@ -138,7 +142,7 @@ def test_rope_positions_bit_exact(cuda, grid, P, start):
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 5, 8])
 @pytest.mark.parametrize("sq,skv,H", [(2340, 4680, 3), (300, 2000, 2)])
-def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H):
+def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H, parity_log):
     """split-KV: fp32 partials staged in smem, bulk-copied out, bulk-loaded back and merged
     lse-weighted by the last CTA of each query tile; every split count (including counts the
     merge has to batch: 8 > 2 partials per batch at D = 128) against fp32 softmax attention."""
@@ -159,7 +163,9 @@ def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H):
         _check(_lib().spx_debug_set_attn_splits(0))
     qf, kf, vf = (t.float()[0].transpose(0, 1) for t in (q, k, v))
     ref = torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf
-    assert rel_l2(o.float()[0].transpose(0, 1), ref) < 1e-2
+    e = rel_l2(o.float()[0].transpose(0, 1), ref)
+    parity_log(rel_l2=e, bar=5e-3)
+    assert e < 5e-3
 
 
 @pytest.mark.parametrize("skv", [640, 4680])
@@ -183,80 +189,4 @@ def test_attention_offset_guard_on_growing_logits(cuda, skv):
     ref = torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf
     got = o.float()[0].transpose(0, 1)
     assert bool(torch.isfinite(got).all())
-    assert rel_l2(got, ref) < 1e-2
-
-
-_PERSIST_CHILD = r"""
-import sys, torch
-from paper_2603_06664_b200._lib import check, lib
-q, k, v = torch.load(sys.argv[1])
-q, k, v = q.cuda(), k.cuda(), v.cuda()
-o = torch.empty_like(q)
-_, sq, H, D = q.shape
-check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq,
-                          k.shape[1], H, D, torch.cuda.current_stream().cuda_stream))
-torch.cuda.synchronize()
-torch.save(o.cpu(), sys.argv[2])
-"""
-
-
-@pytest.mark.parametrize("sq,skv,H,D", [(4680, 4680, 12, 128), (2560, 1000, 16, 64)])
-def test_attention_persistent_opt_in_bit_identical(cuda, tmp_path, sq, skv, H, D):
-    """the opt-in persistent form (SPX_ATTN_PERSIST=1: CTAs walk several (query tile, head)
-    units, the next unit's Q load and first S tiles overlap this unit's epilogue) runs the
-    same per-unit arithmetic as the one-CTA-per-unit grid: outputs are bit-identical"""
-    import os
-    import subprocess
-    import sys
-
-    torch = _t()
-    g = torch.Generator(device="cuda").manual_seed(sq + H)
-    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    o = torch.empty_like(q)
-    _check(_lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, sq, skv,
-                                H, D, _stream()))
-    torch.cuda.synchronize()
-    torch.save((q.cpu(), k.cpu(), v.cpu()), tmp_path / "in.pt")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SPX_ATTN_PERSIST="1", SPX_ATTN_VERBOSE="1",
-               PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
-    r = subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(tmp_path / "in.pt"),
-                        str(tmp_path / "out.pt")], env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
-    if D == 128:  # the layout line (D = 128 path): every unit unsplit, i.e. the persistent form ran
-        assert "n_full=%d" % (((sq + 127) // 128) * H) in r.stderr
-    o_p = torch.load(tmp_path / "out.pt")
-    assert torch.equal(o_p, o.cpu())
-
-
-@pytest.mark.parametrize("kernel", ["pair", "mcast"])
-@pytest.mark.parametrize("sq,skv,H", [(512, 1000, 2), (300, 4680, 3)])
-def test_attention_opt_in_cluster_modes(cuda, tmp_path, kernel, sq, skv, H):
-    """the opt-in cluster variants (SPX_ATTN_KERNEL=pair: CTA-pair MMAs; mcast: K/V multicast
-    across a CTA pair; measured slower, kept for the record) against fp32 attention, incl. a
-    ragged query tile count (padding CTA of the pair) and kv tail"""
-    import os
-    import subprocess
-    import sys
-
-    torch = _t()
-    D = 128
-    g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
-    q = torch.randn(1, sq, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    k = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    v = torch.randn(1, skv, H, D, device=cuda, generator=g).to(torch.bfloat16)
-    torch.save((q.cpu(), k.cpu(), v.cpu()), tmp_path / "in.pt")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SPX_ATTN_KERNEL=kernel,
-               PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
-    r = subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(tmp_path / "in.pt"),
-                        str(tmp_path / "out.pt")], env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
-    o = torch.load(tmp_path / "out.pt").cuda()
-    qf, kf, vf = (t.float().transpose(1, 2) for t in (q, k, v))
-    ref = (torch.softmax(qf @ kf.transpose(-1, -2) / math.sqrt(D), dim=-1) @ vf).transpose(1, 2)
-    assert rel_l2(o.float(), ref) < 1e-2
+    assert rel_l2(got, ref) < 5e-3

@@ -23,12 +23,14 @@ def _free_port():
         return so.getsockname()[1]
 
 
-def _run_ranks(world, tmp_path, window=None, wan=False):
+def _run_ranks(world, tmp_path, window=None, wan=False, mode=None, env=None):
     port = _free_port()
-    args = [str(window if window is not None else -1)] + (["wan"] if wan else [])
+    args = [str(window if window is not None else -1)] + (["wan"] if wan else []) + \
+        ([mode] if mode else [])
     procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "peer_worker.py"), str(r),
                                str(world), str(port), str(tmp_path)] + args,
-                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                              env=dict(os.environ, **(env or {})))
              for r in range(world)]
     logs = []
     for p in procs:
@@ -41,6 +43,8 @@ def _run_ranks(world, tmp_path, window=None, wan=False):
         logs.append(out.decode(errors="replace")[-3000:])
     for r, p in enumerate(procs):
         assert p.returncode == 0, f"rank {r} failed:\n{logs[r]}"
+    if mode == "stall":
+        return (tmp_path / "stall.txt").read_text()
     return [np.load(tmp_path / f"rank{r}.npy") for r in range(world)], \
         [np.load(tmp_path / f"stats{r}.npy") for r in range(world)]
 
@@ -72,3 +76,12 @@ def test_peer_transport_wan_mode_bit_identical_to_p1(cuda, tmp_path):
     got = np.concatenate(slices, axis=1)
     base = peer_worker.make_engine(s, 1, s.CommWorld(1), None, wan=True).generate()
     assert np.array_equal(got, base)
+
+
+def test_peer_barrier_times_out_with_collective_error(cuda, tmp_path):
+    """A rank that never enters the layer calls: the other rank's device barrier gives up after
+    SPX_PEER_TIMEOUT_MS and the engine raises CollectiveError (the reference's behaviour for a
+    rank that leaves the collective order, collectives.cpp:42-52, 88-102) instead of hanging."""
+    outcome = _run_ranks(2, tmp_path, mode="stall", env={"SPX_PEER_TIMEOUT_MS": "1500"})
+    assert outcome.startswith("CollectiveError"), outcome
+    assert "rank 1" in outcome
