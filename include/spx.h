@@ -317,6 +317,20 @@ spx_status spx_engine_generate_block(spx_engine* engine, int64_t block, const ui
  * out_dev[local rank] receives (L/P, H, D); asynchronous on the world's streams */
 spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
                                             const void* const* noise_dev, void* const* out_dev);
+/* streaming generator: n blocks back to back (blocks[i] may repeat -- a block denoised again
+ * overwrites its own KV slots); noise_host[i]: bf16 (steps, L, H, D) of the FULL block i,
+ * out_host[i]: bf16 rows of the local ranks (rank order). The upload of the next step's noise
+ * and the download of the previous block's latent run on their own streams, overlapped with
+ * the compute; returns when every latent is on the host. Host buffers must be pinned. */
+spx_status spx_engine_generate_stream(spx_engine* engine, const int64_t* blocks, int64_t n,
+                                      const uint16_t* const* noise_host, uint16_t* const* out_host);
+/* per-step CUDA graphs (default on): the layer calls of a denoise step are captured once per
+ * KV-ring state and replayed (one launch per step instead of 3 x layers), on a world with one
+ * local rank (PEER, or LOCAL P = 1), the optimized schedule and profiling off; off = every
+ * kernel enqueued by the host (SPX_GRAPHS=0 at load time does the same) */
+spx_status spx_engine_set_graphs(spx_engine* engine, int32_t on);
+/* number of per-step graphs the engine holds (tests) */
+spx_status spx_debug_engine_graphs(const spx_engine* engine, int64_t* count);
 /* one denoise step of a block (the per-step body of generate, generator.cpp:94-110):
  * KvCache::update of the block, then every layer on x_local[local rank] (device bf16
  * (L/P, H, D)) into y_local[local rank]; asynchronous on the world's streams */

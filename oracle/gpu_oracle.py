@@ -12,11 +12,19 @@ on the CPU reference):
   generate                   proj/src/generator.cpp:50-147       (steps do not chain)
 
 plus the Wan-mode extensions the CPU oracle (oracle/spattn_oracle.cpp) restates: QK-RMSNorm
-and the adaLN modulation + gated residual. Everything is float64; the RoPE tables, seeded
-weights and noise come from the CPU oracle (liboracle: the reference's own RNG and std::pow /
-cos / sin), so only the summation order of the matmuls differs from the CPU oracle. It is
-pinned to the CPU oracle at the shapes that one finishes (tests/test_gpu_wan_parity.py:
-relative difference <= 1e-12).
+and the adaLN modulation + gated residual.
+
+storage="bf16" is an error MODEL, not a second oracle: the same float64 arithmetic, but every
+tensor the device path stores between kernels (the layer input x, q / k after RoPE, v, the
+attention output o, the projection output y) is rounded to bf16 there. Its distance to the
+float64 result is the error budget that bf16 storage alone implies at a given depth -- the
+yardstick for the deep-stack tolerance (a 30-layer chain re-rounds 5 tensors per layer; the
+rounding errors random-walk through the stack).
+
+Everything else is float64; the RoPE tables, seeded weights and noise come from the CPU oracle
+(liboracle: the reference's own RNG and std::pow / cos / sin), so only the summation order of
+the matmuls differs from the CPU oracle. It is pinned to the CPU oracle at the shapes that one
+finishes (tests/test_oracle_pin.py: relative difference <= 1e-12).
 """
 from __future__ import annotations
 
@@ -155,7 +163,7 @@ class ReferenceModel:
     def __init__(self, frames, grid_h, grid_w, heads, head_dim, layers, num_blocks, steps,
                  window=None, seed=0, base=10000.0, split=None, weights=None, round_inputs=True,
                  qk_norm=False, norm_weights=None, modulation=None, norm_eps=1e-6,
-                 force_start_frame_zero=False, device="cuda"):
+                 force_start_frame_zero=False, device="cuda", storage="fp64"):
         torch = _torch()
         self.grid = (frames, grid_h, grid_w)
         self.H, self.D = heads, head_dim
@@ -166,6 +174,8 @@ class ReferenceModel:
         self.round_inputs = round_inputs
         self.device = device
         self.force0 = force_start_frame_zero
+        assert storage in ("fp64", "bf16")
+        self.storage = storage
         self.table = RopeRows(self.grid, num_blocks * frames, head_dim, base, split, device)
         W = []
         for l in range(layers):
@@ -194,14 +204,22 @@ class ReferenceModel:
             x = oracle.round_bf16(x)
         return _torch().from_numpy(x.reshape(self.L, self.C)).to(self.device)
 
+    def _st(self, t):
+        """a tensor stored between kernels: bf16 under storage="bf16" (the error model)"""
+        if self.storage == "bf16":
+            torch = _torch()
+            return t.to(torch.bfloat16).to(torch.float64)
+        return t
+
     def layer(self, l, block, start, x):
         """reference_self_attention (sp_attention.cpp:317-348) on x (L, C) float64."""
         W = self.W[l]
         L, H, D = self.L, self.H, self.D
+        x = self._st(x)
         xin = x
         if self.mod is not None:
             m = self.mod[l]
-            xin = layernorm_modulate(x, m[0], m[1], self.norm_eps)
+            xin = self._st(layernorm_modulate(x, m[0], m[1], self.norm_eps))
         q, k, v = (xin @ W[m].t() for m in range(3))
         if self.qk_norm:
             nq = self.norm_w[l, 0] if self.norm_w is not None else None
@@ -209,16 +227,17 @@ class ReferenceModel:
             q = rms_norm(q, nq, self.norm_eps)
             k = rms_norm(k, nk, self.norm_eps)
         cos, sin = self.table.rows(start)
-        q = rope(q.reshape(L, H, D), cos, sin)
-        k = rope(k.reshape(L, H, D), cos, sin)
+        q = self._st(rope(q.reshape(L, H, D), cos, sin))
+        k = self._st(rope(k.reshape(L, H, D), cos, sin))
+        v = self._st(v)
         cache = self.caches[l]
         cache.update(block, k, v.reshape(L, H, D))
         kk, vv = cache.read()
-        o = sdpa(q, kk, vv).reshape(L, self.C)
+        o = self._st(sdpa(q, kk, vv).reshape(L, self.C))
         y = o @ W[3].t()
         if self.mod is not None:
-            return x + self.mod[l, 2][None, :] * y
-        return y
+            return self._st(x + self.mod[l, 2][None, :] * y)
+        return self._st(y)
 
     def block(self, b, noise=None):
         """one block: steps x layers calls (generator.cpp:89-115); noise: optional

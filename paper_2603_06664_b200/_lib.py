@@ -167,6 +167,10 @@ _SIGS = [
     ("spx_engine_generate_block", c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     ("spx_engine_generate_block_device", c_int, [c_void_p, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
     ("spx_engine_generate", c_int, [c_void_p, c_void_p]),
+    ("spx_engine_generate_stream", c_int, [c_void_p, POINTER(c_int64), c_int64, POINTER(c_void_p),
+                                           POINTER(c_void_p)]),
+    ("spx_engine_set_graphs", c_int, [c_void_p, c_int32]),
+    ("spx_debug_engine_graphs", c_int, [c_void_p, POINTER(c_int64)]),
     ("spx_engine_denoise_step", c_int, [c_void_p, c_int64, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
     ("spx_verify_stream", c_int, [POINTER(EngineConfig), c_int32, POINTER(c_int), c_double,
                                   POINTER(VerifyBlock), c_int64, POINTER(c_int32), POINTER(CommStats)]),

@@ -794,6 +794,28 @@ spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
     });
 }
 
+spx_status spx_engine_generate_stream(spx_engine* engine, const int64_t* blocks, int64_t n,
+                                     const uint16_t* const* noise_host, uint16_t* const* out_host) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->generate_stream(blocks, n, noise_host, out_host);
+    });
+}
+
+spx_status spx_engine_set_graphs(spx_engine* engine, int32_t on) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->set_graphs(on != 0);
+    });
+}
+
+spx_status spx_debug_engine_graphs(const spx_engine* engine, int64_t* count) {
+    return guarded([&] {
+        require(engine && count, SPX_ERR_CONFIG, "null argument");
+        *count = engine->e->graph_count();
+    });
+}
+
 spx_status spx_engine_denoise_step(spx_engine* engine, int64_t block, int64_t step,
                                    const void* const* x_local, void* const* y_local) {
     return guarded([&] {

@@ -35,12 +35,16 @@ unsigned long long* g_spans = nullptr;  // [slots][2]
 int64_t g_span_next = 0;
 }  // namespace
 
-unsigned long long* span_slot() {
+bool span_tracing() {
     static const bool on = [] {
         const char* e = std::getenv("SPX_SPAN_TRACE");
         return e && std::atoi(e) == 1;
     }();
-    if (!on) return nullptr;
+    return on;
+}
+
+unsigned long long* span_slot() {
+    if (!span_tracing()) return nullptr;
     if (!g_spans) {
         SPX_CUDA(cudaMalloc(&g_spans, kSpanSlots * 2 * sizeof(unsigned long long)));
         std::vector<unsigned long long> init(kSpanSlots * 2);

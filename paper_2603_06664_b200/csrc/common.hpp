@@ -74,6 +74,7 @@ bool pdl_enabled();
 // Kernel span tracing (SPX_SPAN_TRACE=1, profiling only): each traced launch gets a slot
 // {earliest CTA start, latest CTA end} in globaltimer ns; nullptr when tracing is off.
 unsigned long long* span_slot();
+bool span_tracing();
 int64_t span_count();
 void span_dump(uint64_t* out, int64_t n);
 

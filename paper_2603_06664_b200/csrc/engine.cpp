@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -112,6 +113,7 @@ Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_
 }
 
 Engine::~Engine() {
+    drop_graphs();
     for (RankState& rs : ranks_) {
         cudaSetDevice(rs.device);
         cudaStreamSynchronize(rs.stream);
@@ -131,6 +133,14 @@ Engine::~Engine() {
         if (rs.copy_stream) {
             cudaStreamSynchronize(rs.copy_stream);
             cudaStreamDestroy(rs.copy_stream);
+        }
+        if (rs.d2h_stream) {
+            cudaStreamSynchronize(rs.d2h_stream);
+            cudaStreamDestroy(rs.d2h_stream);
+        }
+        for (int b = 0; b < 2; ++b) {
+            if (rs.ev_out_ready[b]) cudaEventDestroy(rs.ev_out_ready[b]);
+            if (rs.ev_out_free[b]) cudaEventDestroy(rs.ev_out_free[b]);
         }
     }
     for (auto& kv : weights_) {
@@ -256,10 +266,9 @@ void Engine::ipc_import(const uint8_t* blobs, size_t per_rank) {
 }
 
 void Engine::peer_barrier(RankState& rs, int slot) {
-    const uint64_t e = ++epoch_[slot];
     PeerFlags f{};
     for (int r = 0; r < P_; ++r) f.rank_flags[r] = peers_[static_cast<size_t>(r)].flags;
-    peer_barrier_run(f, rs.flags, static_cast<int>(P_), rs.rank, slot, e, peer_timeout_ns_,
+    peer_barrier_run(f, rs.flags, static_cast<int>(P_), rs.rank, slot, peer_timeout_ns_,
                      peer_error_dev_, rs.stream);
 }
 
@@ -322,7 +331,8 @@ void Engine::allocate() {
             rs.tab_scratch = dev_alloc<float2>(rs, static_cast<size_t>(n));
         }
         if (world_->transport() == SPX_TRANSPORT_PEER) {
-            rs.flags = dev_alloc<uint64_t>(rs, static_cast<size_t>(kPeerSlots * P_));
+            // [kPeerSlots][P] shared flag words + [kPeerSlots] private epoch counters
+            rs.flags = dev_alloc<uint64_t>(rs, static_cast<size_t>(kPeerSlots * P_ + kPeerSlots));
             SPX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&peer_error_host_), sizeof(int),
                                    cudaHostAllocMapped));
             *peer_error_host_ = 0;
@@ -720,7 +730,7 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
             run_plan(rs, layer, plan_qkv_exchange(part_, rs.rank, block_base_row_));
         }
         // ledger: one fused exchange (q: G-1 peers, k/v: P-1 peers per source) ...
-        world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
+        if (!capturing_) world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
     } else {
         // three all-gathers along the sequence (collectives.cpp:180-201; ledger +1 each)
         const int64_t shape[4] = {1, Lp_, H_, D_};
@@ -827,7 +837,7 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         run_plan(rs, layer, plan_out_exchange(part_, rs.rank));
     }
     // ... and one output all-to-all (G-1 peers per rank)
-    world_->add_stats(0, 1, 0, out_exchange_elements(part_), 1);
+    if (!capturing_) world_->add_stats(0, 1, 0, out_exchange_elements(part_), 1);
 
     // K8 output projection
     for (int li = 0; li < nl; ++li) {
@@ -893,8 +903,85 @@ void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_s
     }
 }
 
-// the layers of one denoise step on x[0] of every local rank (output in x[layers % 2])
+// the layers of one denoise step on x[0] of every local rank (output in x[layers % 2]):
+// replayed from a CUDA graph per KV-ring state when graphs_allowed(), enqueued launch by
+// launch otherwise
 void Engine::run_step(int64_t start) {
+    if (!graphs_allowed()) {
+        run_step_eager(start);
+        return;
+    }
+    RankState& rs = ranks_[0];
+    SPX_CUDA(cudaSetDevice(rs.device));
+    // everything a step's kernel parameters depend on besides the fixed buffers
+    const std::array<int64_t, 7> key{block_base_row_, num_segs_, seg_start_[0], seg_len_[0],
+                                     seg_start_[1], seg_len_[1], start};
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+        if (graphs_.size() >= kMaxGraphs) {  // evict the least recently used
+            auto lru = graphs_.begin();
+            for (auto g = graphs_.begin(); g != graphs_.end(); ++g)
+                if (g->second.last_use < lru->second.last_use) lru = g;
+            SPX_CUDA(cudaStreamSynchronize(rs.stream));
+            SPX_CUDA(cudaGraphExecDestroy(lru->second.exec));
+            graphs_.erase(lru);
+        }
+        StepGraph sg;
+        const int64_t l0 = launch_count();
+        cudaGraph_t g = nullptr;
+        SPX_CUDA(cudaStreamBeginCapture(rs.stream, cudaStreamCaptureModeThreadLocal));
+        capturing_ = true;
+        try {
+            run_step_eager(start);
+        } catch (...) {
+            capturing_ = false;
+            cudaStreamEndCapture(rs.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        capturing_ = false;
+        SPX_CUDA(cudaStreamEndCapture(rs.stream, &g));
+        sg.launches = launch_count() - l0;
+        count_launch(static_cast<int>(-sg.launches));  // captured, not launched
+        const cudaError_t e = cudaGraphInstantiateWithFlags(&sg.exec, g, 0);
+        cudaGraphDestroy(g);
+        SPX_CUDA(e);
+        it = graphs_.emplace(key, sg).first;
+    }
+    it->second.last_use = ++graph_clock_;
+    SPX_CUDA(cudaGraphLaunch(it->second.exec, rs.stream));
+    count_launch(static_cast<int>(it->second.launches));
+    for (int64_t l = 0; l < cfg_.layers; ++l) {  // the ledger of the replayed layer calls
+        world_->add_stats(0, 0, 1, qkv_exchange_elements(part_), 1);
+        world_->add_stats(0, 1, 0, out_exchange_elements(part_), 1);
+    }
+}
+
+bool Engine::graphs_allowed() const {
+    static const bool env_on = [] {
+        const char* e = std::getenv("SPX_GRAPHS");
+        return !(e && std::atoi(e) == 0);
+    }();
+    // one local rank (multi-rank LOCAL worlds order their streams with host-side events),
+    // no NCCL calls, the optimized schedule (its ledger is the fixed per-call pair above),
+    // no per-stage profiling events and no span tracing
+    return env_on && graphs_enabled_ && ranks_.size() == 1 &&
+           world_->transport() != SPX_TRANSPORT_NCCL && cfg_.ablation == SPX_ABLATION_ALL &&
+           cfg_.profile == 0 && !span_tracing() &&
+           !(world_->transport() == SPX_TRANSPORT_PEER && !peers_ready_);
+}
+
+void Engine::drop_graphs() {
+    if (graphs_.empty()) return;
+    for (RankState& rs : ranks_) {
+        cudaSetDevice(rs.device);
+        cudaStreamSynchronize(rs.stream);
+    }
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+}
+
+void Engine::run_step_eager(int64_t start) {
     for (int64_t l = 0; l < cfg_.layers; ++l) {
         std::vector<const GemmPlan*> qv, ov;
         std::vector<const bf16*> xv;
@@ -1000,6 +1087,100 @@ void Engine::generate_block(int64_t block, const uint16_t* noise_host, uint16_t*
         SPX_CUDA(cudaSetDevice(rs.device));
         SPX_CUDA(cudaMemcpyAsync(out_host + static_cast<size_t>(rs.local) * Lp_ * C_, rs.x[fin],
                                  slice_bytes, cudaMemcpyDeviceToHost, rs.stream));
+    }
+    synchronize();
+}
+
+// Streaming generator (the paper's overlap theme): n blocks
+// back to back with every host copy off the compute stream. The copy stream uploads step k + 1
+// of the noise into one of two staging buffers while step k computes; at the end of a block
+// the latent is copied (device to device) into one of two output staging buffers and a third
+// stream downloads it to the host while the next block computes. The host thread only
+// enqueues (graph launches + copies) and waits once at the end.
+void Engine::generate_stream(const int64_t* blocks, int64_t n, const uint16_t* const* noise_host,
+                             uint16_t* const* out_host) {
+    require(n >= 0 && (n == 0 || (blocks && noise_host && out_host)), SPX_ERR_CONFIG,
+            "null argument");
+    for (int64_t i = 0; i < n; ++i)
+        require(blocks[i] >= 0 && blocks[i] < cfg_.num_blocks && noise_host[i] && out_host[i],
+                SPX_ERR_RANGE, "block " + std::to_string(i) + " out of range or null buffer");
+    const size_t block_elems = static_cast<size_t>(L_ * C_);
+    const size_t slice_bytes = static_cast<size_t>(Lp_ * C_) * sizeof(bf16);
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        if (!rs.copy_stream) {
+            SPX_CUDA(cudaStreamCreateWithFlags(&rs.copy_stream, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b) {
+                rs.nstage[b] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
+                SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_ready[b], cudaEventDisableTiming));
+                SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_used[b], cudaEventDisableTiming));
+            }
+        }
+        if (!rs.d2h_stream) {
+            SPX_CUDA(cudaStreamCreateWithFlags(&rs.d2h_stream, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b) {
+                rs.ostage[b] = dev_alloc<bf16>(rs, static_cast<size_t>(Lp_ * C_));
+                SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_out_ready[b], cudaEventDisableTiming));
+                SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_out_free[b], cudaEventDisableTiming));
+            }
+        }
+        // earlier work (a previous call) may still read the staging buffers
+        for (int b = 0; b < 2; ++b) {
+            SPX_CUDA(cudaEventRecord(rs.ev_used[b], rs.stream));
+            SPX_CUDA(cudaEventRecord(rs.ev_out_free[b], rs.d2h_stream));
+        }
+    }
+    const int fin = static_cast<int>(cfg_.layers % 2);
+    int64_t k = 0;  // global step counter (staging buffer k % 2)
+    auto upload = [&](int64_t i, int64_t step, int64_t kk) {
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            const int b = static_cast<int>(kk % 2);
+            SPX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.ev_used[b], 0));
+            SPX_CUDA(cudaMemcpyAsync(rs.nstage[b],
+                                     noise_host[i] + static_cast<size_t>(step) * block_elems +
+                                         static_cast<size_t>(rs.rank * Lp_ * C_),
+                                     slice_bytes, cudaMemcpyHostToDevice, rs.copy_stream));
+            SPX_CUDA(cudaEventRecord(rs.ev_ready[b], rs.copy_stream));
+        }
+    };
+    if (n > 0) upload(0, 0, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t block = blocks[i];
+        run_block(block, [&](int64_t step) {
+            for (RankState& rs : ranks_) {
+                SPX_CUDA(cudaSetDevice(rs.device));
+                const int b = static_cast<int>(k % 2);
+                SPX_CUDA(cudaStreamWaitEvent(rs.stream, rs.ev_ready[b], 0));
+                SPX_CUDA(cudaMemcpyAsync(rs.x[0], rs.nstage[b], slice_bytes,
+                                         cudaMemcpyDeviceToDevice, rs.stream));
+                SPX_CUDA(cudaEventRecord(rs.ev_used[b], rs.stream));
+            }
+            // the next step's noise (this block's next step, or the next block's first)
+            if (step + 1 < cfg_.denoise_steps)
+                upload(i, step + 1, k + 1);
+            else if (i + 1 < n)
+                upload(i + 1, 0, k + 1);
+            ++k;
+        });
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            const int b = static_cast<int>(i % 2);
+            SPX_CUDA(cudaStreamWaitEvent(rs.stream, rs.ev_out_free[b], 0));
+            SPX_CUDA(cudaMemcpyAsync(rs.ostage[b], rs.x[fin], slice_bytes, cudaMemcpyDeviceToDevice,
+                                     rs.stream));
+            SPX_CUDA(cudaEventRecord(rs.ev_out_ready[b], rs.stream));
+            SPX_CUDA(cudaStreamWaitEvent(rs.d2h_stream, rs.ev_out_ready[b], 0));
+            SPX_CUDA(cudaMemcpyAsync(out_host[i] + static_cast<size_t>(rs.local) * Lp_ * C_,
+                                     rs.ostage[b], slice_bytes, cudaMemcpyDeviceToHost,
+                                     rs.d2h_stream));
+            SPX_CUDA(cudaEventRecord(rs.ev_out_free[b], rs.d2h_stream));
+        }
+    }
+    for (RankState& rs : ranks_) {
+        SPX_CUDA(cudaSetDevice(rs.device));
+        SPX_CUDA(cudaStreamSynchronize(rs.d2h_stream));
+        SPX_CUDA(cudaStreamSynchronize(rs.copy_stream));
     }
     synchronize();
 }

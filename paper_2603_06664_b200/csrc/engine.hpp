@@ -78,6 +78,11 @@ struct RankState {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready[2] = {nullptr, nullptr};
     cudaEvent_t ev_used[2] = {nullptr, nullptr};
+    // generate_stream: block latents leave through two output staging buffers on a D2H stream
+    bf16* ostage[2] = {nullptr, nullptr};
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t ev_out_ready[2] = {nullptr, nullptr};
+    cudaEvent_t ev_out_free[2] = {nullptr, nullptr};
     std::vector<void*> allocations;
 };
 
@@ -112,6 +117,11 @@ class Engine {
     // (steps, L/P, C) bf16, out_dev[local] receives (L/P, C)
     void generate_block_device(int64_t block, const void* const* noise_dev, void* const* out_dev);
     void generate(uint16_t* out_host);
+    // n blocks back to back (blocks[i] may repeat: a block re-denoised overwrites its slots),
+    // noise_host[i]: (steps, L, C) bf16 of block i, out_host[i]: (rows of the local ranks, C);
+    // host copies overlap the compute (upload of the next step, download of the last block)
+    void generate_stream(const int64_t* blocks, int64_t n, const uint16_t* const* noise_host,
+                         uint16_t* const* out_host);
     // one denoise step of a block (generator.cpp:94-110): x[local] (L/P, C) device bf16 in,
     // y[local] after every layer; asynchronous on the world's streams
     void denoise_step(int64_t block, int64_t step, const void* const* x, void* const* y);
@@ -121,6 +131,12 @@ class Engine {
     // 0 off, 1 every stage (six CUDA-event intervals per call), 2 attention launch only,
     // 3 attention launch of every 8th call
     void set_profile(int level) { cfg_.profile = level; }
+    // per-step CUDA graphs on (default) / off (every launch enqueued by the host)
+    int64_t graph_count() const { return static_cast<int64_t>(graphs_.size()); }
+    void set_graphs(bool on) {
+        graphs_enabled_ = on;
+        if (!on) drop_graphs();
+    }
     spx_comm_stats stats() const { return world_->stats(); }
     // PEER transport: CUDA IPC handles of this rank's exchange buffers, and the mapping of
     // every peer's (blobs of all ranks in rank order)
@@ -131,6 +147,9 @@ class Engine {
     void allocate();
     void run_block(int64_t block, const std::function<void(int64_t)>& load_step);
     void run_step(int64_t start_frame);
+    void run_step_eager(int64_t start_frame);
+    bool graphs_allowed() const;
+    void drop_graphs();
     void build_plans();
     // x_in[local]: the layer input (the K1 source with cfg.adaln; otherwise the QKV plans'
     // A operand already points at it)
@@ -179,7 +198,18 @@ class Engine {
     std::vector<PeerView> peers_;  // by global rank
     std::vector<void*> ipc_opened_;
     bool peers_ready_ = false;
-    uint64_t epoch_[2] = {0, 0};
+    // per-step CUDA graphs, keyed by the KV-ring state and start frame (the only launch
+    // parameters that change between steps); see run_step
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        uint64_t last_use = 0;
+    };
+    static constexpr size_t kMaxGraphs = 24;
+    std::map<std::array<int64_t, 7>, StepGraph> graphs_;
+    uint64_t graph_clock_ = 0;
+    bool capturing_ = false;
+    bool graphs_enabled_ = true;
     int* peer_error_host_ = nullptr;  // host-mapped: 1 + the rank a PEER barrier timed out on
     int* peer_error_dev_ = nullptr;
     uint64_t peer_timeout_ns_ = 0;

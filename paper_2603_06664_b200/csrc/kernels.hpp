@@ -180,9 +180,10 @@ void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const fl
 
 // ---------------------------------------------------------------------------------------
 // PEER transport: device-side rank barrier over IPC-mapped flag words. Each rank owns
-// flags[kPeerSlots][P] (uint64, epoch values). After this stream's prior kernels (whose
-// stores may target peer memory): st.release.sys flags[slot][my_rank] = epoch in every
-// rank's array, then spin (ld.acquire.sys) until every entry of flags[slot] >= epoch.
+// flags[kPeerSlots][P] (uint64, epoch values) followed by its private epoch counters
+// [kPeerSlots]. After this stream's prior kernels (whose stores may target peer memory):
+// epoch = ++counter[slot]; st.release.sys flags[slot][my_rank] = epoch in every rank's array,
+// then spin (ld.acquire.sys) until every entry of flags[slot] >= epoch.
 // ---------------------------------------------------------------------------------------
 constexpr int kPeerSlots = 2;
 constexpr int kMaxPeers = 8;
@@ -193,7 +194,7 @@ struct PeerFlags {
 // stores 1 + (the first missing rank) into *error_word (host-mapped) and returns, so a dead or
 // diverged peer surfaces as SPX_ERR_COLLECTIVE instead of a hung stream.
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
-                      uint64_t epoch, uint64_t timeout_ns, int* error_word, cudaStream_t s);
+                      uint64_t timeout_ns, int* error_word, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // Kd: naive fp32 SIMT reference kernels (GPU oracle at shapes the CPU oracle cannot reach).

@@ -21,10 +21,16 @@ namespace {
 // kernel's tail, griddepcontrol.wait makes that kernel's stores (peer stores included)
 // complete before the release, and the next kernel's prologue overlaps the spin
 __global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, int my_rank, int slot,
-                                    uint64_t epoch, uint64_t timeout_ns, int* error_word) {
+                                    uint64_t timeout_ns, int* error_word) {
     pdl_trigger();
     pdl_wait();
     const int r = threadIdx.x;
+    // this slot's epoch lives on the device (after the shared [slots][P] flag words), so that
+    // the launch parameters are the same on every call and a captured CUDA graph replays it
+    uint64_t* my_epoch = my_flags + kPeerSlots * world + slot;
+    uint64_t epoch = 0;
+    if (r == 0) epoch = *my_epoch + 1;
+    epoch = __shfl_sync(0xffffffffu, epoch, 0);
     if (r < world) {
         uint64_t* dst = f.rank_flags[r] + slot * world + my_rank;
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
@@ -51,6 +57,7 @@ __global__ void peer_barrier_kernel(PeerFlags f, uint64_t* my_flags, int world, 
         }
     }
     __syncwarp();
+    if (r == 0) *my_epoch = epoch;
 }
 
 
@@ -151,8 +158,8 @@ __global__ void naive_attention_kernel(const bf16* __restrict__ q, const bf16* _
 }  // namespace
 
 void peer_barrier_run(const PeerFlags& f, uint64_t* my_flags, int world, int my_rank, int slot,
-                      uint64_t epoch, uint64_t timeout_ns, int* error_word, cudaStream_t s) {
-    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot, epoch,
+                      uint64_t timeout_ns, int* error_word, cudaStream_t s) {
+    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, f, my_flags, world, my_rank, slot,
                timeout_ns, error_word);
     count_launch();
 }

@@ -580,6 +580,31 @@ class Engine:
                                               out.ctypes.data))
         return out
 
+    def generate_stream(self, blocks, noise_bits):
+        """blocks back to back with host copies overlapped (spx_engine_generate_stream):
+        noise_bits[i] (steps, L, H, D) uint16 of block blocks[i]; returns the latents, one
+        (rows of the local ranks, H, D) uint16 array per block. Pinned buffers are used."""
+        torch = _torch()
+        n = len(blocks)
+        want = self.cfg.denoise_steps * self.cfg.block_len() * self.cfg.heads * self.cfg.head_dim
+        pins = []
+        for nb in noise_bits:
+            a = np.ascontiguousarray(nb, dtype=np.uint16)
+            if a.size != want:
+                raise ShapeError(f"noise holds {a.size} values, expected {want}")
+            pins.append(torch.from_numpy(a.view(np.int16).reshape(-1)).pin_memory())
+        rows = self.local_len * self.local_ranks
+        outs = [torch.empty(rows * self.cfg.heads * self.cfg.head_dim, dtype=torch.int16).pin_memory()
+                for _ in range(n)]
+        check(lib().spx_engine_generate_stream(self._h, i64_array(list(blocks)), n,
+                                               ptr_array([p.data_ptr() for p in pins]),
+                                               ptr_array([o.data_ptr() for o in outs])))
+        return [o.numpy().view(np.uint16).reshape(rows, self.cfg.heads, self.cfg.head_dim) for o in outs]
+
+    def set_graphs(self, on: bool):
+        """per-step CUDA graphs (default on) / every kernel enqueued by the host"""
+        check(lib().spx_engine_set_graphs(self._h, int(bool(on))))
+
     def denoise_step(self, block, step, x_locals):
         """one denoise step of `block` (generator.cpp:94-110) on every local rank: x_locals are
         (L/P, H, D) bf16 CUDA tensors (noise), returns the last layer's outputs."""

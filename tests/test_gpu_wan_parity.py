@@ -11,11 +11,17 @@ plus sequence-parallel bit identity at H = 12 (P = 2, 4 Ulysses; P = 8 the 4 x 2
 query-split partition), the attention kernel at 4680 x 32760 x 12 and over a wrapped Wan-scale
 ring, and a well-conditioned 2-layer check of the token-discriminating (centred) signal.
 
-Tolerances: deep stacks are compared at RMS level (rel-L2 <= 1e-2): the reference
-model has no residual or norm and its N(0, 1/fan_in) weights give logits of std ~ 1/D, so every
-token collapses toward the block mean of V and the token-discriminating part
-is below bf16 resolution; the centred check therefore uses O(1) logits. The measured errors
-are logged (SPX_PARITY_LOG) and committed as profiles/parity_r02.json.
+Tolerances. Deep stacks: the reference model has no residual or norm and its
+N(0, 1/fan_in) weights give logits of std ~ 1/D, so every token collapses toward the block mean
+of V; the token-discriminating part is below bf16 resolution (the centred check
+therefore uses O(1) logits). Each block's latent is checked
+  * at RMS level: | ||device|| / ||fp64|| - 1 | < 1e-2, and
+  * element-wise: rel-L2(device, fp64) < 1.5 x rel-L2(bf16-storage model, fp64) + 1e-3, where
+    the model is the same fp64 pipeline with every inter-kernel tensor rounded to bf16
+    (gpu_oracle storage="bf16"): the error that bf16 storage alone implies at that depth
+    (one layer: ~3e-3; 30 layers: ~1.1e-2 -- the per-layer roundings random-walk through the
+    chain, so a fixed 1e-2 bar is not a property of the kernels at depth 30).
+The measured errors are logged (SPX_PARITY_LOG) and committed as profiles/parity_r02.json.
 """
 import math
 
@@ -66,17 +72,32 @@ def free_gpu():
     torch.cuda.empty_cache()
 
 
-def compare_blocks(got, ref, parity_log, bar=1e-2):
-    errs = []
+def compare_blocks(got, ref, model, parity_log):
+    """got: device latents, ref: fp64 oracle, model: the bf16-storage error model (or None
+    for single-layer checks, bar 1e-2)."""
+    rows = []
     for b in range(ref.shape[0]):
         e = rel_l2(got[b], ref[b])
-        mx = float(np.abs(got[b] - ref[b]).max())
-        errs.append((e, mx))
-    parity_log(rel_l2_max=max(e for e, _ in errs), rel_l2_per_block=[e for e, _ in errs],
-               max_abs_per_block=[m for _, m in errs],
-               ref_rms=float(np.sqrt(np.mean(ref ** 2))), bar_rel_l2=bar)
-    for b, (e, _) in enumerate(errs):
-        assert e < bar, (b, errs)
+        em = rel_l2(model[b], ref[b]) if model is not None else None
+        rms = abs(np.linalg.norm(got[b]) / np.linalg.norm(ref[b]) - 1.0)
+        rows.append((e, em, rms, float(np.abs(got[b] - ref[b]).max())))
+    parity_log(rel_l2_per_block=[r[0] for r in rows],
+               bf16_storage_model_rel_l2_per_block=[r[1] for r in rows] if model is not None else None,
+               rms_level_dev_per_block=[r[2] for r in rows], max_abs_per_block=[r[3] for r in rows],
+               ref_rms=float(np.sqrt(np.mean(ref ** 2))),
+               bar="rms-level < 1e-2; rel-L2 < 1.5 x bf16-storage model + 1e-3")
+    for b, (e, em, rms, _) in enumerate(rows):
+        assert rms < 1e-2, (b, rows)
+        assert e < (1.5 * em + 1e-3 if em is not None else 1e-2), (b, rows)
+
+
+def oracle_pair(**kw):
+    """the fp64 oracle and the bf16-storage error model of one configuration"""
+    ref = gpu_oracle.ReferenceModel(**WAN, **kw).generate()
+    free_gpu()
+    model = gpu_oracle.ReferenceModel(**WAN, **kw, storage="bf16").generate()
+    free_gpu()
+    return ref, model
 
 
 def test_c2_chunk_30_layers_4_steps_vs_fp64(cuda, parity_log):
@@ -85,8 +106,8 @@ def test_c2_chunk_30_layers_4_steps_vs_fp64(cuda, parity_log):
     got = device_out(eng)
     del eng
     free_gpu()
-    ref = gpu_oracle.ReferenceModel(**WAN, layers=30, num_blocks=1, steps=4).generate()
-    compare_blocks(got, ref, parity_log)
+    ref, model = oracle_pair(layers=30, num_blocks=1, steps=4)
+    compare_blocks(got, ref, model, parity_log)
 
 
 def test_c3_video_7_chunks_vs_fp64(cuda, parity_log):
@@ -95,8 +116,8 @@ def test_c3_video_7_chunks_vs_fp64(cuda, parity_log):
     got = device_out(eng)
     del eng
     free_gpu()
-    ref = gpu_oracle.ReferenceModel(**WAN, layers=30, num_blocks=7, steps=4).generate()
-    compare_blocks(got, ref, parity_log)
+    ref, model = oracle_pair(layers=30, num_blocks=7, steps=4)
+    compare_blocks(got, ref, model, parity_log)
 
 
 @pytest.mark.parametrize("world", [1, 8])
@@ -109,8 +130,8 @@ def test_c5_rolling_window_ring_wraps_vs_fp64(cuda, parity_log, world):
     got = device_out(eng)
     del eng
     free_gpu()
-    ref = gpu_oracle.ReferenceModel(**WAN, layers=2, num_blocks=24, steps=2, window=21).generate()
-    compare_blocks(got, ref, parity_log)
+    ref, model = oracle_pair(layers=2, num_blocks=24, steps=2, window=21)
+    compare_blocks(got, ref, model, parity_log)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
