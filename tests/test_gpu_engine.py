@@ -582,3 +582,56 @@ def test_denoise_step_api_matches_generate_block(cuda, world):
         assert np.array_equal(got.reshape(want[b].shape), want[b]), b
     with pytest.raises(s.RangeError):
         e.denoise_step(0, 3, xs)
+
+
+def _graphs(eng):
+    import ctypes
+
+    from paper_2603_06664_b200._lib import check, lib
+
+    n = ctypes.c_int64()
+    check(lib().spx_debug_engine_graphs(eng._h, ctypes.byref(n)))
+    return n.value
+
+
+@pytest.mark.parametrize("window", [None, 3])
+def test_step_graphs_bit_identical_to_eager(cuda, window):
+    """Per-step CUDA graphs (captured per KV-ring state, replayed for every denoise step):
+    the same outputs bit for bit, the same ledger and the same kernel-launch count as the
+    launch-by-launch path (incl. a wrapping 3-frame window: ring states repeat)."""
+    from paper_2603_06664_b200._lib import lib
+
+    s = spattn()
+    kw = dict(TINY, num_blocks=4)
+    w = _scaled_weights(kw["heads"] * kw["head_dim"], kw["layers"], 4.0, seed=15)
+    runs = {}
+    for graphs in (True, False):
+        eng = _engine_with_weights(cfg_from(kw, steps=3, window_frames=window), w)
+        eng.set_graphs(graphs)
+        l0 = int(lib().spx_launch_count())
+        out = eng.generate()
+        runs[graphs] = (out, eng.stats(), int(lib().spx_launch_count()) - l0, _graphs(eng))
+    assert np.array_equal(runs[True][0], runs[False][0])
+    assert runs[True][1] == runs[False][1] and runs[True][2] == runs[False][2]
+    assert runs[True][3] >= 1 and runs[False][3] == 0
+
+
+def test_generate_stream_matches_block_by_block(cuda):
+    """spx_engine_generate_stream (noise upload of the next step and download of the previous
+    latent overlapped with the compute) == generate_block called block by block, incl. a
+    block denoised twice in a row."""
+    s = spattn()
+    kw = dict(TINY)
+    cfg = cfg_from(kw, steps=2)
+    L, C = 192, kw["heads"] * kw["head_dim"]
+    rng = np.random.default_rng(9)
+    order = [0, 1, 1, 2]
+    noise = [oracle.to_bf16_bits(oracle.round_bf16(rng.standard_normal((2, L, C)) * 0.1))
+             for _ in order]
+    a = s.Engine(cfg)
+    want = [a.generate_block(b, noise[i]) for i, b in enumerate(order)]
+    e = s.Engine(cfg)
+    got = e.generate_stream(order, noise)
+    for i in range(len(order)):
+        assert np.array_equal(got[i], want[i]), i
+    assert e.stats() == a.stats()
