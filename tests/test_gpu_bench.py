@@ -33,7 +33,9 @@ def test_bench_line_contract():
     assert d["unit"] == "latent frames/s" and d["higher_is_better"] is True
     assert d["value"] > 0 and abs(d["value"] - 3 * 1e3 / d["ms_per_step"]) < 1e-6 * d["value"]
     e2e = d["e2e"]
-    assert e2e["unit"] == d["unit"] and 0 < e2e["value"] <= d["value"] * 1.02
+    # the streaming e2e overlaps its copies with compute: bounded by the faster device rate
+    assert e2e["unit"] == d["unit"]
+    assert 0 < e2e["value"] <= max(d["value"], d["graph_replay"]["value"]) * 1.02
     assert e2e["h2d_bytes_per_step"] == 4 * 4680 * 1536 * 2   # 4 denoise steps of bf16 noise
     assert e2e["d2h_bytes_per_step"] == 4680 * 1536 * 2       # one bf16 latent
     rf = d["roofline"]
