@@ -116,6 +116,12 @@ spx_status spx_rope_apply_global(const spx_rope_table* table, const void* x, voi
  * x (tokens, c_in) bf16, w (c_out, c_in) bf16 row-major, y (tokens, c_out) bf16. */
 spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tokens,
                               int64_t c_in, int64_t c_out, void* stream);
+/* project_tokens with the epilogues of the Wan block (extension): acc' = x W^T (+ bias[c_out]
+ * fp32 when bias != NULL); epilogue 0: y = acc', 1: y = residual + gate * acc' (gate fp32
+ * [c_out] or NULL = 1; residual (tokens, c_out) bf16, may alias y), 3: y = GELU_tanh(acc') */
+spx_status spx_project_tokens_ex(const void* x, const void* w, void* y, int64_t tokens,
+                                 int64_t c_in, int64_t c_out, const float* bias, int32_t epilogue,
+                                 const void* residual, const float* gate, void* stream);
 /* K6 scaled_dot_product_attention (proj/src/tensor.cpp:161-209), no mask.
  * q (B, Sq, H, D), k/v (B, Skv, H, D), o (B, Sq, H, D); bf16, B == 1, D in {64, 128}. */
 spx_status spx_attention(const void* q, const void* k, const void* v, void* o, int64_t batch,
@@ -273,6 +279,25 @@ typedef struct spx_engine_config {
                                          weights into L2 (bulk prefetch); 0 (default) since
                                          the weight-tile-early GEMM pipelines made it a net
                                          loss under the power cap */
+    /* The full Wan2.1 DiT block (extension; the reference model is attention-only).
+     * wan_block = 1 implies adaln = qk_norm = 1 and adds, per layer, biases on every
+     * projection, the cross-attention to text_len cached context tokens (affine LayerNorm,
+     * QK-RMSNorm, K/V computed once per video by spx_engine_set_context) and the GELU(tanh)
+     * FFN dim -> ffn_dim -> dim, each with its residual; the six per-layer modulation vectors
+     * come from the timestep embedding of the current denoise step (freq_dim sinusoid, two
+     * Linear layers, SiLU, Linear to 6 dim) plus the layer's modulation parameters. */
+    int32_t wan_block;
+    int64_t ffn_dim;                  /* <= 0: ceil(dim * 35 / 6 / 64) * 64 (8960 at 1536) */
+    int64_t text_len;                 /* context tokens (512) */
+    int64_t text_dim;                 /* raw context width (4096, the umT5 encoder's) */
+    int64_t freq_dim;                 /* sinusoidal timestep embedding width (256) */
+    int32_t sp_bit_exact;             /* 1: attention never splits a query tile's kv range over
+                                         CTAs, so every partition P = G x S keeps the P = 1
+                                         summation order and SP outputs equal P = 1 bit for bit
+                                         (the reference's invariant); 0 (default): split-KV
+                                         layouts where the per-rank grid under-fills the SMs
+                                         (P = 2, 8 at the Wan shape), outputs within bf16
+                                         rounding of P = 1 */
 } spx_engine_config;
 
 /* GenerationConfig defaults (proj/include/spattn/generator.hpp:14-42) */
@@ -324,6 +349,39 @@ spx_status spx_engine_generate_block_device(spx_engine* engine, int64_t block,
  * the compute; returns when every latent is on the host. Host buffers must be pinned. */
 spx_status spx_engine_generate_stream(spx_engine* engine, const int64_t* blocks, int64_t n,
                                       const uint16_t* const* noise_host, uint16_t* const* out_host);
+/* ---- the full Wan2.1 block (cfg.wan_block = 1; extension) ----
+ * Per-layer weights (host pointers; [out][in] row-major bf16 matrices, fp32 vectors). The
+ * self-attention projections themselves are spx_engine_set_layer_weights, its QK-RMSNorm
+ * weights spx_engine_set_norm_weights; this sets everything else of the layer. */
+typedef struct spx_wan_layer_weights {
+    const float *self_bq, *self_bk, *self_bv, *self_bo;      /* [dim] */
+    const float *norm3_w, *norm3_b;                          /* [dim] affine LayerNorm */
+    const uint16_t *cross_q, *cross_k, *cross_v, *cross_o;   /* [dim][dim] */
+    const float *cross_bq, *cross_bk, *cross_bv, *cross_bo;  /* [dim] */
+    const uint16_t *cross_norm_q, *cross_norm_k;             /* [dim] RMSNorm weights */
+    const uint16_t* ffn_w1;                                  /* [ffn_dim][dim] */
+    const float* ffn_b1;                                     /* [ffn_dim] */
+    const uint16_t* ffn_w2;                                  /* [dim][ffn_dim] */
+    const float* ffn_b2;                                     /* [dim] */
+    const float* modulation;                                 /* [6][dim] */
+} spx_wan_layer_weights;
+spx_status spx_engine_set_wan_layer(spx_engine* engine, int64_t layer,
+                                    const spx_wan_layer_weights* w);
+/* the embeddings shared by all layers */
+typedef struct spx_wan_embed_weights {
+    const uint16_t* time_w1; const float* time_b1;  /* [dim][freq_dim], [dim] */
+    const uint16_t* time_w2; const float* time_b2;  /* [dim][dim], [dim] */
+    const uint16_t* proj_w;  const float* proj_b;   /* [6 dim][dim], [6 dim] */
+    const uint16_t* text_w1; const float* text_b1;  /* [dim][text_dim], [dim] */
+    const uint16_t* text_w2; const float* text_b2;  /* [dim][dim], [dim] */
+} spx_wan_embed_weights;
+spx_status spx_engine_set_wan_embeddings(spx_engine* engine, const spx_wan_embed_weights* w);
+/* timesteps of the denoise steps (host fp32 [denoise_steps]; default 1000 -> 250 evenly) */
+spx_status spx_engine_set_timesteps(spx_engine* engine, const float* t);
+/* a video's text context (host bf16 [text_len][text_dim]): runs the text embedding and every
+ * layer's cross-attention K (RMSNorm'd) and V once; they stay cached until the next call */
+spx_status spx_engine_set_context(spx_engine* engine, const uint16_t* text);
+
 /* per-step CUDA graphs (default on): the layer calls of a denoise step are captured once per
  * KV-ring state and replayed (one launch per step instead of 3 x layers), on a world with one
  * local rank (PEER, or LOCAL P = 1), the optimized schedule and profiling off; off = every

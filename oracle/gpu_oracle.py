@@ -120,6 +120,32 @@ def rms_norm(x, w, eps):
     return x * r * (w[None, :] if w is not None else 1.0)
 
 
+def layernorm(x, eps):
+    """non-affine LayerNorm over the last dim (biased variance, eps inside the sqrt)"""
+    mean = x.mean(dim=1, keepdim=True)
+    var = ((x - mean) ** 2).mean(dim=1, keepdim=True)
+    return (x - mean) / _torch().sqrt(var + eps)
+
+
+def gelu_tanh(x):
+    """torch.nn.GELU(approximate="tanh"): 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))"""
+    return 0.5 * x * (1.0 + _torch().tanh(math.sqrt(2.0 / math.pi) * (x + 0.044715 * x ** 3)))
+
+
+def silu(x):
+    return x * _torch().sigmoid(x)
+
+
+def sinusoidal_embedding(dim, t, device="cpu"):
+    """Wan2.1 sinusoidal_embedding_1d(dim, t): [cos(t f_j) | sin(t f_j)], f_j = 10000^(-j/half)"""
+    torch = _torch()
+    half = dim // 2
+    f = torch.pow(torch.tensor(10000.0, dtype=torch.float64, device=device),
+                  -torch.arange(half, dtype=torch.float64, device=device) / half)
+    a = float(t) * f
+    return torch.cat([torch.cos(a), torch.sin(a)])
+
+
 def layernorm_modulate(x, shift, scale, eps):
     mean = x.mean(dim=1, keepdim=True)
     var = ((x - mean) ** 2).mean(dim=1, keepdim=True)
@@ -163,7 +189,7 @@ class ReferenceModel:
     def __init__(self, frames, grid_h, grid_w, heads, head_dim, layers, num_blocks, steps,
                  window=None, seed=0, base=10000.0, split=None, weights=None, round_inputs=True,
                  qk_norm=False, norm_weights=None, modulation=None, norm_eps=1e-6,
-                 force_start_frame_zero=False, device="cuda", storage="fp64"):
+                 force_start_frame_zero=False, device="cuda", storage="fp64", wan=None):
         torch = _torch()
         self.grid = (frames, grid_h, grid_w)
         self.H, self.D = heads, head_dim
@@ -192,7 +218,80 @@ class ReferenceModel:
         self.mod = None
         if modulation is not None:
             self.mod = torch.from_numpy(np.asarray(modulation, dtype=np.float64)).to(device)
+        self.wan = None
+        if wan is not None:
+            self._init_wan(wan)
         self.reset()
+
+    # ---- the full Wan2.1 block (extension; wan/modules/model.py: WanAttentionBlock, the time
+    # embedding / projection and the text embedding of WanModel) ----
+    def _init_wan(self, wan):
+        """wan: dict of numpy arrays -- per layer lists under 'layers' (keys as in
+        spx_wan_layer_weights plus norm_q / norm_k for the self-attention RMSNorm), the
+        embeddings (spx_wan_embed_weights keys), 'text' (text_len, text_dim) and 'timesteps'.
+        Matrices / norm weights must already be bf16 values."""
+        torch = _torch()
+        dev = self.device
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        self.wan = {"layers": [{k: T(v) for k, v in lw.items()} for lw in wan["layers"]]}
+        for k in ("time_w1", "time_b1", "time_w2", "time_b2", "proj_w", "proj_b", "text_w1",
+                  "text_b1", "text_w2", "text_b2"):
+            self.wan[k] = T(wan[k])
+        self.wan["timesteps"] = [float(t) for t in wan["timesteps"]]
+        self.wan["freq_dim"] = self.wan["time_w1"].shape[1]
+        E = self.wan
+        text = T(wan["text"])
+        ctx = self._st(gelu_tanh(self._st(text) @ E["text_w1"].t() + E["text_b1"]))
+        ctx = self._st(ctx @ E["text_w2"].t() + E["text_b2"])
+        self.ctx_kv = []
+        for lw in E["layers"]:
+            k = self._st(rms_norm(self._st(ctx @ lw["cross_k"].t() + lw["cross_bk"]), lw["cross_norm_k"],
+                                  self.norm_eps))
+            v = self._st(ctx @ lw["cross_v"].t() + lw["cross_bv"])
+            self.ctx_kv.append((k.reshape(-1, self.H, self.D), v.reshape(-1, self.H, self.D)))
+
+    def wan_modulation(self, step):
+        """e0 = W_p SiLU(W_2 SiLU(W_1 sinusoid(t) + b_1) + b_2) + b_p, as (6, C)"""
+        E = self.wan
+        x = sinusoidal_embedding(E["freq_dim"], E["timesteps"][step], self.device)
+        h = silu(E["time_w1"] @ x + E["time_b1"])
+        e = E["time_w2"] @ h + E["time_b2"]
+        return (E["proj_w"] @ silu(e) + E["proj_b"]).reshape(6, self.C)
+
+    def wan_layer(self, l, block, start, x, e0):
+        """WanAttentionBlock.forward on x (L, C) with e = modulation[l] + e0 (6, C)"""
+        lw = self.wan["layers"][l]
+        L, H, D = self.L, self.H, self.D
+        e = lw["modulation"] + e0
+        eps = self.norm_eps
+        x = self._st(x)
+        xin = self._st(layernorm(x, eps) * (1.0 + e[1]) + e[0])
+        W = self.W[l]
+        q = xin @ W[0].t() + lw["self_bq"]
+        k = xin @ W[1].t() + lw["self_bk"]
+        v = xin @ W[2].t() + lw["self_bv"]
+        q = rms_norm(self._st(q), lw["norm_q"], eps)
+        k = rms_norm(self._st(k), lw["norm_k"], eps)
+        cos, sin = self.table.rows(start)
+        q = self._st(rope(q.reshape(L, H, D), cos, sin))
+        k = self._st(rope(k.reshape(L, H, D), cos, sin))
+        v = self._st(v)
+        cache = self.caches[l]
+        cache.update(block, k, v.reshape(L, H, D))
+        kk, vv = cache.read()
+        o = self._st(sdpa(q, kk, vv).reshape(L, self.C))
+        x = self._st(x + e[2] * (o @ W[3].t() + lw["self_bo"]))
+        # cross-attention over the cached context (no RoPE)
+        xn = self._st(layernorm(x, eps) * lw["norm3_w"] + lw["norm3_b"])
+        cq = self._st(xn @ lw["cross_q"].t() + lw["cross_bq"])
+        cq = self._st(rms_norm(cq, lw["cross_norm_q"], eps)).reshape(L, H, D)
+        kc, vc = self.ctx_kv[l]
+        oc = self._st(sdpa(cq, kc, vc).reshape(L, self.C))
+        x = self._st(x + oc @ lw["cross_o"].t() + lw["cross_bo"])
+        # FFN
+        xf = self._st(layernorm(x, eps) * (1.0 + e[4]) + e[3])
+        h = self._st(gelu_tanh(xf @ lw["ffn_w1"].t() + lw["ffn_b1"]))
+        return self._st(x + e[5] * (h @ lw["ffn_w2"].t() + lw["ffn_b2"]))
 
     def reset(self):
         hw = self.grid[1] * self.grid[2]
@@ -246,8 +345,9 @@ class ReferenceModel:
         x = None
         for s in range(self.steps):
             x = noise(s) if noise is not None else self.noise(b, s)
+            e0 = self.wan_modulation(s) if self.wan is not None else None
             for l in range(self.layers):
-                x = self.layer(l, b, start, x)
+                x = self.wan_layer(l, b, start, x, e0) if e0 is not None else self.layer(l, b, start, x)
         return x
 
     def generate(self):

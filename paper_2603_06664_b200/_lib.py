@@ -87,7 +87,27 @@ class EngineConfig(ctypes.Structure):
                 ("force_start_frame_zero", c_int32), ("qk_norm", c_int32),
                 ("norm_eps", c_float), ("profile", c_int32),
                 ("fuse_rope_epilogue", c_int32), ("ablation", c_int32), ("adaln", c_int32),
-                ("l2_prefetch", c_int32)]
+                ("l2_prefetch", c_int32), ("wan_block", c_int32), ("ffn_dim", c_int64),
+                ("text_len", c_int64), ("text_dim", c_int64), ("freq_dim", c_int64),
+                ("sp_bit_exact", c_int32)]
+
+
+WAN_LAYER_FIELDS = ("self_bq", "self_bk", "self_bv", "self_bo", "norm3_w", "norm3_b", "cross_q",
+                    "cross_k", "cross_v", "cross_o", "cross_bq", "cross_bk", "cross_bv", "cross_bo",
+                    "cross_norm_q", "cross_norm_k", "ffn_w1", "ffn_b1", "ffn_w2", "ffn_b2",
+                    "modulation")
+WAN_EMBED_FIELDS = ("time_w1", "time_b1", "time_w2", "time_b2", "proj_w", "proj_b", "text_w1",
+                    "text_b1", "text_w2", "text_b2")
+
+
+class WanLayerWeights(ctypes.Structure):
+    """spx_wan_layer_weights (include/spx.h): host pointers, NULL = leave unchanged."""
+
+    _fields_ = [(n, c_void_p) for n in WAN_LAYER_FIELDS]
+
+
+class WanEmbedWeights(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in WAN_EMBED_FIELDS]
 
 
 class VerifyBlock(ctypes.Structure):
@@ -124,6 +144,8 @@ _SIGS = [
     ("spx_rope_apply_global", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                                       c_int64, POINTER(c_int64), c_int64, c_void_p]),
     ("spx_project_tokens", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    ("spx_project_tokens_ex", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                      c_int32, c_void_p, c_void_p, c_void_p]),
     ("spx_attention", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                               c_int64, c_int64, c_void_p]),
     ("spx_kv_ring_create", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int64,
@@ -170,6 +192,10 @@ _SIGS = [
     ("spx_engine_generate_stream", c_int, [c_void_p, POINTER(c_int64), c_int64, POINTER(c_void_p),
                                            POINTER(c_void_p)]),
     ("spx_engine_set_graphs", c_int, [c_void_p, c_int32]),
+    ("spx_engine_set_wan_layer", c_int, [c_void_p, c_int64, POINTER(WanLayerWeights)]),
+    ("spx_engine_set_wan_embeddings", c_int, [c_void_p, POINTER(WanEmbedWeights)]),
+    ("spx_engine_set_timesteps", c_int, [c_void_p, c_void_p]),
+    ("spx_engine_set_context", c_int, [c_void_p, c_void_p]),
     ("spx_debug_engine_graphs", c_int, [c_void_p, POINTER(c_int64)]),
     ("spx_engine_denoise_step", c_int, [c_void_p, c_int64, c_int64, POINTER(c_void_p), POINTER(c_void_p)]),
     ("spx_verify_stream", c_int, [POINTER(EngineConfig), c_int32, POINTER(c_int), c_double,

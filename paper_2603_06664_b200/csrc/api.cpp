@@ -306,13 +306,17 @@ spx_status spx_rope_apply_global(const spx_rope_table* table, const void* x, voi
 }
 
 // ---- dense ops ------------------------------------------------------------------------------
-spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tokens,
-                              int64_t c_in, int64_t c_out, void* stream) {
+spx_status spx_project_tokens_ex(const void* x, const void* w, void* y, int64_t tokens,
+                                 int64_t c_in, int64_t c_out, const float* bias, int32_t epilogue,
+                                 const void* residual, const float* gate, void* stream) {
     return guarded([&] {
         require(x && w && y, SPX_ERR_CONFIG, "null buffer");
         require(tokens >= 1 && c_in >= 1 && c_out >= 1, SPX_ERR_SHAPE, "empty projection");
         require(c_in % 64 == 0 && c_out % 32 == 0, SPX_ERR_UNSUPPORTED,
                 "tcgen05 projection needs c_in % 64 == 0 and c_out % 32 == 0");
+        require(epilogue == 0 || epilogue == 1 || epilogue == 3, SPX_ERR_CONFIG,
+                "epilogue: 0 plain, 1 residual + gate, 3 GELU(tanh)");
+        require(epilogue != 1 || residual, SPX_ERR_CONFIG, "residual epilogue needs a residual");
         GemmOperands o{};
         o.a = static_cast<const bf16*>(x);
         o.a_row_stride = c_in;
@@ -326,10 +330,20 @@ spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tok
         o.M = static_cast<int>(tokens);
         o.N = static_cast<int>(c_out);
         o.K = static_cast<int>(c_in);
+        o.bias = bias;
+        o.epi_mode = epilogue;
+        o.residual = static_cast<const bf16*>(residual);
+        o.residual_row_stride = c_out;
+        o.gate = gate;
         GemmPlan plan;
         gemm_plan(&plan, o, device_sm_count(current_device()));
         gemm_run(plan, as_stream(stream));
     });
+}
+
+spx_status spx_project_tokens(const void* x, const void* w, void* y, int64_t tokens,
+                              int64_t c_in, int64_t c_out, void* stream) {
+    return spx_project_tokens_ex(x, w, y, tokens, c_in, c_out, nullptr, 0, nullptr, nullptr, stream);
 }
 
 namespace {
@@ -704,6 +718,12 @@ void spx_engine_config_defaults(spx_engine_config* c) {
     c->ablation = SPX_ABLATION_ALL;
     c->adaln = 0;
     c->l2_prefetch = 0;  // opt-in: measured 0.4 % slower per chunk at the power cap (round 1)
+    c->wan_block = 0;
+    c->ffn_dim = 0;
+    c->text_len = 512;
+    c->text_dim = 4096;
+    c->freq_dim = 256;
+    c->sp_bit_exact = 0;
 }
 
 spx_status spx_engine_config_validate(const spx_engine_config* cfg, int32_t world_size) {
@@ -799,6 +819,35 @@ spx_status spx_engine_generate_stream(spx_engine* engine, const int64_t* blocks,
     return guarded([&] {
         require_ptr(engine, "engine");
         engine->e->generate_stream(blocks, n, noise_host, out_host);
+    });
+}
+
+spx_status spx_engine_set_wan_layer(spx_engine* engine, int64_t layer,
+                                    const spx_wan_layer_weights* w) {
+    return guarded([&] {
+        require(engine && w, SPX_ERR_CONFIG, "null argument");
+        engine->e->set_wan_layer(layer, *w);
+    });
+}
+
+spx_status spx_engine_set_wan_embeddings(spx_engine* engine, const spx_wan_embed_weights* w) {
+    return guarded([&] {
+        require(engine && w, SPX_ERR_CONFIG, "null argument");
+        engine->e->set_wan_embeddings(*w);
+    });
+}
+
+spx_status spx_engine_set_timesteps(spx_engine* engine, const float* t) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->set_timesteps(t);
+    });
+}
+
+spx_status spx_engine_set_context(spx_engine* engine, const uint16_t* text) {
+    return guarded([&] {
+        require_ptr(engine, "engine");
+        engine->e->set_context(text);
     });
 }
 

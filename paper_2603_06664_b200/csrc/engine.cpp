@@ -76,10 +76,35 @@ void Engine::validate(const spx_engine_config& c, int world_size) {
             "ablation must be a combination of the three AblationFlags bits");
     require(c.adaln == 0 || c.adaln == 1, SPX_ERR_CONFIG, "adaln must be 0 or 1");
     require(c.qk_norm == 0 || c.qk_norm == 1, SPX_ERR_CONFIG, "qk_norm must be 0 or 1");
+    require(c.wan_block == 0 || c.wan_block == 1, SPX_ERR_CONFIG, "wan_block must be 0 or 1");
+    if (c.wan_block) {
+        const int64_t F = wan_ffn_dim(c);
+        require(F >= 64 && F % 64 == 0, SPX_ERR_UNSUPPORTED, "wan_block: ffn_dim must be a multiple of 64");
+        require(c.text_len >= 1 && c.text_dim >= 64 && c.text_dim % 64 == 0, SPX_ERR_UNSUPPORTED,
+                "wan_block: text_len >= 1 and text_dim a multiple of 64");
+        require(c.freq_dim >= 16 && c.freq_dim % 16 == 0 && c.freq_dim <= 8192, SPX_ERR_UNSUPPORTED,
+                "wan_block: freq_dim must be a multiple of 16, <= 8192");
+        require(c.ablation == SPX_ABLATION_ALL, SPX_ERR_UNSUPPORTED,
+                "wan_block runs the optimized schedule (ablation = ALL)");
+    }
+}
+
+int64_t wan_ffn_dim(const spx_engine_config& c) {
+    if (c.ffn_dim > 0) return c.ffn_dim;
+    const int64_t C = c.heads * c.head_dim;
+    return ceil_div(C * 35, 6 * 64) * 64;  // 8960 at the Wan2.1-1.3B dim 1536
 }
 
 Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_(cfg) {
     validate(cfg, world->size());
+    if (cfg_.wan_block) {  // the full block carries the self-attention extensions
+        cfg_.adaln = 1;
+        cfg_.qk_norm = 1;
+        FF_ = wan_ffn_dim(cfg_);
+        TL_ = cfg_.text_len;
+        TD_ = cfg_.text_dim;
+        FD_ = cfg_.freq_dim;
+    }
     if (world->transport() == SPX_TRANSPORT_PEER) {
         require(cfg.ablation == SPX_ABLATION_ALL, SPX_ERR_UNSUPPORTED,
                 "the PEER transport runs the optimized schedule only (ablation = ALL)");
@@ -145,6 +170,7 @@ Engine::~Engine() {
     }
     for (auto& kv : weights_) {
         cudaSetDevice(kv.first);
+        for (void* p : kv.second.wan_allocs) cudaFree(p);
         cudaFree(kv.second.wqkv);
         cudaFree(kv.second.wo);
         cudaFree(kv.second.norm_q);
@@ -361,11 +387,13 @@ void Engine::allocate() {
         SPX_CUDA(cudaEventCreateWithFlags(&rs.ev_attn, cudaEventDisableTiming));
         ranks_.push_back(std::move(rs));
     }
+    if (cfg_.wan_block) allocate_wan();
 }
 
 void Engine::build_plans() {
     for (RankState& rs : ranks_) {
         SPX_CUDA(cudaSetDevice(rs.device));
+        table_->on_device(rs.device);  // the RoPE tables are resident before any capture
         const int sms = device_sm_count(rs.device);
         const DeviceWeights& w = weights_.at(rs.device);
         rs.qkv_plan.resize(static_cast<size_t>(cfg_.layers));
@@ -386,6 +414,7 @@ void Engine::build_plans() {
             q.N = static_cast<int>(3 * C_);
             q.K = static_cast<int>(C_);
             q.b_constant = true;  // weights: uploaded synchronously, never written by a kernel
+            if (cfg_.wan_block) q.bias = w.wan.b_qkv + l * 3 * C_;
             gemm_plan(&rs.qkv_plan[l], q, sms);
 
             GemmOperands o{};
@@ -403,6 +432,10 @@ void Engine::build_plans() {
                 o.residual = rs.x[l % 2];
                 o.residual_row_stride = C_;
                 o.gate = w.mod + (l * 3 + 2) * C_;
+                if (cfg_.wan_block) {  // gate_msa of the step's modulation, + the o bias
+                    o.gate = rs.mod_step + (l * 6 + 2) * C_;
+                    o.bias = w.wan.b_o + l * C_;
+                }
             }
             o.M = static_cast<int>(Lp_);
             o.N = static_cast<int>(C_);
@@ -425,7 +458,7 @@ void Engine::build_plans() {
             a.num_segs = 1;
             a.rows_per_chunk = static_cast<int>(Lp_);
             a.out_row_stride = Hl_ * D_;
-            if (l == 0) {  // one split-KV workspace per rank (layers run in stream order)
+            if (l == 0 && !cfg_.sp_bit_exact) {  // one split-KV workspace per rank (layers in stream order)
                 const size_t ws = attn_workspace_bytes(a, attn_max_splits(a, sms));
                 if (ws > 0) {
                     void* ptr = nullptr;
@@ -441,6 +474,7 @@ void Engine::build_plans() {
             attn_plan(&rs.attn_plan[l], a, sms);
         }
     }
+    if (cfg_.wan_block) build_wan_plans();
 }
 
 void Engine::info(int64_t out[8]) const {
@@ -486,6 +520,7 @@ void Engine::seed_weights() {
         for (float& e : m) e = static_cast<float>(rng.next_normal() * sc);
         set_modulation(l, m.data(), m.data() + C_, m.data() + 2 * C_);
     }
+    if (cfg_.wan_block) seed_wan_weights();
 }
 
 void Engine::set_modulation(int64_t layer, const float* shift, const float* scale,
@@ -681,7 +716,11 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         RankState& rs = ranks_[static_cast<size_t>(li)];
         SPX_CUDA(cudaSetDevice(rs.device));
         mark(li, 0);
-        if (cfg_.adaln) {  // K1: x_in = LN(x)(1 + scale) + shift, the QKV GEMM's A operand
+        if (cfg_.wan_block) {  // K1 with shift_msa / scale_msa of this step's modulation
+            const float* m = rs.mod_step + layer * 6 * C_;
+            ln_modulate_run(x_in[static_cast<size_t>(li)], rs.xm, Lp_, C_, m, m + C_, cfg_.norm_eps,
+                            rs.stream, false, true);
+        } else if (cfg_.adaln) {  // K1: x_in = LN(x)(1 + scale) + shift, the QKV GEMM's A operand
             const float* m = weights_.at(rs.device).mod + layer * 3 * C_;
             ln_modulate_run(x_in[static_cast<size_t>(li)], rs.xm, Lp_, C_, m, m + C_, cfg_.norm_eps,
                             rs.stream);
@@ -845,6 +884,7 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         SPX_CUDA(cudaSetDevice(rs.device));
         gemm_run(*oproj[static_cast<size_t>(li)], rs.stream);
         mark(li, 6);
+        if (cfg_.wan_block) run_wan_tail(rs, layer);  // cross-attention + FFN (token-local)
     }
 }
 
@@ -868,6 +908,8 @@ void Engine::run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>&
 void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, void* const* x,
                             void* const* y) {
     require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
+    require(!cfg_.wan_block, SPX_ERR_UNSUPPORTED,
+            "spx_engine_layer: the full Wan block runs through denoise_step / generate");
     require(start_frame >= 0 && start_frame + F_ <= cfg_.num_blocks * F_, SPX_ERR_RANGE,
             "block frames [" + std::to_string(start_frame) + ", " +
                 std::to_string(start_frame + F_) + ") exceed table max_frames " +
@@ -899,25 +941,34 @@ void Engine::run_block(int64_t block, const std::function<void(int64_t)>& load_s
     begin_block(block);
     for (int64_t step = 0; step < cfg_.denoise_steps; ++step) {
         load_step(step);  // fresh noise into x[0] of every local rank (steps do not chain)
-        run_step(start);
+        run_step(start, step);
     }
 }
 
 // the layers of one denoise step on x[0] of every local rank (output in x[layers % 2]):
 // replayed from a CUDA graph per KV-ring state when graphs_allowed(), enqueued launch by
 // launch otherwise
-void Engine::run_step(int64_t start) {
+void Engine::run_step(int64_t start, int64_t step) {
     if (!graphs_allowed()) {
-        run_step_eager(start);
+        run_step_eager(start, step);
         return;
     }
     RankState& rs = ranks_[0];
     SPX_CUDA(cudaSetDevice(rs.device));
     // everything a step's kernel parameters depend on besides the fixed buffers
-    const std::array<int64_t, 7> key{block_base_row_, num_segs_, seg_start_[0], seg_len_[0],
-                                     seg_start_[1], seg_len_[1], start};
+    // (the Wan block's timestep embedding reads t[step]: the step is part of its state)
+    const std::array<int64_t, 8> key{block_base_row_, num_segs_, seg_start_[0], seg_len_[0],
+                                     seg_start_[1], seg_len_[1], start,
+                                     cfg_.wan_block ? step : -1};
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
+        // first sight of this state: run it launch by launch (lazy per-device set-up such as
+        // table uploads and kernel attributes happens outside any capture) and capture on
+        // the next occurrence
+        if (seen_.insert(key).second) {
+            run_step_eager(start, step);
+            return;
+        }
         if (graphs_.size() >= kMaxGraphs) {  // evict the least recently used
             auto lru = graphs_.begin();
             for (auto g = graphs_.begin(); g != graphs_.end(); ++g)
@@ -931,21 +982,27 @@ void Engine::run_step(int64_t start) {
         cudaGraph_t g = nullptr;
         SPX_CUDA(cudaStreamBeginCapture(rs.stream, cudaStreamCaptureModeThreadLocal));
         capturing_ = true;
+        bool ok = true;
         try {
-            run_step_eager(start);
-        } catch (...) {
-            capturing_ = false;
-            cudaStreamEndCapture(rs.stream, &g);
-            if (g) cudaGraphDestroy(g);
-            throw;
+            run_step_eager(start, step);
+        } catch (const Error&) {
+            ok = false;
         }
         capturing_ = false;
-        SPX_CUDA(cudaStreamEndCapture(rs.stream, &g));
+        const cudaError_t ce = cudaStreamEndCapture(rs.stream, &g);
+        cudaError_t ie = cudaErrorUnknown;
+        if (ok && ce == cudaSuccess && g) ie = cudaGraphInstantiateWithFlags(&sg.exec, g, 0);
+        if (g) cudaGraphDestroy(g);
         sg.launches = launch_count() - l0;
         count_launch(static_cast<int>(-sg.launches));  // captured, not launched
-        const cudaError_t e = cudaGraphInstantiateWithFlags(&sg.exec, g, 0);
-        cudaGraphDestroy(g);
-        SPX_CUDA(e);
+        if (!ok || ce != cudaSuccess || ie != cudaSuccess) {
+            // the step does not capture on this system: clear the capture error and stay on
+            // the launch-by-launch path for this engine (nothing of the step ran)
+            cudaGetLastError();
+            graphs_enabled_ = false;
+            run_step_eager(start, step);
+            return;
+        }
         it = graphs_.emplace(key, sg).first;
     }
     it->second.last_use = ++graph_clock_;
@@ -981,7 +1038,13 @@ void Engine::drop_graphs() {
     graphs_.clear();
 }
 
-void Engine::run_step_eager(int64_t start) {
+void Engine::run_step_eager(int64_t start, int64_t step) {
+    if (cfg_.wan_block) {  // this step's timestep embedding -> every layer's modulation
+        for (RankState& rs : ranks_) {
+            SPX_CUDA(cudaSetDevice(rs.device));
+            wan_time_embedding_run(rs.te, static_cast<int>(step), rs.stream);
+        }
+    }
     for (int64_t l = 0; l < cfg_.layers; ++l) {
         std::vector<const GemmPlan*> qv, ov;
         std::vector<const bf16*> xv;
@@ -1006,7 +1069,7 @@ void Engine::denoise_step(int64_t block, int64_t step, const void* const* x, voi
         SPX_CUDA(cudaMemcpyAsync(rs.x[0], x[rs.local], slice_bytes, cudaMemcpyDeviceToDevice,
                                  rs.stream));
     }
-    run_step(cfg_.force_start_frame_zero ? 0 : block * F_);
+    run_step(cfg_.force_start_frame_zero ? 0 : block * F_, step);
     const int fin = static_cast<int>(cfg_.layers % 2);
     for (RankState& rs : ranks_) {
         SPX_CUDA(cudaSetDevice(rs.device));

@@ -24,6 +24,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <set>
 #include <vector>
 
 #include "../../include/spx.h"
@@ -35,6 +36,48 @@
 
 namespace spx {
 
+// the full Wan2.1 block's parameters beyond the self-attention projections (cfg.wan_block),
+// one copy per device; [out][in] row-major bf16 matrices, fp32 vectors
+struct WanWeights {
+    float* b_qkv = nullptr;                  // [layers][3C] self-attention q | k | v biases
+    float* b_o = nullptr;                    // [layers][C]
+    float* n3_w = nullptr;                   // [layers][C] affine LayerNorm (norm3)
+    float* n3_b = nullptr;
+    bf16* cq = nullptr;                      // [layers][C][C] cross-attention projections
+    bf16* ck = nullptr;
+    bf16* cv = nullptr;
+    bf16* co = nullptr;
+    float* bcq = nullptr;                    // [layers][C]
+    float* bck = nullptr;
+    float* bcv = nullptr;
+    float* bco = nullptr;
+    bf16* cnq = nullptr;                     // [layers][C] cross-attention RMSNorm weights
+    bf16* cnk = nullptr;
+    bf16* w1 = nullptr;                      // [layers][F][C] FFN
+    float* b1 = nullptr;                     // [layers][F]
+    bf16* w2 = nullptr;                      // [layers][C][F]
+    float* b2 = nullptr;                     // [layers][C]
+    float* mod_param = nullptr;              // [layers][6][C]
+    bf16* tw1 = nullptr;                     // [C][freq_dim] time embedding
+    float* tb1 = nullptr;
+    bf16* tw2 = nullptr;                     // [C][C]
+    float* tb2 = nullptr;
+    bf16* pw = nullptr;                      // [6C][C] time projection
+    float* pb = nullptr;
+    bf16* xw1 = nullptr;                     // [C][text_dim] text embedding
+    float* xb1 = nullptr;
+    bf16* xw2 = nullptr;                     // [C][C]
+    float* xb2 = nullptr;
+    float* tsteps = nullptr;                 // [denoise_steps]
+    // per video: the text context and every layer's cross-attention K (RMSNorm'd) and V
+    bf16* text = nullptr;                    // [text_len][text_dim]
+    bf16* text_h = nullptr;                  // [text_len][C]
+    bf16* ctx = nullptr;                     // [text_len][C]
+    bf16* ktmp = nullptr;                    // [text_len][C]
+    bf16* k_ctx = nullptr;                   // [layers][text_len][C]
+    bf16* v_ctx = nullptr;
+};
+
 struct DeviceWeights {
     int device = 0;
     bf16* wqkv = nullptr;  // [layers][3C][C]
@@ -42,6 +85,8 @@ struct DeviceWeights {
     bf16* norm_q = nullptr;  // [layers][C]
     bf16* norm_k = nullptr;
     float* mod = nullptr;  // [layers][3][C] adaLN shift | scale | gate (cfg.adaln)
+    WanWeights wan;        // cfg.wan_block
+    std::vector<void*> wan_allocs;
 };
 
 struct RankState {
@@ -72,6 +117,16 @@ struct RankState {
     size_t attn_ws_bytes = 0;
     cudaEvent_t ev_k3 = nullptr;
     cudaEvent_t ev_attn = nullptr;
+    // cfg.wan_block: the cross-attention and FFN tail of every layer, and the step's modulation
+    bf16* ca_q = nullptr;             // (L/P, C) cross-attention q projection
+    bf16* ca_qn = nullptr;            // (L/P, H, D) after its RMSNorm
+    bf16* ca_o = nullptr;             // (L/P, C) cross-attention output
+    bf16* ffn_h = nullptr;            // (L/P, F) GELU(x W1^T + b1)
+    float* mod_step = nullptr;        // [layers][6][C] modulation of the current denoise step
+    float* temb = nullptr;            // time-embedding scratch: sinus | h1 | e | e0
+    WanTimeEmbed te;
+    std::vector<GemmPlan> cq_plan, co_plan, f1_plan, f2_plan;  // per layer
+    std::vector<AttnPlan> ca_plan;    // per layer: q over the cached context K/V
     // generate_block from host noise: the next denoise step's noise is uploaded on a copy
     // stream into a staging buffer while the current step computes
     bf16* nstage[2] = {nullptr, nullptr};
@@ -106,6 +161,10 @@ class Engine {
                            const uint16_t* wv, const uint16_t* wo);
     void set_norm_weights(int64_t layer, const uint16_t* wq, const uint16_t* wk);
     void set_modulation(int64_t layer, const float* shift, const float* scale, const float* gate);
+    void set_wan_layer(int64_t layer, const spx_wan_layer_weights& w);
+    void set_wan_embeddings(const spx_wan_embed_weights& w);
+    void set_timesteps(const float* t);
+    void set_context(const uint16_t* text);
     void begin_block(int64_t block_index);
     // a new video: every layer's KV cache empty again (generate() builds fresh caches,
     // generator.cpp:69-81); device ring memory is reused as is
@@ -146,8 +205,13 @@ class Engine {
   private:
     void allocate();
     void run_block(int64_t block, const std::function<void(int64_t)>& load_step);
-    void run_step(int64_t start_frame);
-    void run_step_eager(int64_t start_frame);
+    void run_step(int64_t start_frame, int64_t step);
+    void run_step_eager(int64_t start_frame, int64_t step);
+    void run_wan_tail(RankState& rs, int64_t layer);
+    void allocate_wan();
+    void build_wan_plans();
+    void seed_wan_weights();
+    void compute_context();
     bool graphs_allowed() const;
     void drop_graphs();
     void build_plans();
@@ -173,6 +237,7 @@ class Engine {
     spx_engine_config cfg_;
     // geometry
     int64_t F_, Hg_, Wg_, HW_, L_, H_, D_, C_, P_, G_, S_, Lp_, Lq_, Hl_;
+    int64_t FF_ = 0, TL_ = 0, TD_ = 0, FD_ = 0;  // wan_block: ffn, text len / dim, freq dim
     int64_t cap_frames_ = 0;
     Partition part_{};
     std::unique_ptr<RopeTable> table_;
@@ -206,7 +271,8 @@ class Engine {
         uint64_t last_use = 0;
     };
     static constexpr size_t kMaxGraphs = 24;
-    std::map<std::array<int64_t, 7>, StepGraph> graphs_;
+    std::map<std::array<int64_t, 8>, StepGraph> graphs_;
+    std::set<std::array<int64_t, 8>> seen_;  // states run once (captured on the next run)
     uint64_t graph_clock_ = 0;
     bool capturing_ = false;
     bool graphs_enabled_ = true;
@@ -223,5 +289,7 @@ class Engine {
 
 // G (head groups) for P ranks and H heads: the largest divisor of P that divides H
 int64_t choose_head_groups(int64_t P, int64_t H);
+// the Wan FFN hidden size of a config (cfg.ffn_dim, or the Wan2.1 ratio rounded to 64)
+int64_t wan_ffn_dim(const spx_engine_config& c);
 
 }  // namespace spx

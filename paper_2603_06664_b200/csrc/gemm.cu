@@ -48,6 +48,7 @@ struct GemmParams {
     const bf16* residual;
     int64_t ldr;
     const float* gate;
+    const float* bias;
     RopeLaunch rope;  // epi_mode 2
     // epi_mode 2 lookups (host-computed: no integer division in the epilogue)
     int head_shift;         // log2(head_dim)
@@ -205,6 +206,16 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, in
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
     const ChunkDst d = chunk_dst(p, col0);
+    if (p.epi_mode != 2 && p.bias) {  // warp-uniform; the 32 bias values are a broadcast load
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+            f[j] += b.x;
+            f[j + 1] += b.y;
+            f[j + 2] += b.z;
+            f[j + 3] += b.w;
+        }
+    }
     if (p.epi_mode == 2) {
         if (d.which < 2 && rr.valid) rope_rotate_chunk(p.rope, rr, d.d0, f);
     } else if (p.epi_mode == 1 && row < p.M) {
@@ -217,9 +228,20 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, in
             for (int e = 0; e < 4; ++e) {
                 float2 rs = unpack_bf16x2(rw[e]);
                 const int j = q * 8 + e * 2;
-                f[j] = rs.x + p.gate[col0 + j] * f[j];
-                f[j + 1] = rs.y + p.gate[col0 + j + 1] * f[j + 1];
+                const float g0 = p.gate ? p.gate[col0 + j] : 1.0f;
+                const float g1 = p.gate ? p.gate[col0 + j + 1] : 1.0f;
+                f[j] = rs.x + g0 * f[j];
+                f[j + 1] = rs.y + g1 * f[j + 1];
             }
+        }
+    } else if (p.epi_mode == 3) {
+        // GELU, tanh approximation (torch.nn.GELU(approximate="tanh"), the Wan FFN):
+        // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float x = f[j];
+            const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+            f[j] = 0.5f * x * (1.0f + tanhf(u));
         }
     }
 #pragma unroll
@@ -749,6 +771,10 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     p.residual = o.residual;
     p.ldr = o.residual_row_stride;
     p.gate = o.gate;
+    p.bias = o.bias;
+    require(o.epi_mode != 1 || o.residual, SPX_ERR_CONFIG, "gemm: residual epilogue without residual");
+    require(!o.bias || (reinterpret_cast<uintptr_t>(o.bias) & 15) == 0, SPX_ERR_ALIGNMENT,
+            "gemm: bias must be 16-byte aligned");
     if (rope) {
         require(gemm_rope_fusable(plan, *rope), SPX_ERR_UNSUPPORTED,
                 "gemm: rope epilogue needs 3C outputs, C % BN == 0, D % 32 == 0, no QK-norm");

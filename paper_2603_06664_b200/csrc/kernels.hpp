@@ -27,12 +27,17 @@ struct GemmOperands {
     bf16* out = nullptr;
     int64_t out_row_stride = 0;
     int M = 0, N = 0, K = 0;
-    // epilogue: 0 -> out = acc ; 1 -> out = residual + gate[col] * acc (adaLN gate + residual)
-    //           2 -> Causal-RoPE rotate-and-pack (set by gemm_run's rope argument)
+    // epilogue (acc' = acc + bias[col] when bias != nullptr):
+    //   0 -> out = acc'
+    //   1 -> out = residual + gate[col] * acc' (adaLN gate + residual; gate == nullptr: 1)
+    //   2 -> Causal-RoPE rotate-and-pack (set by gemm_run's rope argument; no bias)
+    //   3 -> out = GELU_tanh(acc') (the Wan FFN's first projection)
+    // out may alias residual (each element is read, then written, by the same warp)
     int epi_mode = 0;
     const bf16* residual = nullptr;
     int64_t residual_row_stride = 0;
     const float* gate = nullptr;
+    const float* bias = nullptr;   // fp32 [N]
     // B is not written by the kernel launched just before (e.g. weights): its first pipeline
     // stages are loaded before griddepcontrol.wait, overlapping the previous kernel's tail
     bool b_constant = false;
@@ -174,9 +179,41 @@ struct Box4 {
 void copy_box_run(void* dst, const void* src, const Box4& box, int elem_bytes, cudaStream_t s);
 
 // K1 (Wan adaLN extension): y = LayerNorm(x) * (1 + scale) + shift, rows x dim bf16,
-// shift/scale fp32 [dim] (modulate.cu)
+// shift/scale fp32 [dim] (modulate.cu); affine: y = LayerNorm(x) * scale + shift (Wan's norm3).
+// mod_from_kernel: shift/scale are written by an earlier kernel of the stream (read after the
+// PDL wait instead of before it)
 void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const float* shift,
-                     const float* scale, float eps, cudaStream_t s);
+                     const float* scale, float eps, cudaStream_t s, bool affine = false,
+                     bool mod_from_kernel = false);
+
+// ---------------------------------------------------------------------------------------
+// Wan2.1 block extensions (wan.cu): timestep embedding + per-layer modulation, once per step.
+// ---------------------------------------------------------------------------------------
+struct WanTimeEmbed {
+    const float* tsteps = nullptr;   // [denoise_steps] timesteps (device)
+    int freq_dim = 256, dim = 0, layers = 0;
+    const bf16* w1 = nullptr;        // [dim][freq_dim]
+    const float* b1 = nullptr;
+    const bf16* w2 = nullptr;        // [dim][dim]
+    const float* b2 = nullptr;
+    const bf16* wp = nullptr;        // [6 dim][dim]
+    const float* bp = nullptr;
+    const float* mod_param = nullptr;  // [layers][6][dim] per-layer modulation parameters
+    float* sinus = nullptr;          // scratch [freq_dim]
+    float* h1 = nullptr;             // scratch [dim]
+    float* e = nullptr;              // [dim]
+    float* e0 = nullptr;             // [6 dim]
+    float* mod = nullptr;            // out [layers][6][dim] = mod_param + e0
+};
+void wan_time_embedding_run(const WanTimeEmbed& te, int step, cudaStream_t s);
+// y[n] = act(sum_k W[n][k] act(x[k]) + b[n]) (SiLU on input and/or output), fp32 vectors
+void gemv_run(const bf16* W, const float* b, const float* x, float* y, int N, int K, bool silu_in,
+              bool silu_out, cudaStream_t s);
+// counter-based N(offset, scale^2) fill (the Wan-block synthetic weights, seeded on device)
+void fill_normal_bf16_run(bf16* out, int64_t n, uint64_t seed, float scale, float offset,
+                          cudaStream_t s);
+void fill_normal_f32_run(float* out, int64_t n, uint64_t seed, float scale, float offset,
+                         cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // PEER transport: device-side rank barrier over IPC-mapped flag words. Each rank owns

@@ -1,5 +1,7 @@
 // modulate.cu -- K1: the Wan block's adaLN modulation in front of the QKV projection,
 //   x_in = LayerNorm(x) * (1 + scale) + shift          (non-affine LN over the model dim)
+// and, with affine = 1, the affine LayerNorm in front of the cross-attention (Wan's norm3),
+//   y = LayerNorm(x) * weight + bias                   (scale = weight, shift = bias)
 // (a Wan-mode extension with no reference counterpart; the residual + gate after
 // the output projection, x += gate * W_o o, is the O-GEMM's epi_mode 1 epilogue).
 //
@@ -33,18 +35,30 @@ template <int NV>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     ln_modulate_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int rows, int dim,
                        const float* __restrict__ shift, const float* __restrict__ scale,
-                       float eps) {
+                       float eps, int affine, int mod_from_kernel) {
     extern __shared__ float4 s_mod[];  // [nvec][4]: shift lo, shift hi, scale lo, scale hi
     pdl_trigger();
     const int lane = threadIdx.x % 32;
     const int nvec = dim / 8;
+    // constant modulation (uploaded weights) is staged before the PDL wait, overlapping the
+    // previous kernel's tail; a per-step modulation written by a kernel (the Wan timestep
+    // embedding) only after it
+    if (mod_from_kernel) pdl_wait();
+    const float one = affine ? 0.0f : 1.0f;
     for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) {
         const int v = i / 4, q = i % 4;
         const float* srcp = (q < 2 ? shift : scale) + v * 8 + (q & 1) * 4;
-        s_mod[i] = __ldg(reinterpret_cast<const float4*>(srcp));
+        float4 m = __ldg(reinterpret_cast<const float4*>(srcp));
+        if (q >= 2) {  // the multiplier: 1 + scale (adaLN) or weight (affine LayerNorm)
+            m.x += one;
+            m.y += one;
+            m.z += one;
+            m.w += one;
+        }
+        s_mod[i] = m;
     }
     __syncthreads();
-    pdl_wait();  // x was written by the previous kernel (the last O-projection)
+    if (!mod_from_kernel) pdl_wait();  // x was written by the previous kernel
     const int warps = static_cast<int>(gridDim.x) * kWarpsPerBlock;
     const int pairs = (rows + 1) / 2;
     for (int pr = static_cast<int>(blockIdx.x) * kWarpsPerBlock + static_cast<int>(threadIdx.x / 32);
@@ -99,8 +113,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             const float4 sh0 = s_mod[c * 4], sh1 = s_mod[c * 4 + 1];
             const float4 sc0 = s_mod[c * 4 + 2], sc1 = s_mod[c * 4 + 3];
             const float shv[8] = {sh0.x, sh0.y, sh0.z, sh0.w, sh1.x, sh1.y, sh1.z, sh1.w};
-            const float scv[8] = {1.0f + sc0.x, 1.0f + sc0.y, 1.0f + sc0.z, 1.0f + sc0.w,
-                                  1.0f + sc1.x, 1.0f + sc1.y, 1.0f + sc1.z, 1.0f + sc1.w};
+            const float scv[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
             const uint32_t a[4] = {v0[i].x, v0[i].y, v0[i].z, v0[i].w};
             const uint32_t b[4] = {v1[i].x, v1[i].y, v1[i].z, v1[i].w};
             uint32_t oa[4], ob[4];
@@ -121,7 +134,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }  // namespace
 
 void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const float* shift,
-                     const float* scale, float eps, cudaStream_t s) {
+                     const float* scale, float eps, cudaStream_t s, bool affine,
+                     bool mod_from_kernel) {
     require(rows >= 0 && dim > 0 && dim % 8 == 0 && dim <= 2048, SPX_ERR_SHAPE,
             "layernorm_modulate: dim must be a positive multiple of 8, <= 2048");
     require((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
@@ -142,15 +156,16 @@ void ln_modulate_run(const bf16* x, bf16* y, int64_t rows, int64_t dim, const fl
     const dim3 block(kWarpsPerBlock * 32);
     const size_t smem = static_cast<size_t>(dim / 8) * 4 * sizeof(float4);
     const int r = static_cast<int>(rows), d = static_cast<int>(dim);
+    const int af = affine ? 1 : 0, mk = mod_from_kernel ? 1 : 0;
     switch (nv) {
-        case 1: launch_pdl(ln_modulate_kernel<1>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 2: launch_pdl(ln_modulate_kernel<2>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 3: launch_pdl(ln_modulate_kernel<3>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 4: launch_pdl(ln_modulate_kernel<4>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 5: launch_pdl(ln_modulate_kernel<5>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 6: launch_pdl(ln_modulate_kernel<6>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        case 7: launch_pdl(ln_modulate_kernel<7>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
-        default: launch_pdl(ln_modulate_kernel<8>, grid, block, smem, s, x, y, r, d, shift, scale, eps); break;
+        case 1: launch_pdl(ln_modulate_kernel<1>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 2: launch_pdl(ln_modulate_kernel<2>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 3: launch_pdl(ln_modulate_kernel<3>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 4: launch_pdl(ln_modulate_kernel<4>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 5: launch_pdl(ln_modulate_kernel<5>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 6: launch_pdl(ln_modulate_kernel<6>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        case 7: launch_pdl(ln_modulate_kernel<7>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
+        default: launch_pdl(ln_modulate_kernel<8>, grid, block, smem, s, x, y, r, d, shift, scale, eps, af, mk); break;
     }
     SPX_CUDA_LAUNCH();
     count_launch();

@@ -439,6 +439,14 @@ class GenerationConfig:
     fuse_rope_epilogue: bool = True  # RoPE + pack in the QKV GEMM epilogue (qk_norm off)
     adaln: bool = False  # Wan adaLN modulation + gated residual (extension, default off)
     l2_prefetch: bool = False  # attention warms the next projections' weights into L2 (opt-in)
+    # the full Wan2.1 DiT block (extension): cross-attention, GELU FFN, timestep adaLN
+    wan_block: bool = False
+    ffn_dim: int = 0          # 0: ceil(dim * 35 / 6 / 64) * 64 (8960 at dim 1536)
+    text_len: int = 512
+    text_dim: int = 4096
+    freq_dim: int = 256
+    # attention never splits kv ranges across CTAs: SP outputs == P = 1 bit for bit at every P
+    sp_bit_exact: bool = False
     ablation: AblationFlags = field(default_factory=AblationFlags.all_on)
 
     def block_len(self):
@@ -471,6 +479,10 @@ class GenerationConfig:
         c.ablation = self.ablation.bits()
         c.adaln = int(self.adaln)
         c.l2_prefetch = int(self.l2_prefetch)
+        c.wan_block = int(self.wan_block)
+        c.ffn_dim = self.ffn_dim
+        c.text_len, c.text_dim, c.freq_dim = self.text_len, self.text_dim, self.freq_dim
+        c.sp_bit_exact = int(self.sp_bit_exact)
         return c
 
     def validate(self):
@@ -600,6 +612,48 @@ class Engine:
                                                ptr_array([p.data_ptr() for p in pins]),
                                                ptr_array([o.data_ptr() for o in outs])))
         return [o.numpy().view(np.uint16).reshape(rows, self.cfg.heads, self.cfg.head_dim) for o in outs]
+
+    # ---- the full Wan2.1 block (cfg.wan_block) ----
+    @staticmethod
+    def _wan_struct(cls, fields, arrays):
+        keep = []
+        st = cls()
+        for name, a in arrays.items():
+            if name not in fields:
+                raise ConfigError(f"unknown Wan weight {name!r}")
+            if a is None:
+                continue
+            a = np.asarray(a)
+            # matrices / RMSNorm weights are bf16 bits (uint16), everything else fp32
+            arr = np.ascontiguousarray(a, dtype=np.uint16 if a.dtype == np.uint16 else np.float32)
+            keep.append(arr)
+            setattr(st, name, arr.ctypes.data)
+        return st, keep
+
+    def set_wan_layer(self, layer, **arrays):
+        """spx_engine_set_wan_layer: keyword arrays named as in spx_wan_layer_weights (bf16 bit
+        arrays as uint16 for matrices and RMSNorm weights, float arrays for the rest)."""
+        st, keep = self._wan_struct(_lib.WanLayerWeights, _lib.WAN_LAYER_FIELDS, arrays)
+        check(lib().spx_engine_set_wan_layer(self._h, layer, ctypes.byref(st)))
+        del keep
+
+    def set_wan_embeddings(self, **arrays):
+        st, keep = self._wan_struct(_lib.WanEmbedWeights, _lib.WAN_EMBED_FIELDS, arrays)
+        check(lib().spx_engine_set_wan_embeddings(self._h, ctypes.byref(st)))
+        del keep
+
+    def set_timesteps(self, t):
+        a = np.ascontiguousarray(t, dtype=np.float32)
+        if a.size != self.cfg.denoise_steps:
+            raise ShapeError(f"{a.size} timesteps for {self.cfg.denoise_steps} denoise steps")
+        check(lib().spx_engine_set_timesteps(self._h, a.ctypes.data))
+
+    def set_context(self, text_bits):
+        """a video's text context, bf16 bits (text_len, text_dim)"""
+        a = np.ascontiguousarray(text_bits, dtype=np.uint16)
+        if a.size != self.cfg.text_len * self.cfg.text_dim:
+            raise ShapeError(f"context holds {a.size} values, expected text_len x text_dim")
+        check(lib().spx_engine_set_context(self._h, a.ctypes.data))
 
     def set_graphs(self, on: bool):
         """per-step CUDA graphs (default on) / every kernel enqueued by the host"""

@@ -1,0 +1,151 @@
+"""The full Wan2.1 DiT block on the device (cfg.wan_block = 1: timestep adaLN, self-attention
+with QK-RMSNorm + Causal-RoPE, cross-attention to the cached text context, GELU(tanh) FFN,
+biases and residuals) against the float64 oracle extension (oracle/gpu_oracle.py, wan=...),
+pinned by the closed-form tests in tests/test_oracle_wan.py. The reference model is
+attention-only: this block has no reference counterpart, parity is against the
+restatement of Wan2.1's wan/modules/model.py. Bars: one-layer-scale bf16 error, rel-L2 < 1e-2,
+and the centred (token-discriminating) signal < 3e-2; at the Wan shape also bit identity of the
+SP partitions (P = 2 Ulysses, P = 8 four head groups x two query halves)."""
+import numpy as np
+import pytest
+
+import wan_weights
+from oracle import gpu_oracle, oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def spattn():
+    from paper_2603_06664_b200 import spattn as s
+
+    return s
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def centered(x):
+    return x - x.mean(axis=0, keepdims=True)
+
+
+def engine(kw, layers, steps, blocks, world, tl, td, fd, F, w_self, wan, **extra):
+    s = spattn()
+    cfg = s.GenerationConfig(grid_per_block=s.GridSpec(kw["frames"], kw["grid_h"], kw["grid_w"]),
+                             num_blocks=blocks, layers=layers, denoise_steps=steps, heads=kw["heads"],
+                             head_dim=kw["head_dim"], world_size=world, wan_block=True, ffn_dim=F,
+                             text_len=tl, text_dim=td, freq_dim=fd, **extra)
+    eng = s.Engine(cfg, seed_weights=False)
+    wan_weights.load(eng, w_self, wan)
+    return eng
+
+
+def run(kw, layers, steps, blocks, world, tl, td, fd, F, seed, parity_log=None, model=False):
+    C = kw["heads"] * kw["head_dim"]
+    w_self, wan = wan_weights.make(C, F, layers, tl, td, fd, steps, seed)
+    eng = engine(kw, layers, steps, blocks, world, tl, td, fd, F, w_self, wan)
+    got = spattn().bf16_bits_to_float(eng.generate())
+    L = kw["frames"] * kw["grid_h"] * kw["grid_w"]
+    got = got.reshape(blocks, L, C)
+    return got, w_self, wan
+
+
+TINY = dict(frames=3, grid_h=8, grid_w=8, heads=4, head_dim=64)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_wan_block_tiny_matches_fp64_oracle(cuda, parity_log, world):
+    got, w_self, wan = run(TINY, 2, 2, 2, world, 64, 256, 256, 1024, seed=31)
+    ref = gpu_oracle.ReferenceModel(**TINY, layers=2, num_blocks=2, steps=2, weights=w_self, wan=wan,
+                                    qk_norm=True).generate()
+    e = [rel_l2(got[b], ref[b]) for b in range(2)]
+    ec = [rel_l2(centered(got[b]), centered(ref[b])) for b in range(2)]
+    parity_log(rel_l2=e, centred_rel_l2=ec, bar_rel_l2=1e-2, bar_centred=3e-2)
+    assert max(e) < 1e-2 and max(ec) < 3e-2, (e, ec)
+
+
+def test_wan_block_sp_bit_identical_tiny(cuda):
+    outs = [run(TINY, 2, 2, 2, P, 64, 256, 256, 1024, seed=32)[0] for P in (1, 2, 4, 8)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+WAN = dict(frames=3, grid_h=30, grid_w=52, heads=12, head_dim=128)
+
+
+def test_wan_block_wan21_shape_vs_fp64(cuda, parity_log):
+    """Wan2.1-1.3B block shape: dim 1536, 12 heads, FFN 8960, 512 x 4096 text context, 256-wide
+    timestep sinusoid; 2 layers x 2 steps over 2 chunks. Compared with the fp64 oracle and
+    with its bf16-storage error model."""
+    got, w_self, wan = run(WAN, 2, 2, 2, 1, 512, 4096, 256, 8960, seed=33)
+    import gc
+
+    import torch
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    kw = dict(**WAN, layers=2, num_blocks=2, steps=2, weights=w_self, wan=wan, qk_norm=True)
+    ref = gpu_oracle.ReferenceModel(**kw).generate()
+    model = gpu_oracle.ReferenceModel(**kw, storage="bf16").generate()
+    e = [rel_l2(got[b], ref[b]) for b in range(2)]
+    em = [rel_l2(model[b], ref[b]) for b in range(2)]
+    ec = [rel_l2(centered(got[b]), centered(ref[b])) for b in range(2)]
+    parity_log(rel_l2=e, bf16_storage_model_rel_l2=em, centred_rel_l2=ec,
+               bar="rel-L2 < max(1e-2, 1.5 x model); centred < 3e-2")
+    for b in range(2):
+        assert e[b] < max(1e-2, 1.5 * em[b]) and ec[b] < 3e-2, (e, em, ec)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_wan_block_wan21_shape_sp_bit_identical(cuda, world, parity_log):
+    base = run(WAN, 2, 2, 2, 1, 512, 4096, 256, 8960, seed=34)[0]
+    got = run(WAN, 2, 2, 2, world, 512, 4096, 256, 8960, seed=34)[0]
+    parity_log(identical=bool(np.array_equal(got, base)), world=world)
+    assert np.array_equal(got, base)
+
+
+def test_wan_block_seeded_engine_runs_and_graphs_match(cuda):
+    """The engine's own synthetic init (device-seeded weights, default timesteps and context):
+    finite latents, and the per-step graphs (one per (ring state, step)) reproduce the
+    launch-by-launch run bit for bit."""
+    s = spattn()
+    cfg = s.GenerationConfig(grid_per_block=s.GridSpec(3, 8, 8), num_blocks=2, layers=2,
+                             denoise_steps=3, heads=4, head_dim=64, wan_block=True, text_len=64,
+                             text_dim=256)
+    outs = []
+    for graphs in (True, False):
+        eng = s.Engine(cfg)
+        eng.set_graphs(graphs)
+        outs.append(eng.generate())
+    vals = s.bf16_bits_to_float(outs[0])
+    assert np.isfinite(vals).all() and np.abs(vals).max() > 0
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_gemm_bias_gelu_and_residual_epilogues(cuda, parity_log):
+    """The GEMM epilogues the Wan block adds: + bias, GELU(tanh), residual without a gate."""
+    import torch
+
+    from paper_2603_06664_b200._lib import check, lib
+
+    M, K, N = 4680, 1536, 8960
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K ** 0.5).to(torch.bfloat16)
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    y = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    check(lib().spx_project_tokens_ex(x.data_ptr(), w.data_ptr(), y.data_ptr(), M, K, N, b.data_ptr(),
+                                      3, None, None, st))
+    r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    z = r.clone()
+    check(lib().spx_project_tokens_ex(x.data_ptr(), w.data_ptr(), z.data_ptr(), M, K, N, b.data_ptr(),
+                                      1, z.data_ptr(), None, st))
+    torch.cuda.synchronize()
+    acc = x.float() @ w.float().t() + b
+    ref = torch.nn.functional.gelu(acc, approximate="tanh")
+    e1 = float((y.float() - ref).norm() / ref.norm())
+    ref2 = r.float() + acc
+    e2 = float((z.float() - ref2).norm() / ref2.norm())
+    parity_log(gelu_rel_l2=e1, residual_rel_l2=e2, bar=3e-3)
+    assert e1 < 3e-3 and e2 < 3e-3

@@ -136,15 +136,34 @@ def test_c5_rolling_window_ring_wraps_vs_fp64(cuda, parity_log, world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_c2_sp_bit_identical_to_p1_at_h12(cuda, world, parity_log):
-    """The reference's invariant (test_sp_attention.cpp:116-130) at the Wan shape and depth:
-    P = 2, 4 (Ulysses: 6 / 3 heads per rank) and P = 8 (4 head groups x 2 query halves, which
-    the reference itself cannot run: 12 % 8 != 0) produce the P = 1 latent bit for bit."""
+    """The reference's invariant (test_sp_attention.cpp:116-130) at the Wan shape and depth
+    (30 layers x 4 steps, 2 chunks): with sp_bit_exact the partitions P = 2, 4 (Ulysses: 6 / 3
+    heads per rank) and P = 8 (4 head groups x 2 query halves, which the reference itself
+    cannot run: 12 % 8 != 0) produce the P = 1 latents bit for bit."""
     s = spattn()
-    base = s.Engine(cfg(2, 30, 4)).generate()
+    base = s.Engine(cfg(2, 30, 4, sp_bit_exact=True)).generate()
     free_gpu()
-    got = s.Engine(cfg(2, 30, 4, world=world)).generate()
+    got = s.Engine(cfg(2, 30, 4, world=world, sp_bit_exact=True)).generate()
     parity_log(identical=bool(np.array_equal(got, base)), world=world)
     assert np.array_equal(got, base)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c2_sp_default_layout_within_bf16_of_p1(cuda, world, parity_log):
+    """The default (fast) layouts: where a rank's (query tile x head) grid under-fills the
+    148 SMs (P = 2: 222 tiles, P = 8: 57 tiles) attention splits kv ranges over CTAs, which
+    changes the fp32 summation order; the latents then agree with P = 1 to bf16 rounding
+    (north_star: activations within a stated bf16 tolerance; indices / permutations stay
+    bit-exact). P = 4 (111 tiles, unsplit) stays bit-identical."""
+    s = spattn()
+    base = s.bf16_bits_to_float(s.Engine(cfg(2, 30, 4)).generate())
+    free_gpu()
+    got = s.bf16_bits_to_float(s.Engine(cfg(2, 30, 4, world=world)).generate())
+    e = [rel_l2(got[b], base[b]) for b in range(2)]
+    parity_log(rel_l2_vs_p1=e, identical=bool(np.array_equal(got, base)), world=world, bar=1e-2)
+    assert max(e) < 1e-2
+    if world == 4:
+        assert np.array_equal(got, base)
 
 
 def _scaled_weights(layers, scale_qk, seed):
@@ -155,21 +174,26 @@ def _scaled_weights(layers, scale_qk, seed):
 
 
 @pytest.mark.parametrize("world", [1, 8])
-def test_wan_two_layers_centred_signal(cuda, parity_log, world):
-    """2 layers x 1 step over 2 chunks with O(1) logits: the centred (per-token) part of the
-    output, not only the block mean, matches the fp64 oracle."""
+def test_wan_one_layer_centred_signal(cuda, parity_log, world):
+    """1 layer x 1 step over 2 chunks with O(1) logits (W_q, W_k scaled by 16: logit std
+    s^2 / D = 2 at D = 128): the centred (per-token) part of the output, not only the block
+    mean, matches the fp64 oracle. (With the reference init the logit std is ~1/D and the
+    token-discriminating signal is below bf16 resolution; a second layer of
+    this residual-free model collapses it again.)"""
     s = spattn()
-    w = _scaled_weights(2, 4.0, seed=21)
-    eng = s.Engine(cfg(2, 2, 1, world=world), seed_weights=False)
-    for l in range(2):
-        eng.set_layer_weights_bits(l, *[oracle.to_bf16_bits(w[l, m]) for m in range(4)])
+    w = _scaled_weights(1, 16.0, seed=21)
+    eng = s.Engine(cfg(2, 1, 1, world=world), seed_weights=False)
+    eng.set_layer_weights_bits(0, *[oracle.to_bf16_bits(w[0, m]) for m in range(4)])
     got = device_out(eng)
     del eng
     free_gpu()
-    ref = gpu_oracle.ReferenceModel(**WAN, layers=2, num_blocks=2, steps=1, weights=w).generate()
+    ref = gpu_oracle.ReferenceModel(**WAN, layers=1, num_blocks=2, steps=1, weights=w).generate()
     e = [rel_l2(got[b], ref[b]) for b in range(2)]
     ec = [rel_l2(centered(got[b]), centered(ref[b])) for b in range(2)]
-    parity_log(rel_l2=e, centred_rel_l2=ec, bar_rel_l2=1e-2, bar_centred=3e-2)
+    cshare = [float(np.linalg.norm(centered(ref[b])) / np.linalg.norm(ref[b])) for b in range(2)]
+    parity_log(rel_l2=e, centred_rel_l2=ec, centred_share_of_ref=cshare, bar_rel_l2=1e-2,
+               bar_centred=3e-2)
+    assert min(cshare) > 0.1  # the check is meaningful: tokens are distinct
     assert max(e) < 1e-2 and max(ec) < 3e-2, (e, ec)
 
 
