@@ -402,6 +402,23 @@ def main():
                  "latent_frames_per_s": 3 / (wan_ms[0] / 1e3),
                  "chunk_ms": wan_ms, "note": "frames/s of the first chunk (C2); chunk 2 attends 6 frames"}
 
+    # ---- the full Wan2.1 block (cross-attention to 512 cached text tokens, GELU FFN 8960,
+    # timestep adaLN; device-seeded synthetic weights), C2 chunk ----
+    full_ms = run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
+                        noise_dev, out_dev, barrier, max_over_ranks, blocks=2, wan_full=True)
+    Lp_full = L // world_size
+    gf_layer = (8 * Lp_full * C * C + 4 * L * L * C / world_size   # self-attn GEMMs + attention (chunk 0)
+                + 4 * Lp_full * C * C + 4 * Lp_full * 512 * C        # cross-attn q/o GEMMs + attention
+                + 4 * Lp_full * C * 8960) / 1e9                      # FFN
+    wan_full = {"workload": "C2 chunk through the full Wan2.1-1.3B block: timestep embedding + "
+                            "adaLN (6 modulation vectors per layer), self-attention (QK-RMSNorm, "
+                            "Causal-RoPE, biases), cross-attention to 512 cached text tokens, "
+                            "GELU(tanh) FFN 1536 -> 8960 -> 1536, gated residuals; 30 layers x 4 "
+                            "steps, device-seeded synthetic weights (no reference counterpart)",
+                "first_frame_latency_ms": full_ms[0], "latent_frames_per_s": 3 / (full_ms[0] / 1e3),
+                "chunk_ms": full_ms, "gflop_per_layer_call_per_rank": gf_layer,
+                "tflops_per_rank": gf_layer * 120 / full_ms[0]}
+
     # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
     peaks, peak_src = load_peaks()
     rope_mb = run_rope_microbench(torch, spattn, lib, check, peaks) if rank == 0 else None
@@ -460,6 +477,7 @@ def main():
         "video_5s": video,
         "video_60s": long_video,
         "wan_block": wan_block,
+        "wan_block_full": wan_full,
         "rope_microbench": rope_mb,
         "clocks": clocks, "gpu_launches": launches, "ledger": eng.stats(),
         "exchange": exchange_summary(eng.stats(), world_size, args, ms_per_chunk),
@@ -530,7 +548,8 @@ def _set_profile(eng, level):
 
 
 def run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size, noise_dev,
-              out_dev, barrier, max_over_ranks, blocks=7, window=-1, warmup=True, wan=False):
+              out_dev, barrier, max_over_ranks, blocks=7, window=-1, warmup=True, wan=False,
+              wan_full=False):
     """A video of `blocks` chunks (3 latent frames each, 30 layers, 4 denoise steps) on a
     second engine; per-chunk device times (CUDA events on the engine stream). window < 0:
     unlimited KV cache; otherwise the rolling window of `window` frames (the ring wraps and
@@ -543,7 +562,8 @@ def run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size
                                   layers=WAN["layers"], denoise_steps=WAN["steps"], heads=H,
                                   head_dim=D, world_size=world_size, seed=0, profile=False,
                                   window_frames=window if window > 0 else None,
-                                  fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=wan, adaln=wan)
+                                  fuse_rope_epilogue=not args.no_fuse_rope, qk_norm=wan, adaln=wan,
+                                  wan_block=wan_full)
     eng = new_engine(cfg)
     sp = ctypes.c_void_p()
     check(lib().spx_world_stream(world._h, 0, ctypes.byref(sp)))

@@ -123,7 +123,8 @@ spx_status spx_project_tokens_ex(const void* x, const void* w, void* y, int64_t 
                                  int64_t c_in, int64_t c_out, const float* bias, int32_t epilogue,
                                  const void* residual, const float* gate, void* stream);
 /* K6 scaled_dot_product_attention (proj/src/tensor.cpp:161-209), no mask.
- * q (B, Sq, H, D), k/v (B, Skv, H, D), o (B, Sq, H, D); bf16, B == 1, D in {64, 128}. */
+ * q (B, Sq, H, D), k/v (B, Skv, H, D), o (B, Sq, H, D); bf16, B == 1, D in {64, 128} on the
+ * tcgen05 kernel, D in {16, 32} (the reference default / desk shapes) on a SIMT kernel. */
 spx_status spx_attention(const void* q, const void* k, const void* v, void* o, int64_t batch,
                          int64_t sq, int64_t skv, int64_t heads, int64_t head_dim, void* stream);
 

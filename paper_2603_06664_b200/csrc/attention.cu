@@ -892,6 +892,65 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
     }
 }
 
+// head_dim 16 / 32 (the reference's default and desk configurations, GenerationConfig
+// defaults D = 16: generator.hpp:14-42): below the 64-element rows the tcgen05 / TMA tile
+// layout is built for; these shapes are tiny (48-token blocks), so a SIMT kernel serves them.
+// One warp per (query row, head); lanes stride over the keys of both ring segments with a
+// per-lane online softmax, merged across the warp at the end. Same output addressing as K6.
+template <int D>
+__global__ void __launch_bounds__(128) attn_small_kernel(const bf16* __restrict__ q,
+                                                        const bf16* __restrict__ k,
+                                                        const bf16* __restrict__ v,
+                                                        const AttnParams p, int64_t q_stride,
+                                                        int64_t kv_stride) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x % 32;
+    const int64_t pair = static_cast<int64_t>(blockIdx.x) * 4 + threadIdx.x / 32;
+    if (pair >= static_cast<int64_t>(p.sq) * p.heads) return;
+    const int row = static_cast<int>(pair / p.heads);
+    const int head = static_cast<int>(pair % p.heads);
+    float qf[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) qf[d] = __bfloat162float(q[row * q_stride + head * D + d]) * p.scale_log2;
+    const int total = p.seg_len[0] + p.seg_len[1];
+    float m = -INFINITY, l = 0.0f, acc[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[d] = 0.0f;
+    for (int j = lane; j < total; j += 32) {
+        const int r = j < p.seg_len[0] ? p.seg_start[0] + j : p.seg_start[1] + (j - p.seg_len[0]);
+        const bf16* kr = k + static_cast<int64_t>(r) * kv_stride + head * D;
+        const bf16* vr = v + static_cast<int64_t>(r) * kv_stride + head * D;
+        float s = 0.0f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) s = fmaf(qf[d], __bfloat162float(kr[d]), s);
+        const float mn = fmaxf(m, s);
+        const float a = exp2f(m - mn), e = exp2f(s - mn);
+        l = l * a + e;
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc[d] = acc[d] * a + e * __bfloat162float(vr[d]);
+        m = mn;
+    }
+    float mw = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+    const float a = m == -INFINITY ? 0.0f : exp2f(m - mw);
+    l *= a;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    const float inv = 1.0f / l;
+    const int chunk = row / p.rows_per_chunk;
+    bf16* dst = p.out_base[chunk] + static_cast<int64_t>(row - chunk * p.rows_per_chunk) * p.out_row_stride +
+                static_cast<int64_t>(head) * D;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        float x = acc[d] * a;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == d % 32) dst[d] = __float2bfloat16_rn(x * inv);
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -994,13 +1053,19 @@ size_t attn_workspace_bytes(const AttnOperands& ops, int max_splits) {
 }
 
 void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count) {
-    require(ops.head_dim == 64 || ops.head_dim == 128, SPX_ERR_UNSUPPORTED,
-            "attention: head_dim must be 64 or 128 (got " + std::to_string(ops.head_dim) + ")");
+    require(ops.head_dim == 16 || ops.head_dim == 32 || ops.head_dim == 64 || ops.head_dim == 128,
+            SPX_ERR_UNSUPPORTED,
+            "attention: head_dim must be 16, 32, 64 or 128 (got " + std::to_string(ops.head_dim) + ")");
     require(ops.batch == 1, SPX_ERR_UNSUPPORTED, "attention kernel: batch must be 1");
     require(ops.sq > 0 && ops.heads > 0, SPX_ERR_SHAPE, "attention: empty problem");
     require(ops.rows_per_chunk > 0 && ceil_div(ops.sq, ops.rows_per_chunk) <= 8, SPX_ERR_SHAPE,
             "attention: at most 8 output chunks");
     plan->ops = ops;
+    if (ops.head_dim < 64) {  // SIMT path (attn_small_kernel): no tensor maps, no splits
+        attn_set_segments(plan, ops.seg_start, ops.seg_len, ops.num_segs);
+        plan->max_splits = 1;
+        return;
+    }
     char err[256];
     const uint32_t box[3] = {64, 1, 128};
     {
@@ -1052,6 +1117,23 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     for (int s = 0; s < 2; ++s) {
         p.seg_start[s] = o.seg_start[s];
         p.seg_len[s] = o.seg_len[s];
+    }
+    if (o.head_dim < 64) {
+        p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(o.head_dim));
+        for (int i = 0; i < 8; ++i) p.out_base[i] = o.out_base[i];
+        p.rows_per_chunk = o.rows_per_chunk;
+        p.out_row_stride = o.out_row_stride;
+        p.heads = o.heads;
+        const int64_t pairs = static_cast<int64_t>(o.sq) * o.heads;
+        const dim3 grid(static_cast<unsigned>(ceil_div(pairs, 4)));
+        const int64_t qs = static_cast<int64_t>(o.heads) * o.head_dim;
+        if (o.head_dim == 16)
+            launch_pdl(attn_small_kernel<16>, grid, dim3(128), 0, stream, o.q, o.k, o.v, p, qs, qs);
+        else
+            launch_pdl(attn_small_kernel<32>, grid, dim3(128), 0, stream, o.q, o.k, o.v, p, qs, qs);
+        SPX_CUDA_LAUNCH();
+        count_launch();
+        return;
     }
     p.seg_tiles0 = static_cast<int>(ceil_div(o.seg_len[0], kBKV));
     p.total_tiles = p.seg_tiles0 + static_cast<int>(ceil_div(o.seg_len[1], kBKV));

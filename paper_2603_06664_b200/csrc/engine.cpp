@@ -64,8 +64,12 @@ void Engine::validate(const spx_engine_config& c, int world_size) {
             "window_frames smaller than one block is not supported");
     // device path constraints
     require(c.batch == 1, SPX_ERR_UNSUPPORTED, "device engine runs batch 1");
-    require(c.head_dim == 64 || c.head_dim == 128, SPX_ERR_UNSUPPORTED,
-            "device engine needs head_dim 64 or 128");
+    require(c.head_dim == 16 || c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128,
+            SPX_ERR_UNSUPPORTED,
+            "device engine needs head_dim 16, 32, 64 or 128 (16 / 32: the reference's small "
+            "configurations, attention on the SIMT path)");
+    require(!c.wan_block || c.head_dim >= 64, SPX_ERR_UNSUPPORTED,
+            "wan_block needs head_dim 64 or 128");
     const int64_t C = c.heads * c.head_dim;
     require(C % 64 == 0 && C <= 2048, SPX_ERR_UNSUPPORTED,
             "device engine needs a model dim that is a multiple of 64 and <= 2048");
@@ -125,6 +129,12 @@ Engine::Engine(World* world, const spx_engine_config& cfg) : world_(world), cfg_
     Lq_ = L_ / S_;
     Hl_ = H_ / G_;
     part_ = Partition::make(P_, H_, L_, D_);
+    // the O-projection reads the head-group slabs through a 3-D TMA whose inner extent must be
+    // a multiple of 64 elements; below that (small head_dim, many groups) the attention
+    // epilogue stores o rows interleaved instead: (L/P, C) with group g at columns g H/G D
+    o_interleaved_ = (Hl_ * D_) % 64 != 0;
+    require(!o_interleaved_ || world->transport() != SPX_TRANSPORT_NCCL, SPX_ERR_UNSUPPORTED,
+            "NCCL transport needs (heads / groups) x head_dim to be a multiple of 64");
     cap_frames_ = cfg.window_frames < 0 ? cfg.num_blocks * F_
                                         : ceil_div(cfg.window_frames, F_) * F_;
     frames_ = FrameRing(cap_frames_, cfg.window_frames);
@@ -419,10 +429,17 @@ void Engine::build_plans() {
 
             GemmOperands o{};
             o.a = rs.o_recv;
-            o.a_row_stride = Hl_ * D_;
-            o.a_group_stride = Lp_ * Hl_ * D_;
-            o.groups = static_cast<int>(G_);
-            o.k_inner = static_cast<int>(Hl_ * D_);
+            if (o_interleaved_) {  // (L/P, C) rows, head group g at columns [g H/G D, ...)
+                o.a_row_stride = C_;
+                o.a_group_stride = Lp_ * C_;
+                o.groups = 1;
+                o.k_inner = static_cast<int>(C_);
+            } else {               // [G][L/P][H/G D] slabs, un-interleaved by the 3-D TMA
+                o.a_row_stride = Hl_ * D_;
+                o.a_group_stride = Lp_ * Hl_ * D_;
+                o.groups = static_cast<int>(G_);
+                o.k_inner = static_cast<int>(Hl_ * D_);
+            }
             o.b = w.wo + l * C_ * C_;
             o.b_row_stride = C_;
             o.out = rs.x[(l + 1) % 2];
@@ -457,7 +474,7 @@ void Engine::build_plans() {
             a.seg_len[0] = static_cast<int>(HW_);  // placeholder until begin_block
             a.num_segs = 1;
             a.rows_per_chunk = static_cast<int>(Lp_);
-            a.out_row_stride = Hl_ * D_;
+            a.out_row_stride = o_interleaved_ ? C_ : Hl_ * D_;
             if (l == 0 && !cfg_.sp_bit_exact) {  // one split-KV workspace per rank (layers in stream order)
                 const size_t ws = attn_workspace_bytes(a, attn_max_splits(a, sms));
                 if (ws > 0) {
@@ -846,7 +863,8 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
         for (int64_t c = 0; c < G_; ++c) {
             const int i = static_cast<int>(rs.p * G_ + c);
             if (local || peer) {
-                plan.ops.out_base[c] = o_recv_of(i) + rs.g * slab;
+                plan.ops.out_base[c] = o_interleaved_ ? o_recv_of(i) + rs.g * Hl_ * D_
+                                                      : o_recv_of(i) + rs.g * slab;
             } else {
                 plan.ops.out_base[c] = i == rs.rank ? rs.o_recv + rs.g * slab : rs.o_send + c * slab;
             }

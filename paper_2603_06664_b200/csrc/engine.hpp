@@ -237,7 +237,8 @@ class Engine {
     spx_engine_config cfg_;
     // geometry
     int64_t F_, Hg_, Wg_, HW_, L_, H_, D_, C_, P_, G_, S_, Lp_, Lq_, Hl_;
-    int64_t FF_ = 0, TL_ = 0, TD_ = 0, FD_ = 0;  // wan_block: ffn, text len / dim, freq dim
+    int64_t FF_ = 0, TL_ = 0, TD_ = 0, FD_ = 0;
+    bool o_interleaved_ = false;  // attention output stored as (L/P, C) rows (see constructor)  // wan_block: ffn, text len / dim, freq dim
     int64_t cap_frames_ = 0;
     Partition part_{};
     std::unique_ptr<RopeTable> table_;

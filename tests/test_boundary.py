@@ -141,8 +141,11 @@ def test_config_validation_mirrors_reference():
         spattn.GenerationConfig(window_frames=2, **wan).validate()  # window < tau
     with pytest.raises(spattn.ShapeError):
         spattn.GenerationConfig(grid_per_block=spattn.GridSpec(0, 4, 4), heads=4, head_dim=64).validate()
+    spattn.GenerationConfig().validate()  # reference default D = 16: SIMT attention path
     with pytest.raises(spattn.UnsupportedError):
-        spattn.GenerationConfig().validate()  # reference default D = 16: no tcgen05 path
+        spattn.GenerationConfig(head_dim=24, heads=8).validate()  # D must divide 256
+    with pytest.raises(spattn.UnsupportedError):
+        spattn.GenerationConfig(wan_block=True).validate()  # the full block needs D >= 64
 
 
 def test_checksum_matches_reference_report_format():

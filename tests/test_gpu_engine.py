@@ -635,3 +635,58 @@ def test_generate_stream_matches_block_by_block(cuda):
     for i in range(len(order)):
         assert np.array_equal(got[i], want[i]), i
     assert e.stats() == a.stats()
+
+
+DESK = dict(frames=3, grid_h=4, grid_w=4, num_blocks=5, layers=4, heads=8, head_dim=16)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_desk_config_acceptance_criterion_1(cuda, seed, parity_log):
+    """The reference's acceptance criterion 1 (tests/acceptance.cpp:44-87): the GenerationConfig
+    defaults (3 x 4 x 4 grid, H = 8, D = 16, 4 layers, 2 steps, 5 blocks) at P in {1, 2, 4, 8}
+    x seeds {0, 1, 2} equal the P = 1 reference. D = 16 runs attention on the SIMT path and the
+    O-projection on interleaved output rows; against the fp64 oracle on the same bf16 inputs
+    the bar is bf16 (rel-L2 < 1e-2 per block), and every P equals P = 1 bit for bit."""
+    s = spattn()
+    ref = oracle.generate(**DESK, steps=2, seed=seed, round_inputs=True)
+    base = None
+    for P in (1, 2, 4, 8):
+        got = s.bf16_bits_to_float(s.Engine(cfg_from(DESK, steps=2, world=P, seed=seed)).generate())
+        e = [rel_l2(got[b], ref[b]) for b in range(DESK["num_blocks"])]
+        parity_log(**{f"rel_l2_p{P}": e})
+        assert max(e) < 1e-2, (P, e)
+        if base is None:
+            base = got
+        assert np.array_equal(got, base), P
+
+
+def test_desk_config_ablation_lattice_bit_identical(cuda):
+    """the 2^3 AblationFlags lattice at the desk shape (D = 16), P = 2 and 4 vs optimized P = 1"""
+    s = spattn()
+    base = s.bf16_bits_to_float(s.Engine(cfg_from(DESK, world=1, fuse_rope_epilogue=False)).generate())
+    for P in (2, 4):
+        for flags in s.AblationFlags.lattice():
+            got = s.bf16_bits_to_float(s.Engine(cfg_from(DESK, world=P, fuse_rope_epilogue=False,
+                                                         ablation=flags)).generate())
+            assert np.array_equal(got, base), (P, flags)
+
+
+@pytest.mark.parametrize("D", [16, 32])
+def test_small_head_dim_attention_matches_fp32(cuda, D, parity_log):
+    import torch
+
+    from paper_2603_06664_b200._lib import check, lib
+
+    g = torch.Generator(device="cuda").manual_seed(D)
+    q = torch.randn(1, 96, 8, D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(1, 240, 8, D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, 240, 8, D, device=cuda, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 1, 96, 240, 8, D,
+                              torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    qf, kf, vf = (t.float()[0].transpose(0, 1) for t in (q, k, v))
+    ref = (torch.softmax(qf @ kf.transpose(1, 2) / math.sqrt(D), dim=-1) @ vf).transpose(0, 1)
+    e = float((o.float()[0] - ref).norm() / ref.norm())
+    parity_log(rel_l2=e, bar=5e-3)
+    assert e < 5e-3
