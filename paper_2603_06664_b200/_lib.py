@@ -214,6 +214,7 @@ _SIGS = [
     ("spx_engine_ipc_import", c_int, [c_void_p, c_void_p, c_int64]),
     ("spx_debug_set_gemm_variant", c_int, [c_int32]),
     ("spx_debug_set_attn_splits", c_int, [c_int32]),
+    ("spx_debug_set_attn_v3", c_int, [c_int32]),
     ("spx_debug_spans", c_int, [c_void_p, c_int64, c_void_p]),
     ("spx_debug_gemm_trace", c_int, [c_void_p, c_int64]),
     ("spx_debug_naive_gemm", c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),

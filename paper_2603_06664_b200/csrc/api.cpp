@@ -1048,6 +1048,10 @@ spx_status spx_debug_spans(uint64_t* out, int64_t capacity, int64_t* count) {
     });
 }
 
+spx_status spx_debug_set_attn_v3(int32_t on) {
+    return guarded([&] { attn_set_v3(on); });
+}
+
 spx_status spx_debug_set_attn_splits(int32_t splits) {
     return guarded([&] {
         require(splits >= 0 && splits <= 8, SPX_ERR_CONFIG, "attention splits must be 0..8");

@@ -81,6 +81,12 @@ struct AttnParams {
     int64_t pf_bytes[2];
     long long* trace;      // SPX_ATTN_EXPERIMENT=5: per-CTA clock64 marks [cta][16][4]
     unsigned long long* span;  // SPX_SPAN_TRACE
+    // raw operand pointers (v3's exact fallback path and the small-D kernel)
+    const bf16* q_ptr;
+    const bf16* k_ptr;
+    const bf16* v_ptr;
+    int64_t q_row_stride;   // elements between query rows (heads * D)
+    int64_t kv_row_stride;  // elements between kv rows
 };
 
 __device__ __forceinline__ void attn_mark(const AttnParams& p, int k) {
@@ -892,6 +898,392 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
     }
 }
 
+
+// =========================================================================================
+// v3: one 128-row query tile per CTA; the kv range is split between two softmax warpgroups
+// as in v2, but the two slots accumulate into ONE O (TMEM) with a common exponent offset (the
+// max over both slots' first tiles, exchanged once), which frees the TMEM for separate P
+// buffers:  S0 | S1 | O | P0 | P1  = 128 + 128 + 128 + 64 + 64 columns.
+// With P no longer written over S, the MMA issues S_i(j+1) as soon as the softmax has loaded
+// S_i(j) into registers (s_free), so a slot's dependency chain per tile is softmax + PV
+// instead of softmax + PV + QK^T. MMA issue order (= the producer's ring order):
+//   QK0(0) QK1(0) | QK0(j+1) PV0(j) QK1(j+1) PV1(j) | ...
+// Overflow: the fixed offset covers logits up to offset + 64 (log2 units) exactly; if a later
+// tile's exponentials exceed 2^64 (or are not finite), the shared O cannot be rescaled
+// without stopping both slots, so the CTA flags it and recomputes its rows exactly on the
+// CUDA cores after the main loop (never taken for sane inputs; tested).
+// =========================================================================================
+template <int D>
+__global__ void __launch_bounds__(kThreadsV2, 1)
+    attn_fwd_v3_kernel(const __grid_constant__ CUtensorMap map_q,
+                       const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
+    using L = SmemV2<D, 0>;
+    constexpr uint32_t kSlots = L::kSlots;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sQ = smem + L::kOffQ;
+    uint8_t* ring = smem + L::kOffRing;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+    uint64_t* q_full = bars;
+    uint64_t* slot_full = bars + 1;
+    uint64_t* slot_empty = slot_full + kSlots;
+    uint64_t* s_full = slot_empty + kSlots;  // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* pv_done = p_full + 2;          // [2]
+    uint64_t* s_free = pv_done + 2;          // [2] (the merge / xfer slots of v2)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+    float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
+    float* st_l = st_m + 256;                                     // [2][128]
+    __shared__ int s_ovf;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    pdl_trigger();
+    span_begin(p.span);
+    const int t_idx = static_cast<int>(blockIdx.x);
+    const int q_tile = t_idx % p.qt;
+    const int head = t_idx / p.qt;
+    const int n_total = p.total_tiles;
+    const int n0 = (n_total + 1) / 2;
+    const int n1 = n_total - n0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_q);
+        tma_prefetch_desc(&map_k);
+        tma_prefetch_desc(&map_v);
+        mbar_init(q_full, 1);
+        for (uint32_t s = 0; s < kSlots; ++s) {
+            mbar_init(&slot_full[s], 1);
+            mbar_init(&slot_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);   // one arrival per softmax warp
+            mbar_init(&pv_done[i], 1);
+            mbar_init(&s_free[i], 4);   // one arrival per softmax warp
+        }
+        s_ovf = 0;
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t t_O = tmem_base + 256;
+    pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
+
+    if (warp < 4) {
+        setmaxnreg_dec56();
+        if (warp == 0 && lane == 0) {
+            // ---------------- TMA producer: the MMA consumption order ----------------
+            uint32_t t = 0;
+            mbar_arrive_expect_tx(q_full, kBQ * D * 2);
+#pragma unroll
+            for (int c = 0; c < (int)L::kChunks; ++c)
+                tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
+            auto load = [&](bool is_v, int g) {
+                const uint32_t slot = t % kSlots;
+                const uint32_t ph = (t / kSlots) & 1;
+                mbar_wait(&slot_empty[slot], ph ^ 1);
+                mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
+                int row, valid;
+                kv_tile_coords(p, g, row, valid);
+                uint8_t* dst = ring + slot * L::kTileBytes;
+#pragma unroll
+                for (int c = 0; c < (int)L::kChunks; ++c)
+                    tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
+                                c * 64, head, row);
+                ++t;
+            };
+            load(false, 0);
+            if (n1 > 0) load(false, n0);
+            for (int j = 0; j < n0; ++j) {
+                if (j + 1 < n0) load(false, j + 1);
+                load(true, j);
+                if (j < n1) {
+                    if (j + 1 < n1) load(false, n0 + j + 1);
+                    load(true, n0 + j);
+                }
+            }
+        } else if (warp == 1) {
+            // ---------------- MMA issuer ----------------
+            const bool issuer = elect_one();
+            constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
+            const uint32_t q_addr = smem_u32(sQ);
+            const uint32_t ring_addr = smem_u32(ring);
+            uint32_t t = 0;
+            bool first_pv = true;
+            auto take = [&]() {
+                const uint32_t slot = t % kSlots;
+                mbar_wait(&slot_full[slot], (t / kSlots) & 1);
+                tc_fence_after();
+                ++t;
+                return slot;
+            };
+            auto issue_s = [&](int i) {
+                const uint32_t slot = take();
+                const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
+                if (issuer) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                        umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
+                                     make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                    }
+                    umma_commit(&s_full[i]);
+                    umma_commit(&slot_empty[slot]);
+                }
+                __syncwarp();
+            };
+            auto issue_pv = [&](int i, int j) {
+                const uint32_t slot = take();
+                mbar_wait(&p_full[i], j & 1);
+                tc_fence_after();
+                const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
+                const uint32_t t_p = tmem_base + 384 + i * 64;
+                if (issuer) {
+#pragma unroll
+                    for (int kk = 0; kk < kBKV / 16; ++kk)
+                        umma_bf16_ts(t_O, t_p + kk * 8,
+                                     make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                     idesc_o, (first_pv && kk == 0) ? 0u : 1u);
+                    umma_commit(&pv_done[i]);
+                    umma_commit(&slot_empty[slot]);
+                }
+                first_pv = false;
+                __syncwarp();
+            };
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            issue_s(0);
+            if (n1 > 0) issue_s(1);
+            for (int j = 0; j < n0; ++j) {
+                if (j + 1 < n0) {
+                    mbar_wait(&s_free[0], j & 1);  // the softmax holds S0(j) in registers
+                    tc_fence_after();
+                    issue_s(0);
+                }
+                issue_pv(0, j);
+                if (j < n1) {
+                    if (j + 1 < n1) {
+                        mbar_wait(&s_free[1], j & 1);
+                        tc_fence_after();
+                        issue_s(1);
+                    }
+                    issue_pv(1, j);
+                }
+            }
+        }
+    } else {
+        setmaxnreg_inc224();
+        // ---------------- softmax warpgroups ----------------
+        const int i = (warp - 4) / 4;           // slot
+        const int q = warp % 4;                 // TMEM lane quarter
+        const int r = q * 32 + lane;            // query row in the tile == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const uint32_t t_s = tmem_base + i * 128 + lane_off;
+        const uint32_t t_p = tmem_base + 384 + i * 64 + lane_off;
+        const int n = i == 0 ? n0 : n1;
+        const int g0 = i == 0 ? 0 : n0;
+        const float scale = p.scale_log2;
+        float m_run = -INFINITY;
+        float l_run = 0.0f;
+        bool ovf = false;
+        if (n == 0) {  // (a one-tile kv range: slot 1 idle) still joins the offset exchange
+            st_m[i * 128 + r] = -INFINITY;
+            named_bar_sync(1, 256);
+        }
+        for (int j = 0; j < n; ++j) {
+            int row, valid;
+            kv_tile_coords(p, g0 + j, row, valid);
+            mbar_wait(&s_full[i], j & 1);
+            tc_fence_after();
+            uint32_t u[kBKV];
+#pragma unroll
+            for (int c = 0; c < kBKV / 32; ++c)
+                tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+            tmem_ld_wait();
+            // S_i is in registers: the MMA may overwrite it with S_i(j + 1)
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[i]);
+            if (valid < kBKV) {  // ragged tail tile only: masked logits -> -inf (exp -> 0)
+#pragma unroll
+                for (int c = 0; c < kBKV; ++c)
+                    if (c >= valid) u[c] = 0xff800000u;
+            }
+            if (j == 0) {  // common exponent offset: max over both slots' first tiles
+                float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < kBKV; c += 8) {
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4)
+                        mq[k4] = fmax3f(mq[k4], __uint_as_float(u[c + 2 * k4]),
+                                        __uint_as_float(u[c + 2 * k4 + 1]));
+                }
+                st_m[i * 128 + r] = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * scale;
+                named_bar_sync(1, 256);
+                m_run = fmaxf(st_m[r], st_m[128 + r]);
+            }
+            uint32_t pk[kBKV / 2];
+            float lt;
+            {  // P = exp2(s scale - m), bf16 pairs; lt = the row sum
+                const float2 sc2 = make_float2(scale, scale);
+                const float2 nm2 = make_float2(-m_run, -m_run);
+                float2 ls[4];
+#pragma unroll
+                for (int e = 0; e < kBKV / 2; ++e) {
+                    const float2 x = ffma2(
+                        make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2, nm2);
+                    float2 pr;
+                    if ((e & 7) >= 8 - SPX_POLY_OF_8) {
+                        pr = ex2_poly2(x);
+                    } else {
+                        pr.x = ex2_approx(x.x);
+                        pr.y = ex2_approx(x.y);
+                    }
+                    ls[e & 3] = e < 4 ? pr : fadd2(ls[e & 3], pr);
+                    pk[e] = pack_bf16x2(pr.x, pr.y);
+                }
+                const float2 s01 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+                lt = s01.x + s01.y;
+            }
+            ovf = ovf || !(lt < 1.8446744e19f);  // 2^64, or inf / NaN
+            l_run += lt;
+            // P_i(j - 1) has been read by its PV before P_i(j) overwrites the buffer
+            if (j > 0) {
+                mbar_wait(&pv_done[i], (j - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c = 0; c < kBKV / 32; ++c) tmem_st16(t_p + c * 16, &pk[c * 16]);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[i]);
+        }
+        if (n > 0) {
+            mbar_wait(&pv_done[i], (n - 1) & 1);
+            tc_fence_after();
+        }
+        if (ovf) s_ovf = 1;
+        // ---------------- epilogue: O / (l0 + l1), rows staged in the idle Q smem ----------------
+        st_l[i * 128 + r] = l_run;
+        tc_fence_before();
+        named_bar_sync(1, 256);  // both slots' last PVs are done; l and the flag are visible
+        tc_fence_after();
+        const float inv = 1.0f / (st_l[r] + st_l[128 + r]);
+        const bool fallback = s_ovf != 0;
+        constexpr uint32_t kRowBytes = D * 2;
+        constexpr uint32_t kU = kRowBytes / 16;
+        const uint32_t s_base = smem_u32(smem);
+        if (!fallback) {
+#pragma unroll 1
+            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+                uint32_t o[32];
+                tmem_ld32(t_O + lane_off + c * 32, o);
+                tmem_ld_wait();
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t unit = static_cast<uint32_t>(c * 4 + v);
+                    const uint32_t a = s_base + static_cast<uint32_t>(r) * kRowBytes +
+                                       ((unit ^ (static_cast<uint32_t>(r) & (kU - 1))) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                                 "r"(pack_bf16x2(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv)),
+                                 "r"(pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv)),
+                                 "r"(pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv)),
+                                 "r"(pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv))
+                                 : "memory");
+                }
+            }
+        } else {
+            // exact recompute of this thread's row, columns [i D/2, (i + 1) D/2), from global
+            // memory with a running max (rare path; see the kernel comment)
+            const int qi = q_tile * kBQ + r;
+            float acc[D / 2];
+#pragma unroll
+            for (int d = 0; d < D / 2; ++d) acc[d] = 0.0f;
+            float m = -INFINITY, l = 0.0f;
+            if (qi < p.sq) {
+                const bf16* qr = p.q_ptr + static_cast<int64_t>(qi) * p.q_row_stride + head * D;
+                const int total = p.seg_len[0] + p.seg_len[1];
+                for (int jj = 0; jj < total; ++jj) {
+                    const int kr = jj < p.seg_len[0] ? p.seg_start[0] + jj : p.seg_start[1] + (jj - p.seg_len[0]);
+                    const bf16* krow = p.k_ptr + static_cast<int64_t>(kr) * p.kv_row_stride + head * D;
+                    const bf16* vrow = p.v_ptr + static_cast<int64_t>(kr) * p.kv_row_stride + head * D + i * (D / 2);
+                    float sdot = 0.0f;
+                    for (int d = 0; d < D; ++d) sdot = fmaf(__bfloat162float(qr[d]), __bfloat162float(krow[d]), sdot);
+                    sdot *= scale;
+                    const float mn = fmaxf(m, sdot);
+                    const float a = exp2f(m - mn), e = exp2f(sdot - mn);
+                    l = l * a + e;
+#pragma unroll
+                    for (int d = 0; d < D / 2; ++d) acc[d] = acc[d] * a + e * __bfloat162float(vrow[d]);
+                    m = mn;
+                }
+            }
+            const float il = 1.0f / l;
+#pragma unroll
+            for (int v = 0; v < D / 16; ++v) {
+                const uint32_t unit = static_cast<uint32_t>(i * (D / 16) + v);
+                const uint32_t a = s_base + static_cast<uint32_t>(r) * kRowBytes +
+                                   ((unit ^ (static_cast<uint32_t>(r) & (kU - 1))) << 4);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                             "r"(pack_bf16x2(acc[8 * v + 0] * il, acc[8 * v + 1] * il)),
+                             "r"(pack_bf16x2(acc[8 * v + 2] * il, acc[8 * v + 3] * il)),
+                             "r"(pack_bf16x2(acc[8 * v + 4] * il, acc[8 * v + 5] * il)),
+                             "r"(pack_bf16x2(acc[8 * v + 6] * il, acc[8 * v + 7] * il))
+                             : "memory");
+            }
+        }
+        named_bar_sync(1, 256);
+        const int tid = static_cast<int>(threadIdx.x) - 128;
+#pragma unroll 1
+        for (int idx = tid; idx < kBQ * static_cast<int>(kU); idx += 256) {
+            const int row = idx / static_cast<int>(kU);
+            const uint32_t uu = static_cast<uint32_t>(idx) % kU;
+            const int q_row = q_tile * kBQ + row;
+            if (q_row >= p.sq) continue;
+            uint4 w;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(s_base + static_cast<uint32_t>(row) * kRowBytes +
+                               ((uu ^ (static_cast<uint32_t>(row) & (kU - 1))) << 4))
+                         : "memory");
+            const int chunk = q_row / p.rows_per_chunk;
+            bf16* drow = p.out_base[chunk] +
+                         static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
+                         static_cast<int64_t>(head) * D;
+            *reinterpret_cast<uint4*>(drow + uu * 8) = w;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    span_end(p.span);
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+template <int D>
+void attn_v3_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
+    static bool done[64] = {};
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 63]) {
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(SmemV2<D, 0>::kBytes)));
+        done[dev & 63] = true;
+    }
+    launch_pdl(attn_fwd_v3_kernel<D>, grid, dim3(kThreadsV2), SmemV2<D, 0>::kBytes, stream, plan.map_q,
+               plan.map_k, plan.map_v, p);
+}
+
 // head_dim 16 / 32 (the reference's default and desk configurations, GenerationConfig
 // defaults D = 16: generator.hpp:14-42): below the 64-element rows the tcgen05 / TMA tile
 // layout is built for; these shapes are tiny (48-token blocks), so a SIMT kernel serves them.
@@ -976,6 +1368,14 @@ int choose_splits(int64_t n, int64_t tiles, int sm_count, int cap) {
     return best;
 }
 }  // namespace
+
+// the shared-O / early-S kernel (v3) for unsplit layouts: SPX_ATTN_V3=1 (0 = v2)
+std::atomic<int> g_attn_v3{[] {
+    const char* e = std::getenv("SPX_ATTN_V3");
+    return e ? std::atoi(e) : 0;
+}()};
+bool attn_v3_enabled() { return g_attn_v3.load(std::memory_order_relaxed) != 0; }
+void attn_set_v3(int on) { g_attn_v3.store(on, std::memory_order_relaxed); }
 
 std::atomic<int> g_forced_splits{[] {  // tuning override: SPX_ATTN_SPLITS=<1..8>
     const char* e = std::getenv("SPX_ATTN_SPLITS");
@@ -1153,6 +1553,11 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     }
     p.out_row_stride = o.out_row_stride;
     p.out_batch_stride = o.out_batch_stride;
+    p.q_ptr = o.q;
+    p.k_ptr = o.k;
+    p.v_ptr = o.v;
+    p.q_row_stride = static_cast<int64_t>(o.heads) * o.head_dim;
+    p.kv_row_stride = static_cast<int64_t>(o.heads) * o.head_dim;
     // kv splits for this call's kv length, within the planned workspace
     {
         int dev = 0;
@@ -1205,6 +1610,12 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 attn_v2_launch<128, 5>(g2, plan, p, stream);
             else
                 attn_v2_launch<64, 5>(g2, plan, p, stream);
+        } else if (attn_v3_enabled() && p.n_full == T && p.experiment == 0) {
+            // every tile unsplit: the shared-O / early-S kernel
+            if (o.head_dim == 128)
+                attn_v3_launch<128>(dim3(static_cast<unsigned>(T)), plan, p, stream);
+            else
+                attn_v3_launch<64>(dim3(static_cast<unsigned>(T)), plan, p, stream);
         } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
             const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
             if (o.head_dim == 128)

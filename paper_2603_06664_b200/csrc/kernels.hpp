@@ -117,6 +117,9 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count);
 void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs);
 // split-KV override (tests / tuning): 0 = modelled choice, else the kv splits per query tile
 void attn_force_splits(int s);
+// the shared-O / early-S attention kernel (v3) for unsplit layouts: on / off (SPX_ATTN_V3)
+void attn_set_v3(int on);
+bool attn_v3_enabled();
 void attn_run(const AttnPlan& plan, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------------------

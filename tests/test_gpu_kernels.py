@@ -81,9 +81,17 @@ def test_project_tokens_every_tile_variant(cuda, variant, M, K, N):
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
+@pytest.fixture(params=[0, 1], ids=["v2", "v3"])
+def attn_kernel(request):
+    """run the test with the v2 kernel (per-slot O) and with v3 (shared O, early S)"""
+    _check(_lib().spx_debug_set_attn_v3(request.param))
+    yield request.param
+    _check(_lib().spx_debug_set_attn_v3(0))
+
+
 @pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),
-                                        (4680, 4680, 12, 128), (1170, 9360, 3, 128)])
-def test_attention_matches_fp32(cuda, sq, skv, H, D, parity_log):
+                                        (4680, 4680, 12, 128), (1170, 9360, 3, 128), (128, 100, 1, 128)])
+def test_attention_matches_fp32(cuda, sq, skv, H, D, parity_log, attn_kernel):
     torch = _t()
     g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
     # O(1) logits (well-conditioned softmax), as in the tolerance tier of SURVEY 8c
@@ -169,7 +177,7 @@ def test_attention_split_kv_matches_fp32(cuda, splits, sq, skv, H, parity_log):
 
 
 @pytest.mark.parametrize("skv", [640, 4680])
-def test_attention_offset_guard_on_growing_logits(cuda, skv):
+def test_attention_offset_guard_on_growing_logits(cuda, skv, attn_kernel):
     """The softmax takes its exponent offset from each warpgroup's first kv tile and skips the
     per-tile max afterwards; logits that later jump far above that offset (here by ~500 in
     natural units, > 2^64 after exp) must trip the overflow guard, which redoes the tile with

@@ -11,9 +11,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --profile-only --steps 1 --warmup 1 > $O/launches.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_full.csv \
     python tools/wan_chunk.py full 30 > $O/launches_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 20 -c 1 -o $O/attn python tools/wan_chunk.py ref 2 > $O/ncu_attn.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_pair -s 20 -c 1 -o $O/qkv python tools/wan_chunk.py ref 2 > $O/ncu_qkv.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_kernel -s 20 -c 1 -o $O/oproj python tools/wan_chunk.py ref 2 > $O/ncu_oproj.log 2>&1
+SPX_GRAPHS=0 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 9 -c 1 -o $O/attn python tools/wan_chunk.py ref 2 > $O/ncu_attn.log 2>&1
+SPX_GRAPHS=0 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_pair -s 9 -c 1 -o $O/qkv python tools/wan_chunk.py ref 2 > $O/ncu_qkv.log 2>&1
+SPX_GRAPHS=0 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_kernel -s 9 -c 1 -o $O/oproj python tools/wan_chunk.py ref 2 > $O/ncu_oproj.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:rope_norm_pack -s 10 -c 1 -o $O/k3 python tools/wan_chunk.py wan 2 > $O/ncu_k3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:ln_modulate -s 10 -c 1 -o $O/k1 python tools/wan_chunk.py wan 2 > $O/ncu_k1.log 2>&1
 ncu --set full --clock-control none -k regex:gemm -s 100 -c 12 -o $O/fullblock_gemms python tools/wan_chunk.py full 2 > $O/ncu_full.log 2>&1

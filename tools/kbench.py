@@ -141,6 +141,8 @@ if __name__ == "__main__":
         which = "attn"
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     lib()
+    if os.environ.get("KBENCH_ATTN_V3"):
+        check(lib().spx_debug_set_attn_v3(int(os.environ["KBENCH_ATTN_V3"])))
     _side = torch.cuda.Stream()  # graph capture needs a non-default stream
     torch.cuda.set_stream(_side)
     if which in ("attn", "all"):
