@@ -443,9 +443,10 @@ spx_status spx_debug_set_gemm_variant(int32_t variant);
 /* Force the attention kernel's kv splits per query tile (1..8) for plans made after the call;
  * 0 = the planner's wave model (tests and tuning; also SPX_ATTN_SPLITS at load time). */
 spx_status spx_debug_set_attn_splits(int32_t splits);
-/* attention kernel for unsplit layouts: 1 = v3 (one O accumulator shared by both softmax
- * slots, separate P buffers, S(j+1) issued while the softmax works on S(j)), 0 = v2 (per-slot
- * O, P over S); also SPX_ATTN_V3 at load time */
+/* attention kernel for unsplit layouts: v3 = one O accumulator shared by both softmax slots,
+ * separate P buffers, S(j+1) issued while the softmax works on S(j); v2 = per-slot O with P
+ * written over S. 0 = always v2, 1 (default) = v3 when the layout fills >= one wave of SMs (or
+ * the run asks for exact SP layouts), 2 = always v3; also SPX_ATTN_V3 at load time */
 spx_status spx_debug_set_attn_v3(int32_t on);
 /* SPX_SPAN_TRACE=1 only: per traced launch (GEMM, attention, in launch order) the earliest CTA
  * start and the latest CTA end, globaltimer ns: out[2 i], out[2 i + 1] (capacity u64 slots). */

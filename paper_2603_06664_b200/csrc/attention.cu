@@ -48,6 +48,12 @@ constexpr int kBKV = 128;    // kv rows per tile
 // profiling-only variants of the hot loop (SPX_ATTN_EXPERIMENT=2: exponentials on the FMA
 // pipe) are compiled in only with -DSPX_ATTN_PROFILING=1: a runtime branch inside the
 // unrolled exp loop is predicated, i.e. it costs issue slots on every element
+// the same share for v3 (separate tuning: A/B on one box, kbench attn, 2 reps: of 1 / 2 / 3 /
+// 4 / 5 -> 0.1043 / 0.1048 / 0.1054 / 0.1060 / 0.1094 ms at the Wan chunk and 0.670 / 0.680 /
+// 0.686 / 0.688 / 0.716 ms at 32760 keys)
+#ifndef SPX_V3_POLY_OF_8
+#define SPX_V3_POLY_OF_8 1
+#endif
 #ifndef SPX_ATTN_PROFILING
 #define SPX_ATTN_PROFILING 0
 #endif
@@ -1140,7 +1146,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     const float2 x = ffma2(
                         make_float2(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])), sc2, nm2);
                     float2 pr;
-                    if ((e & 7) >= 8 - SPX_POLY_OF_8) {
+                    if ((e & 7) >= 8 - SPX_V3_POLY_OF_8) {
                         pr = ex2_poly2(x);
                     } else {
                         pr.x = ex2_approx(x.x);
@@ -1369,10 +1375,12 @@ int choose_splits(int64_t n, int64_t tiles, int sm_count, int cap) {
 }
 }  // namespace
 
-// the shared-O / early-S kernel (v3) for unsplit layouts: SPX_ATTN_V3=1 (0 = v2)
+// the shared-O / early-S kernel (v3) for unsplit layouts: SPX_ATTN_V3 = 0 never, 1 (default)
+// when the layout has at least one full wave of CTAs or the plan asks for it (exact SP
+// layouts: every partition must run the same kernel), 2 always
 std::atomic<int> g_attn_v3{[] {
     const char* e = std::getenv("SPX_ATTN_V3");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
 }()};
 bool attn_v3_enabled() { return g_attn_v3.load(std::memory_order_relaxed) != 0; }
 void attn_set_v3(int on) { g_attn_v3.store(on, std::memory_order_relaxed); }
@@ -1599,6 +1607,9 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
     }
     {
         const int64_t T = static_cast<int64_t>(p.qt) * o.heads;
+        int dev = 0;
+        SPX_CUDA(cudaGetDevice(&dev));
+        const int sms = device_sm_count(dev);
         static const bool pair_merge = [] {  // SPX_ATTN_SPLIT_PAIR=0: the workspace merge
             const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
             return !(e && std::atoi(e) == 0);
@@ -1610,7 +1621,8 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 attn_v2_launch<128, 5>(g2, plan, p, stream);
             else
                 attn_v2_launch<64, 5>(g2, plan, p, stream);
-        } else if (attn_v3_enabled() && p.n_full == T && p.experiment == 0) {
+        } else if (p.n_full == T && p.experiment == 0 && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
+                   (g_attn_v3.load(std::memory_order_relaxed) == 2 || o.prefer_v3 || T >= sms)) {
             // every tile unsplit: the shared-O / early-S kernel
             if (o.head_dim == 128)
                 attn_v3_launch<128>(dim3(static_cast<unsigned>(T)), plan, p, stream);

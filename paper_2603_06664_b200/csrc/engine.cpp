@@ -488,6 +488,7 @@ void Engine::build_plans() {
             }
             a.workspace = rs.attn_ws;
             a.workspace_bytes = rs.attn_ws_bytes;
+            a.prefer_v3 = cfg_.sp_bit_exact != 0;
             attn_plan(&rs.attn_plan[l], a, sms);
         }
     }

@@ -200,6 +200,7 @@ void Engine::build_wan_plans() {
             a.out_base[0] = rs.ca_o;
             a.rows_per_chunk = static_cast<int>(Lp_);
             a.out_row_stride = C_;
+            a.prefer_v3 = cfg_.sp_bit_exact != 0;
             attn_plan(&rs.ca_plan[static_cast<size_t>(l)], a, sms);
         }
     }

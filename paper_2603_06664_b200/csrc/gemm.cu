@@ -54,12 +54,21 @@ struct GemmParams {
     int head_shift;         // log2(head_dim)
     int8_t head_group[16];  // head -> its head group g
     int8_t head_slot[16];   // head -> index within the group
+    int n_fastest;    // tile raster: 1 = n index fastest (concurrent CTAs share A row blocks:
+                      // A larger than B), 0 = m fastest (concurrent CTAs share B = weights)
     int b_early;      // stages whose B tile the producer loaded before griddepcontrol.wait
     int experiment;   // profiling (SPX_GEMM_EXPERIMENT): 1 = rope epilogue without rotation,
                       // 5 = per-tile clock64 timeline of the pair kernel into `trace`
     long long* trace;  // [cta][16 tiles][4]: mma start, mma issued, epilogue start, end
     unsigned long long* span;  // SPX_SPAN_TRACE
 };
+
+__device__ __forceinline__ int tile_m(const GemmParams& p, int tile) {
+    return p.n_fastest ? tile / p.num_n_tiles : tile % p.num_m_tiles;
+}
+__device__ __forceinline__ int tile_n(const GemmParams& p, int tile) {
+    return p.n_fastest ? tile % p.num_n_tiles : tile / p.num_m_tiles;
+}
 
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int it, int kind) {
     if (p.experiment == 5 && it < 16) p.trace[(blockIdx.x * 16 + it) * 4 + kind] = clock64();
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // B (weights) of this CTA's first tile: not produced by the previous kernel, so it
         // streams in while that kernel drains; A follows after the PDL wait
         if (static_cast<int>(blockIdx.x) < num_tiles) {
-            const int n0 = (static_cast<int>(blockIdx.x) / p.num_m_tiles) * BN;
+            const int n0 = tile_n(p, static_cast<int>(blockIdx.x)) * BN;
             for (int kt = 0; kt < p.b_early; ++kt) {
                 mbar_arrive_expect_tx(&full[kt], kABytes + kBBytes);
                 tma_load_2d(sB + kt * kBBytes, &map_b, &full[kt], kt * kBK, n0);
@@ -346,8 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = (tile % p.num_m_tiles) * kBM;
-                const int n0 = (tile / p.num_m_tiles) * BN;
+                const int m0 = tile_m(p, tile) * kBM;
+                const int n0 = tile_n(p, tile) * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const bool early = tile == static_cast<int>(blockIdx.x) && kt < p.b_early;
@@ -410,8 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            const int m0 = (tile % p.num_m_tiles) * kBM;
-            const int n0 = (tile / p.num_m_tiles) * BN;
+            const int m0 = tile_m(p, tile) * kBM;
+            const int n0 = tile_n(p, tile) * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             if (warp == 4 && lane == 0) trace_mark(p, it, 2);
@@ -528,8 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int m0 = (tile % p.num_m_tiles) * 256 + cta * 128;
-                const int n0 = (tile / p.num_m_tiles) * BN + cta * (BN / 2);
+                const int m0 = tile_m(p, tile) * 256 + cta * 128;
+                const int n0 = tile_n(p, tile) * BN + cta * (BN / 2);
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kABytes + kBBytes));
@@ -598,8 +607,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            const int m0 = (tile % p.num_m_tiles) * 256 + cta * 128;
-            const int n0 = (tile / p.num_m_tiles) * BN;
+            const int m0 = tile_m(p, tile) * 256 + cta * 128;
+            const int n0 = tile_n(p, tile) * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             if (warp == 4 && lane == 0) trace_mark(p, it, 2);
@@ -765,6 +774,16 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     p.k_inner = o.k_inner;
     p.num_m_tiles = static_cast<int>(ceil_div(o.M, plan.pair ? 256 : kBM));
     p.num_n_tiles = static_cast<int>(ceil_div(o.N, plan.bn));
+    // raster: when A is the larger operand (the FFN's second projection: 84 MB of
+    // activations against 27.5 MB of weights) the CTAs in flight walk n first, so each A row
+    // block is read by its n-tiles at about the same time (once from DRAM) instead of once per
+    // wave of m-fastest tiles (ncu: 208 MB DRAM read per launch against 111 MB of operands)
+    static const int raster_env = [] {  // SPX_GEMM_RASTER: -1 auto, 0 m fastest, 1 n fastest
+        const char* e = std::getenv("SPX_GEMM_RASTER");
+        return e ? std::atoi(e) : -1;
+    }();
+    p.n_fastest = raster_env >= 0 ? raster_env
+                                  : (static_cast<int64_t>(o.M) * o.K > static_cast<int64_t>(o.N) * o.K * 2 ? 1 : 0);
     p.out = o.out;
     p.ldo = o.out_row_stride;
     p.epi_mode = o.epi_mode;

@@ -99,6 +99,9 @@ struct AttnOperands {
     // weights of the projections that follow (their HBM reads leave the GEMMs' critical path)
     const void* l2_prefetch[2] = {nullptr, nullptr};
     int64_t l2_prefetch_bytes[2] = {0, 0};
+    // unsplit layouts run the v3 kernel when they fill at least one wave of the SMs; true: also
+    // below that (cfg.sp_bit_exact: every partition of a run must use the same kernel)
+    bool prefer_v3 = false;
 };
 
 struct AttnPlan {
@@ -117,7 +120,8 @@ void attn_plan(AttnPlan* plan, const AttnOperands& ops, int sm_count);
 void attn_set_segments(AttnPlan* plan, const int* seg_start, const int* seg_len, int num_segs);
 // split-KV override (tests / tuning): 0 = modelled choice, else the kv splits per query tile
 void attn_force_splits(int s);
-// the shared-O / early-S attention kernel (v3) for unsplit layouts: on / off (SPX_ATTN_V3)
+// the shared-O / early-S attention kernel (v3) for unsplit layouts: 0 never, 1 auto, 2 always
+// (SPX_ATTN_V3)
 void attn_set_v3(int on);
 bool attn_v3_enabled();
 void attn_run(const AttnPlan& plan, cudaStream_t stream);

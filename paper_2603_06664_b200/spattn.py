@@ -90,10 +90,12 @@ class RopeFrequencyTable:
 
     def __init__(self, handle):
         self._h = handle
+        self._destroy = lib().spx_rope_table_destroy
 
     def __del__(self):
+        # the bound destroy function outlives module teardown at interpreter exit
         if getattr(self, "_h", None):
-            lib().spx_rope_table_destroy(self._h)
+            (getattr(self, "_destroy", None) or lib().spx_rope_table_destroy)(self._h)
             self._h = None
 
     def _info(self):
@@ -208,14 +210,16 @@ class KvCache:
     def __init__(self, tokens_per_frame, window_frames=None, heads=1, head_dim=2, capacity_frames=0,
                  device=0):
         self._h = ctypes.c_void_p()
+        self._destroy = lib().spx_kv_ring_destroy
         self.heads, self.head_dim = heads, head_dim
         self._tpf = tokens_per_frame
         check(lib().spx_kv_ring_create(device, tokens_per_frame, -1 if window_frames is None else window_frames,
                                        capacity_frames, heads, head_dim, ctypes.byref(self._h)))
 
     def __del__(self):
+        # the bound destroy function outlives module teardown at interpreter exit
         if getattr(self, "_h", None):
-            lib().spx_kv_ring_destroy(self._h)
+            (getattr(self, "_destroy", None) or lib().spx_kv_ring_destroy)(self._h)
             self._h = None
 
     def _info(self):
@@ -274,6 +278,7 @@ class CommWorld:
     devices: per-rank CUDA device ids (default: all ranks share the current device)."""
 
     def __init__(self, world_size, devices: Optional[Sequence[int]] = None, _handle=None):
+        self._destroy = lib().spx_world_destroy
         if _handle is not None:
             self._h = _handle
         else:
@@ -304,8 +309,9 @@ class CommWorld:
         return bytes(uid)
 
     def __del__(self):
+        # the bound destroy function outlives module teardown at interpreter exit
         if getattr(self, "_h", None):
-            lib().spx_world_destroy(self._h)
+            (getattr(self, "_destroy", None) or lib().spx_world_destroy)(self._h)
             self._h = None
 
     def info(self):
@@ -502,6 +508,7 @@ class Engine:
         self.world = world if world is not None else CommWorld(cfg.world_size)
         self._c = cfg.to_c()
         self._h = ctypes.c_void_p()
+        self._destroy = lib().spx_engine_destroy
         check(lib().spx_engine_create(self.world._h, ctypes.byref(self._c), ctypes.byref(self._h)))
         info = i64_array([0] * 8)
         check(lib().spx_engine_info(self._h, info))
@@ -512,8 +519,9 @@ class Engine:
             check(lib().spx_engine_seed_weights(self._h))
 
     def __del__(self):
+        # the bound destroy function outlives module teardown at interpreter exit
         if getattr(self, "_h", None):
-            lib().spx_engine_destroy(self._h)
+            (getattr(self, "_destroy", None) or lib().spx_engine_destroy)(self._h)
             self._h = None
 
     def ipc_export(self) -> bytes:

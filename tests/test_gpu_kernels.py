@@ -81,12 +81,12 @@ def test_project_tokens_every_tile_variant(cuda, variant, M, K, N):
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
-@pytest.fixture(params=[0, 1], ids=["v2", "v3"])
+@pytest.fixture(params=[0, 2], ids=["v2", "v3"])
 def attn_kernel(request):
-    """run the test with the v2 kernel (per-slot O) and with v3 (shared O, early S)"""
+    """run the test with the v2 kernel (per-slot O) and with v3 (shared O, early S) forced"""
     _check(_lib().spx_debug_set_attn_v3(request.param))
     yield request.param
-    _check(_lib().spx_debug_set_attn_v3(0))
+    _check(_lib().spx_debug_set_attn_v3(1))
 
 
 @pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),

@@ -160,8 +160,9 @@ def test_c2_sp_default_layout_vs_fp64(cuda, world, parity_log, c2_two_chunks_ora
     148 SMs (P = 2: 222 tiles, P = 8: 57 tiles) attention splits kv ranges over CTAs, which
     changes the fp32 summation order, so the latents are not bit-identical to P = 1 (north_star
     asks bit-exactness for indices / permutations, a stated bf16 tolerance for activations).
-    Each P is held to the same bar as P = 1 against the fp64 oracle; P = 4 (111 tiles, no split)
-    stays bit-identical to P = 1."""
+    Each P is held to the same bar as P = 1 against the fp64 oracle. (P = 4 does not split, but
+    its single wave of 111 tiles runs the v2 attention kernel while P = 1's three waves run v3:
+    also not bit-identical; sp_bit_exact pins one kernel and one layout.)"""
     s = spattn()
     got = device_out(s.Engine(cfg(2, 30, 4, world=world)))
     free_gpu()
@@ -170,8 +171,6 @@ def test_c2_sp_default_layout_vs_fp64(cuda, world, parity_log, c2_two_chunks_ora
     base = device_out(s.Engine(cfg(2, 30, 4)))
     parity_log(rel_l2_vs_p1=[rel_l2(got[b], base[b]) for b in range(2)],
                identical_to_p1=bool(np.array_equal(got, base)), world=world)
-    if world == 4:
-        assert np.array_equal(got, base)
 
 
 def _scaled_weights(layers, scale_qk, seed):
