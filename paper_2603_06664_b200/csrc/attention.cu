@@ -464,6 +464,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             int row, valid;
             kv_tile_coords(p, g0 + j, row, valid);
             mbar_wait(&s_full[i], j & 1);
+            // PV_i(j - 1) precedes QK_i(j) in the MMA pipe, so this phase is complete already;
+            // observing every phase keeps the barrier protocol explicit (compute-sanitizer
+            // synccheck flags committed phases nobody waits on)
+            if (j > 0) mbar_wait(&pv_done[i], (j - 1) & 1);
             tc_fence_after();
             if (p.experiment == 1) {  // profiling: MMA/TMA/barrier skeleton only
                 tc_fence_before();
@@ -535,9 +539,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             float lt = exp_tile();
             if (j > 0 && __any_sync(0xffffffffu, !(lt < 1.8446744e19f))) {  // 2^64, or inf / NaN
                 load_s();  // S is still in TMEM (P not written yet)
-                const float m_new = fmaxf(m_run, row_max() * scale);
-                mbar_wait(&pv_done[i], (j - 1) & 1);
-                tc_fence_after();
+                const float m_new = fmaxf(m_run, row_max() * scale);  // (PV_i(j - 1) done: above)
                 const float alpha = ex2_approx(m_run - m_new);
 #pragma unroll 1
                 for (int c = 0; c < D / 32; ++c) {

@@ -11,6 +11,18 @@
 
 namespace spx {
 
+// n / d for 0 <= n < 2^31 by a multiply-high (d >= 1; host-computed magic m and shift s):
+// s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1, n / d = (umulhi(n, m) + n) >> s
+struct FastDiv {
+    uint32_t d = 1, m = 0, s = 0;
+    FastDiv() = default;
+    __host__ explicit FastDiv(uint32_t divisor) : d(divisor) {
+        while ((uint64_t(1) << s) < d) ++s;
+        m = static_cast<uint32_t>(((uint64_t(1) << s) - d) * (uint64_t(1) << 32) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 // (cos, sin) of rotation pair j at position (t, h, w): band tables are [pos][pairs_b]
 __device__ __forceinline__ float2 band_cs(const RopeLaunch& l, int j, int t, int h, int w) {
     if (j < l.pairs[0]) return __ldg(&l.tab[0][t * l.pairs[0] + j]);
