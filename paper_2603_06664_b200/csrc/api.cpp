@@ -1037,6 +1037,8 @@ spx_status spx_debug_gemm_trace(int64_t* out, int64_t n) {
         SPX_CUDA(cudaDeviceSynchronize());
         SPX_CUDA(cudaMemcpy(out, gemm_trace_buffer(), static_cast<size_t>(n) * 8,
                             cudaMemcpyDeviceToHost));
+        // read-and-clear: the next traced launch starts from an empty buffer
+        SPX_CUDA(cudaMemset(gemm_trace_buffer(), 0, 1024 * 16 * 4 * sizeof(int64_t)));
     });
 }
 

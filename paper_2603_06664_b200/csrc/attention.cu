@@ -100,6 +100,19 @@ __device__ __forceinline__ void attn_mark(const AttnParams& p, int k) {
     const int64_t me = (static_cast<int64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     if (me < 1024) p.trace[me * 64 + k] = clock64();
 }
+// profiling (SPX_ATTN_EXPERIMENT=5): global start (slot 7) / end (slot 8) in globaltimer ns and
+// the SM id (slot 9) of this CTA, for a per-SM timeline across CTAs
+__device__ __forceinline__ void attn_mark_global(const AttnParams& p, int k) {
+    if (p.experiment != 5) return;
+    const int64_t me = (static_cast<int64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (me >= 1024) return;
+    p.trace[me * 64 + k] = static_cast<long long>(globaltimer_ns());
+    if (k == 7) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[me * 64 + 9] = smid;
+    }
+}
 
 // this CTA's share of the L2 prefetch ranges, 16 KB bulk prefetches (no smem, no barrier)
 __device__ __forceinline__ void l2_prefetch_share(const AttnParams& p) {
@@ -289,7 +302,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int lane = threadIdx.x % 32;
     pdl_trigger();
     span_begin(p.span);
-    if (threadIdx.x == 0) attn_mark(p, 4);  // CTA entry
+    if (threadIdx.x == 0) {
+        attn_mark(p, 4);  // CTA entry
+        attn_mark_global(p, 7);
+    }
     int q_tile, head, split, ns;
     if constexpr (kSplitPair) {
         const int t = static_cast<int>(blockIdx.x) >> 1;
@@ -859,7 +875,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             }
         }
     }
-    if (threadIdx.x == 128) attn_mark(p, 3);
+    if (threadIdx.x == 128) {
+        attn_mark(p, 3);
+        attn_mark_global(p, 8);
+    }
     tc_fence_before();
     if constexpr (kSplitPair)  // mode 5: split 1's smem is read by its bulk copy
         cluster_sync_all();
@@ -950,6 +969,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const int lane = threadIdx.x % 32;
     pdl_trigger();
     span_begin(p.span);
+    if (threadIdx.x == 0) {
+        attn_mark(p, 4);  // CTA entry
+        attn_mark_global(p, 7);
+    }
     const int t_idx = static_cast<int>(blockIdx.x);
     const int q_tile = t_idx % p.qt;
     const int head = t_idx / p.qt;
@@ -982,6 +1005,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t t_O = tmem_base + 256;
     pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
+    if (threadIdx.x == 0) attn_mark(p, 0);
 
     if (warp < 4) {
         setmaxnreg_dec56();
@@ -1179,6 +1203,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tc_fence_after();
         }
         if (ovf) s_ovf = 1;
+        if (threadIdx.x == 128) attn_mark(p, 1);  // softmax loop done
         // ---------------- epilogue: O / (l0 + l1), rows staged in the idle Q smem ----------------
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
@@ -1272,6 +1297,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     tc_fence_before();
     __syncthreads();
     span_end(p.span);
+    if (threadIdx.x == 128) {
+        attn_mark(p, 3);
+        attn_mark_global(p, 8);
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
@@ -1616,14 +1645,14 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
             return !(e && std::atoi(e) == 0);
         }();
-        if (pair_merge && p.n_full == 0 && p.splits == 2 && p.experiment != 5) {
+        if (pair_merge && p.n_full == 0 && p.splits == 2) {
             // every tile in 2 splits: the two CTAs of a cluster merge through DSMEM
             const dim3 g2(static_cast<unsigned>(2 * T));
             if (o.head_dim == 128)
                 attn_v2_launch<128, 5>(g2, plan, p, stream);
             else
                 attn_v2_launch<64, 5>(g2, plan, p, stream);
-        } else if (p.n_full == T && p.experiment == 0 && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
+        } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
                    (g_attn_v3.load(std::memory_order_relaxed) == 2 || o.prefer_v3 || T >= sms)) {
             // every tile unsplit: the shared-O / early-S kernel
             if (o.head_dim == 128)

@@ -71,7 +71,7 @@ __device__ __forceinline__ int tile_n(const GemmParams& p, int tile) {
 }
 
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int it, int kind) {
-    if (p.experiment == 5 && it < 16) p.trace[(blockIdx.x * 16 + it) * 4 + kind] = clock64();
+    if (p.experiment == 5 && it < 14) p.trace[(blockIdx.x * 16 + it) * 4 + kind] = clock64();
 }
 
 // kRopeSmem = false (single-CTA kernel, epilogues without RoPE): the table area is traded for

@@ -43,12 +43,18 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     uint8_t* ring = reinterpret_cast<uint8_t*>(s_mod + 4 * nvec);
     pdl_trigger();
     if (threadIdx.x == 0) row_pipe_init(bars, sh.stages);
+    __syncthreads();
+    if (threadIdx.x / 32 == kPipeWarps) {  // producer: x was written by the previous kernel
+        pdl_wait();
+        row_pipe_produce(reinterpret_cast<const uint8_t*>(x), static_cast<int64_t>(dim) * 2, rows, sh, ring, bars);
+        return;
+    }
     // constant modulation (uploaded weights) is staged before the PDL wait, overlapping the
     // previous kernel's tail; a per-step modulation written by a kernel (the Wan timestep
-    // embedding) only after it
+    // embedding) only after it. Either way the row reads are already streaming.
     if (mod_from_kernel) pdl_wait();
     const float one = affine ? 0.0f : 1.0f;
-    for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nvec * 4; i += kPipeWarps * 32) {
         const int v = i / 4, q = i % 4;
         const float* srcp = (q < 2 ? shift : scale) + v * 8 + (q & 1) * 4;
         float4 m = __ldg(reinterpret_cast<const float4*>(srcp));
@@ -60,13 +66,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
         }
         s_mod[i] = m;
     }
-    __syncthreads();
-    if (!mod_from_kernel) pdl_wait();  // x was written by the previous kernel
+    row_pipe_consumer_sync();
+    if (!mod_from_kernel) pdl_wait();  // y may still be read by the previous kernel
     // two rows per step (a stage holds rb >= 2 rows of a C <= 2048 row): the modulation vectors
     // are read from shared memory once for both; packed f32x2 math, two-pass variance from the
     // registers; y = x a + b with a = rstd (1 + scale), b = shift - mean a
-    row_pipe_run(reinterpret_cast<const uint8_t*>(x), static_cast<int64_t>(dim) * 2, rows, sh, ring, bars,
-                 [&](int r0, int n, const uint8_t* stage, int lane) {
+    row_pipe_consume(rows, sh, ring, bars, [&](int r0, int n, const uint8_t* stage, int lane) {
 #pragma unroll 1
       for (int ri = 0; ri < n; ri += 2) {
         const bool two = ri + 1 < n;

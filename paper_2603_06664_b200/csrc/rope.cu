@@ -125,12 +125,20 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     uint8_t* ring = reinterpret_cast<uint8_t*>(s_nw + (NORM ? 4 * nvec : 0));
     pdl_trigger();
     if (threadIdx.x == 0) row_pipe_init(bars, sh.stages);
-    for (int i = threadIdx.x; i < 8 * 17; i += blockDim.x) {
+    __syncthreads();
+    if (threadIdx.x / 32 == kPipeWarps) {  // producer: the rows were written by the QKV projection
+        pdl_wait();
+        row_pipe_produce(reinterpret_cast<const uint8_t*>(l.in), l.in_row_stride * 2, static_cast<int>(l.rows),
+                         sh, ring, bars);
+        return;
+    }
+    // consumers: per-CTA constants while the first rows stream in
+    for (int i = threadIdx.x; i < 8 * 17; i += kPipeWarps * 32) {
         const int g = i / 17, j = i % 17;
         s_dst[i] = j == 0 ? l.dst.q[g] : (j <= 8 ? l.dst.k[g][j - 1] : l.dst.v[g][j - 9]);
     }
     if constexpr (NORM) {  // constant weights: staged while the previous kernel drains
-        for (int i = threadIdx.x; i < (KV ? 2 : 1) * nvec; i += blockDim.x) {
+        for (int i = threadIdx.x; i < (KV ? 2 : 1) * nvec; i += kPipeWarps * 32) {
             const bf16* wsrc = i < nvec ? l.norm_w_q + 8 * i : l.norm_w_k + 8 * (i - nvec);
             const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wsrc));
             s_nw[2 * i] = make_float4(bf16_lo(wv.x), bf16_lo(wv.y), bf16_lo(wv.z), bf16_lo(wv.w));
@@ -170,10 +178,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
         tab_e[e] = l.tab[b] + j;
         stride_e[e] = l.pairs[b];
     }
-    __syncthreads();
-    pdl_wait();  // the input rows were written by the previous kernel (the QKV projection)
-    row_pipe_run(reinterpret_cast<const uint8_t*>(l.in), l.in_row_stride * 2, static_cast<int>(l.rows), sh,
-                 ring, bars, [&](int r0, int n, const uint8_t* stage, int lane_) {
+    row_pipe_consumer_sync();
+    pdl_wait();  // the destinations may still be read by the previous kernels
+    row_pipe_consume(static_cast<int>(l.rows), sh, ring, bars, [&](int r0, int n, const uint8_t* stage, int lane_) {
 #pragma unroll 1
       for (int ri = 0; ri < n; ++ri) {
         const int row = r0 + ri;

@@ -98,45 +98,59 @@ __device__ __forceinline__ void stg128(void* p, uint4 v) {
                  : "memory");
 }
 
-// Runs the pipeline; fn(r0, n, const uint8_t* stage_smem, lane) is called by the consumer warp
-// that owns the block of rows [r0, r0 + n) (n <= rb, rows row_bytes apart in shared memory). CTA c streams blocks b = c, c + gridDim.x, ... of rb rows; its k-th block lands in
-// stage k % stages and is processed by warp k % kPipeWarps, so 15 stages are computed at a time
-// while the producer keeps the rest of the ring loading. `in` rows are `in_stride` bytes apart
-// (one bulk copy per block when equal to row_bytes). bars: 2 * kPipeMaxStages uint64_t of
-// shared memory (row_pipe_init), ring: stages * rb * row_bytes bytes (16-byte aligned). The
-// caller executes griddepcontrol.wait (or not) before calling. Every thread of the CTA calls.
+// The pipeline, in two halves run by different warps. fn(r0, n, const uint8_t* stage_smem, lane)
+// is called by the consumer warp that owns the block of rows [r0, r0 + n) (n <= rb, rows
+// row_bytes apart in shared memory). CTA c streams blocks b = c, c + gridDim.x, ... of rb rows;
+// its k-th block lands in stage k % stages and is processed by warp k % kPipeWarps, so 15
+// stages are computed at a time while the producer keeps the rest of the ring loading. `in`
+// rows are `in_stride` bytes apart (one bulk copy per block when equal to row_bytes). bars:
+// 2 * kPipeMaxStages uint64_t of shared memory (row_pipe_init, made visible by a CTA barrier
+// before either half starts), ring: stages * rb * row_bytes bytes (16-byte aligned).
+//
+// The producer warp (warp kPipeWarps) starts streaming as soon as the barriers exist (after its
+// own griddepcontrol.wait when the rows come from the previous kernel), while the consumer
+// warps stage their per-CTA constants; the consumers then sync among themselves only
+// (row_pipe_consumer_sync), so the constant staging overlaps the first reads.
+__device__ __forceinline__ void row_pipe_produce(const uint8_t* in, int64_t in_stride, int rows,
+                                                 const RowPipeShape& sh, uint8_t* ring, uint64_t* bars) {
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kPipeMaxStages;
+    if (threadIdx.x % 32 != 0) return;
+    const int nblk = (rows + sh.rb - 1) / sh.rb;
+    const uint32_t stage_bytes = static_cast<uint32_t>(sh.rb) * sh.row_bytes;
+    int k = 0;
+    for (int b = static_cast<int>(blockIdx.x); b < nblk; b += static_cast<int>(gridDim.x), ++k) {
+        const int s = k % sh.stages;
+        mbar_wait(&empty[s], ((k / sh.stages) & 1) ^ 1);
+        const int r0 = b * sh.rb;
+        const int n = min(sh.rb, rows - r0);
+        uint8_t* dst = ring + s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * sh.row_bytes);
+        if (in_stride == static_cast<int64_t>(sh.row_bytes)) {
+            bulk_load_g2s(dst, in + static_cast<int64_t>(r0) * in_stride, static_cast<uint32_t>(n) * sh.row_bytes,
+                          &full[s]);
+        } else {
+            for (int i = 0; i < n; ++i)
+                bulk_load_g2s(dst + i * sh.row_bytes, in + static_cast<int64_t>(r0 + i) * in_stride,
+                              sh.row_bytes, &full[s]);
+        }
+    }
+}
+
+// the consumer warps' barrier (named barrier 1; the producer never joins it)
+__device__ __forceinline__ void row_pipe_consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kPipeWarps * 32) : "memory");
+}
+
 template <class Fn>
-__device__ __forceinline__ void row_pipe_run(const uint8_t* in, int64_t in_stride, int rows,
-                                             const RowPipeShape& sh, uint8_t* ring, uint64_t* bars,
-                                             Fn&& fn) {
+__device__ __forceinline__ void row_pipe_consume(int rows, const RowPipeShape& sh, uint8_t* ring,
+                                                 uint64_t* bars, Fn&& fn) {
     uint64_t* full = bars;
     uint64_t* empty = bars + kPipeMaxStages;
     const int warp = static_cast<int>(threadIdx.x / 32);
     const int lane = static_cast<int>(threadIdx.x % 32);
     const int nblk = (rows + sh.rb - 1) / sh.rb;
     const uint32_t stage_bytes = static_cast<uint32_t>(sh.rb) * sh.row_bytes;
-    if (warp == kPipeWarps) {
-        if (lane == 0) {
-            int k = 0;
-            for (int b = static_cast<int>(blockIdx.x); b < nblk; b += static_cast<int>(gridDim.x), ++k) {
-                const int s = k % sh.stages;
-                mbar_wait(&empty[s], ((k / sh.stages) & 1) ^ 1);
-                const int r0 = b * sh.rb;
-                const int n = min(sh.rb, rows - r0);
-                uint8_t* dst = ring + s * stage_bytes;
-                mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * sh.row_bytes);
-                if (in_stride == static_cast<int64_t>(sh.row_bytes)) {
-                    bulk_load_g2s(dst, in + static_cast<int64_t>(r0) * in_stride,
-                                  static_cast<uint32_t>(n) * sh.row_bytes, &full[s]);
-                } else {
-                    for (int i = 0; i < n; ++i)
-                        bulk_load_g2s(dst + i * sh.row_bytes, in + static_cast<int64_t>(r0 + i) * in_stride,
-                                      sh.row_bytes, &full[s]);
-                }
-            }
-        }
-        return;
-    }
     int k = warp;
 #pragma unroll 1
     for (int b = static_cast<int>(blockIdx.x) + warp * static_cast<int>(gridDim.x); b < nblk;

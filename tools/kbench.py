@@ -92,6 +92,54 @@ def gemm(iters):
                           "torch_ms": round(ref_ms, 4)}), flush=True)
 
 
+def gemm_variants(iters):
+    """every tile variant (spx_debug_set_gemm_variant) against the planner's choice and torch"""
+    shapes = [(4680, 1536, 4608), (4680, 1536, 1536), (2340, 1536, 4608), (2340, 1536, 1536),
+              (1170, 1536, 4608), (1170, 1536, 1536), (585, 1536, 4608), (585, 1536, 1536),
+              (585, 1536, 8960), (585, 8960, 1536)]
+    only = os.environ.get("KBENCH_GEMM_SHAPES")
+    if only:
+        shapes = [tuple(int(v) for v in t.split("x")) for t in only.split(",")]
+    nv = 0
+    while lib().spx_debug_set_gemm_variant(nv) == 0:  # count the planner's variants
+        nv += 1
+    check(lib().spx_debug_set_gemm_variant(-1))
+    for M, K, N in shapes:
+        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+        y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        row = {"kernel": "gemm_variants", "M": M, "K": K, "N": N}
+        for v in list(range(nv)) + [-1]:
+            check(lib().spx_debug_set_gemm_variant(v))
+            ms = timeit(lambda: check(lib().spx_project_tokens(x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                                               M, K, N, stream_handle())), iters)
+            row["auto" if v < 0 else f"v{v}"] = round(ms * 1e3, 2)
+        check(lib().spx_debug_set_gemm_variant(-1))
+        row["torch_us"] = round(timeit(lambda: torch.matmul(x, w.t()), iters) * 1e3, 2)
+        row["auto_frac_peak"] = round(2.0 * M * N * K / (row["auto"] * 1e-6) / 1e12 / PEAK_TF, 3)
+        print(json.dumps(row), flush=True)
+
+
+def attn_splits(iters):
+    """attention at per-rank shapes, each forced kv split count 1..6 against the planner's"""
+    for sq, skv, H in ATTN_SHAPES:
+        D = 128
+        q = (torch.randn(1, sq, H, D, device="cuda") * 0.5).to(torch.bfloat16)
+        k = (torch.randn(1, skv, H, D, device="cuda") * 0.5).to(torch.bfloat16)
+        v = torch.randn(1, skv, H, D, device="cuda").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        row = {"kernel": "attn_splits", "sq": sq, "skv": skv, "heads": H}
+        for sp in [1, 2, 3, 4, 6, 0]:
+            check(lib().spx_debug_set_attn_splits(sp))
+            ms = timeit(lambda: check(lib().spx_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                          o.data_ptr(), 1, sq, skv, H, D, stream_handle())), iters)
+            row["auto" if sp == 0 else f"s{sp}"] = round(ms * 1e3, 2)
+        check(lib().spx_debug_set_attn_splits(0))
+        ideal = 4.0 * sq * skv * H * D / (PEAK_TF * 1e12) * 1e6
+        row["auto_frac_peak"] = round(ideal / row["auto"], 3)
+        print(json.dumps(row), flush=True)
+
+
 def rope(iters):
     tab = ctypes.c_void_p()
     split = (ctypes.c_int64 * 3)(22, 21, 21)
@@ -147,6 +195,10 @@ if __name__ == "__main__":
     torch.cuda.set_stream(_side)
     if which in ("attn", "all"):
         attn(iters)
+    if which == "gemmv":
+        gemm_variants(iters)
+    if which == "attnsplit":
+        attn_splits(iters)
     if which in ("gemm", "all"):
         gemm(iters)
     if which in ("rope", "all"):
