@@ -927,25 +927,46 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
 
 
 // =========================================================================================
-// v3: one 128-row query tile per CTA; the kv range is split between two softmax warpgroups
-// as in v2, but the two slots accumulate into ONE O (TMEM) with a common exponent offset (the
-// max over both slots' first tiles, exchanged once), which frees the TMEM for separate P
-// buffers:  S0 | S1 | O | P0 | P1  = 128 + 128 + 128 + 64 + 64 columns.
+// v3: the kv range of a 128-row query tile is split between two softmax warpgroups as in v2,
+// but the two slots accumulate into ONE O (TMEM) with a common exponent offset (the max over
+// both slots' first tiles, exchanged once), which frees the TMEM for separate P buffers:
+//   S0 | S1 | O | P0 | P1  = 128 + 128 + 128 + 64 + 64 columns.
 // With P no longer written over S, the MMA issues S_i(j+1) as soon as the softmax has loaded
 // S_i(j) into registers (s_free), so a slot's dependency chain per tile is softmax + PV
 // instead of softmax + PV + QK^T. MMA issue order (= the producer's ring order):
 //   QK0(0) QK1(0) | QK0(j+1) PV0(j) QK1(j+1) PV1(j) | ...
+// Persistent: a CTA walks query tiles blockIdx.x, blockIdx.x + gridDim.x, ... (grid = min(tiles,
+// SMs)). Q is double-buffered in shared memory and the barrier phases run on across tiles, so
+// the producer loads Q and the first K/V tiles of tile k+1, and the MMA issues its first
+// QK^T, while the softmax warps run the epilogue of tile k; O is handed over as soon as the
+// epilogue has it in registers (o_free). The CTA prologue (barriers, TMEM, descriptors) and
+// the launch gap between CTAs are paid once per SM instead of once per tile.
 // Overflow: the fixed offset covers logits up to offset + 64 (log2 units) exactly; if a later
 // tile's exponentials exceed 2^64 (or are not finite), the shared O cannot be rescaled
-// without stopping both slots, so the CTA flags it and recomputes its rows exactly on the
-// CUDA cores after the main loop (never taken for sane inputs; tested).
+// without stopping both slots, so the CTA flags it and recomputes that tile's rows exactly on
+// the CUDA cores after its main loop (never taken for sane inputs; tested).
 // =========================================================================================
+template <int D>
+struct SmemV3 {
+    static constexpr uint32_t kChunks = D / 64;
+    static constexpr uint32_t kTileBytes = kBKV * D * 2;
+    static constexpr uint32_t kSlots = D == 128 ? kSlotsV2 : 2 * kSlotsV2;
+    static constexpr uint32_t kQBytes = kBQ * D * 2;
+    static constexpr uint32_t kOffQ = 0;  // [2] query tiles (also the epilogue's row staging)
+    static constexpr uint32_t kOffRing = kOffQ + 2 * kQBytes;
+    static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
+    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done/s_free[2], o_free, q_free[2]
+    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 8 + 1 + 2;
+    static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
+    static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
+};
+
 template <int D>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v3_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    using L = SmemV2<D, 0>;
+    using L = SmemV3<D>;
     constexpr uint32_t kSlots = L::kSlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -953,14 +974,16 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint8_t* sQ = smem + L::kOffQ;
     uint8_t* ring = smem + L::kOffRing;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-    uint64_t* q_full = bars;
-    uint64_t* slot_full = bars + 1;
+    uint64_t* q_full = bars;                 // [2]
+    uint64_t* slot_full = bars + 2;
     uint64_t* slot_empty = slot_full + kSlots;
     uint64_t* s_full = slot_empty + kSlots;  // [2]
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* pv_done = p_full + 2;          // [2]
-    uint64_t* s_free = pv_done + 2;          // [2] (the merge / xfer slots of v2)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+    uint64_t* s_free = pv_done + 2;          // [2]
+    uint64_t* o_free = s_free + 2;           // the epilogue holds O in registers
+    uint64_t* q_free = o_free + 1;           // [2] the epilogue's row staging in Q buffer b is done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_free + 2);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
     __shared__ int s_ovf;
@@ -973,9 +996,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         attn_mark(p, 4);  // CTA entry
         attn_mark_global(p, 7);
     }
-    const int t_idx = static_cast<int>(blockIdx.x);
-    const int q_tile = t_idx % p.qt;
-    const int head = t_idx / p.qt;
+    const int num_tiles = p.qt * p.heads;
     const int n_total = p.total_tiles;
     const int n0 = (n_total + 1) / 2;
     const int n1 = n_total - n0;
@@ -984,7 +1005,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         tma_prefetch_desc(&map_q);
         tma_prefetch_desc(&map_k);
         tma_prefetch_desc(&map_v);
-        mbar_init(q_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&q_full[b], 1);
+            mbar_init(&q_free[b], 256);  // every softmax thread, after its last staging read
+        }
         for (uint32_t s = 0; s < kSlots; ++s) {
             mbar_init(&slot_full[s], 1);
             mbar_init(&slot_empty[s], 1);
@@ -995,6 +1019,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_init(&pv_done[i], 1);
             mbar_init(&s_free[i], 4);   // one arrival per softmax warp
         }
+        mbar_init(o_free, 8);  // one arrival per softmax warp
         s_ovf = 0;
         fence_mbar_init();
     }
@@ -1012,32 +1037,40 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         if (warp == 0 && lane == 0) {
             // ---------------- TMA producer: the MMA consumption order ----------------
             uint32_t t = 0;
-            mbar_arrive_expect_tx(q_full, kBQ * D * 2);
-#pragma unroll
-            for (int c = 0; c < (int)L::kChunks; ++c)
-                tma_load_3d(sQ + c * (kBQ * 128), &map_q, q_full, c * 64, head, q_tile * kBQ);
-            auto load = [&](bool is_v, int g) {
-                const uint32_t slot = t % kSlots;
-                const uint32_t ph = (t / kSlots) & 1;
-                mbar_wait(&slot_empty[slot], ph ^ 1);
-                mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
-                int row, valid;
-                kv_tile_coords(p, g, row, valid);
-                uint8_t* dst = ring + slot * L::kTileBytes;
+            int it = 0;
+            for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+                const int q_tile = tile % p.qt;
+                const int head = tile / p.qt;
+                const int b = it & 1;
+                if (it >= 2) mbar_wait(&q_free[b], ((it - 2) >> 1) & 1);  // tile it-2's staging done
+                mbar_arrive_expect_tx(&q_full[b], L::kQBytes);
 #pragma unroll
                 for (int c = 0; c < (int)L::kChunks; ++c)
-                    tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
-                                c * 64, head, row);
-                ++t;
-            };
-            load(false, 0);
-            if (n1 > 0) load(false, n0);
-            for (int j = 0; j < n0; ++j) {
-                if (j + 1 < n0) load(false, j + 1);
-                load(true, j);
-                if (j < n1) {
-                    if (j + 1 < n1) load(false, n0 + j + 1);
-                    load(true, n0 + j);
+                    tma_load_3d(sQ + b * L::kQBytes + c * (kBQ * 128), &map_q, &q_full[b], c * 64, head,
+                                q_tile * kBQ);
+                auto load = [&](bool is_v, int g) {
+                    const uint32_t slot = t % kSlots;
+                    const uint32_t ph = (t / kSlots) & 1;
+                    mbar_wait(&slot_empty[slot], ph ^ 1);
+                    mbar_arrive_expect_tx(&slot_full[slot], L::kTileBytes);
+                    int row, valid;
+                    kv_tile_coords(p, g, row, valid);
+                    uint8_t* dst = ring + slot * L::kTileBytes;
+#pragma unroll
+                    for (int c = 0; c < (int)L::kChunks; ++c)
+                        tma_load_3d(dst + c * (kBKV * 128), is_v ? &map_v : &map_k, &slot_full[slot],
+                                    c * 64, head, row);
+                    ++t;
+                };
+                load(false, 0);
+                if (n1 > 0) load(false, n0);
+                for (int j = 0; j < n0; ++j) {
+                    if (j + 1 < n0) load(false, j + 1);
+                    load(true, j);
+                    if (j < n1) {
+                        if (j + 1 < n1) load(false, n0 + j + 1);
+                        load(true, n0 + j);
+                    }
                 }
             }
         } else if (warp == 1) {
@@ -1045,10 +1078,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             const bool issuer = elect_one();
             constexpr uint32_t idesc_s = make_idesc_bf16(kBQ, kBKV, false, false);
             constexpr uint32_t idesc_o = make_idesc_bf16(kBQ, D, false, true);
-            const uint32_t q_addr = smem_u32(sQ);
             const uint32_t ring_addr = smem_u32(ring);
             uint32_t t = 0;
-            bool first_pv = true;
+            uint32_t gs0 = 0, gs1 = 0;  // S tiles issued per slot (all tiles of this CTA)
+            uint32_t gp0 = 0, gp1 = 0;  // PV tiles issued per slot
             auto take = [&]() {
                 const uint32_t slot = t % kSlots;
                 mbar_wait(&slot_full[slot], (t / kSlots) & 1);
@@ -1056,57 +1089,69 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 ++t;
                 return slot;
             };
-            auto issue_s = [&](int i) {
-                const uint32_t slot = take();
-                const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
-                if (issuer) {
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                        umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
-                                     make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
-                    }
-                    umma_commit(&s_full[i]);
-                    umma_commit(&slot_empty[slot]);
-                }
-                __syncwarp();
-            };
-            auto issue_pv = [&](int i, int j) {
-                const uint32_t slot = take();
-                mbar_wait(&p_full[i], j & 1);
-                tc_fence_after();
-                const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
-                const uint32_t t_p = tmem_base + 384 + i * 64;
-                if (issuer) {
-#pragma unroll
-                    for (int kk = 0; kk < kBKV / 16; ++kk)
-                        umma_bf16_ts(t_O, t_p + kk * 8,
-                                     make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
-                                     idesc_o, (first_pv && kk == 0) ? 0u : 1u);
-                    umma_commit(&pv_done[i]);
-                    umma_commit(&slot_empty[slot]);
-                }
-                first_pv = false;
-                __syncwarp();
-            };
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            issue_s(0);
-            if (n1 > 0) issue_s(1);
-            for (int j = 0; j < n0; ++j) {
-                if (j + 1 < n0) {
-                    mbar_wait(&s_free[0], j & 1);  // the softmax holds S0(j) in registers
-                    tc_fence_after();
-                    issue_s(0);
-                }
-                issue_pv(0, j);
-                if (j < n1) {
-                    if (j + 1 < n1) {
-                        mbar_wait(&s_free[1], j & 1);
+            int it = 0;
+            for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+                const int b = it & 1;
+                const uint32_t q_addr = smem_u32(sQ + b * L::kQBytes);
+                bool first_pv = true;
+                auto issue_s = [&](int i) {
+                    const uint32_t g = i == 0 ? gs0 : gs1;
+                    if (g > 0) {  // the softmax holds S_i(previous) in registers
+                        mbar_wait(&s_free[i], (g - 1) & 1);
                         tc_fence_after();
-                        issue_s(1);
                     }
-                    issue_pv(1, j);
+                    const uint32_t slot = take();
+                    const uint32_t k_addr = ring_addr + slot * L::kTileBytes;
+                    if (issuer) {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                            umma_bf16_ss(tmem_base + i * 128, make_desc_sw128(q_addr + off, 16, 1024),
+                                         make_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                        }
+                        umma_commit(&s_full[i]);
+                        umma_commit(&slot_empty[slot]);
+                    }
+                    if (i == 0)
+                        ++gs0;
+                    else
+                        ++gs1;
+                    __syncwarp();
+                };
+                auto issue_pv = [&](int i) {
+                    const uint32_t slot = take();
+                    mbar_wait(&p_full[i], (i == 0 ? gp0 : gp1) & 1);
+                    if (first_pv && it > 0) mbar_wait(o_free, (it - 1) & 1);  // tile it-1's O is read
+                    tc_fence_after();
+                    const uint32_t v_addr = ring_addr + slot * L::kTileBytes;
+                    const uint32_t t_p = tmem_base + 384 + i * 64;
+                    if (issuer) {
+#pragma unroll
+                        for (int kk = 0; kk < kBKV / 16; ++kk)
+                            umma_bf16_ts(t_O, t_p + kk * 8,
+                                         make_desc_sw128(v_addr + kk * 16 * 128, kBKV * 128, 1024),
+                                         idesc_o, (first_pv && kk == 0) ? 0u : 1u);
+                        umma_commit(&pv_done[i]);
+                        umma_commit(&slot_empty[slot]);
+                    }
+                    if (i == 0)
+                        ++gp0;
+                    else
+                        ++gp1;
+                    first_pv = false;
+                    __syncwarp();
+                };
+                mbar_wait(&q_full[b], (it >> 1) & 1);
+                tc_fence_after();
+                issue_s(0);
+                if (n1 > 0) issue_s(1);
+                for (int j = 0; j < n0; ++j) {
+                    if (j + 1 < n0) issue_s(0);
+                    issue_pv(0);
+                    if (j < n1) {
+                        if (j + 1 < n1) issue_s(1);
+                        issue_pv(1);
+                    }
                 }
             }
         }
@@ -1122,6 +1167,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const int n = i == 0 ? n0 : n1;
         const int g0 = i == 0 ? 0 : n0;
         const float scale = p.scale_log2;
+        constexpr uint32_t kRowBytes = D * 2;
+        constexpr uint32_t kU = kRowBytes / 16;
+        int it = 0;
+        for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+        const int q_tile = tile % p.qt;
+        const int head = tile / p.qt;
+        const int b = it & 1;
+        const uint32_t gbase = static_cast<uint32_t>(it * n);  // this slot's kv tiles before this tile
         float m_run = -INFINITY;
         float l_run = 0.0f;
         bool ovf = false;
@@ -1130,9 +1183,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             named_bar_sync(1, 256);
         }
         for (int j = 0; j < n; ++j) {
+            const uint32_t G = gbase + static_cast<uint32_t>(j);
             int row, valid;
             kv_tile_coords(p, g0 + j, row, valid);
-            mbar_wait(&s_full[i], j & 1);
+            mbar_wait(&s_full[i], G & 1);
             tc_fence_after();
             uint32_t u[kBKV];
 #pragma unroll
@@ -1186,9 +1240,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             }
             ovf = ovf || !(lt < 1.8446744e19f);  // 2^64, or inf / NaN
             l_run += lt;
-            // P_i(j - 1) has been read by its PV before P_i(j) overwrites the buffer
+            // P_i(j - 1) has been read by its PV before P_i(j) overwrites the buffer (at j = 0
+            // the previous tile's epilogue waited for its last PV)
             if (j > 0) {
-                mbar_wait(&pv_done[i], (j - 1) & 1);
+                mbar_wait(&pv_done[i], (G - 1) & 1);
                 tc_fence_after();
             }
 #pragma unroll
@@ -1199,30 +1254,37 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             if (lane == 0) mbar_arrive(&p_full[i]);
         }
         if (n > 0) {
-            mbar_wait(&pv_done[i], (n - 1) & 1);
+            mbar_wait(&pv_done[i], (gbase + static_cast<uint32_t>(n) - 1) & 1);
             tc_fence_after();
         }
         if (ovf) s_ovf = 1;
-        if (threadIdx.x == 128) attn_mark(p, 1);  // softmax loop done
-        // ---------------- epilogue: O / (l0 + l1), rows staged in the idle Q smem ----------------
+        if (threadIdx.x == 128) attn_mark(p, 1);  // softmax loop done (last tile's)
+        // ---------------- epilogue: O / (l0 + l1), rows staged in this tile's Q buffer ----------------
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
         named_bar_sync(1, 256);  // both slots' last PVs are done; l and the flag are visible
         tc_fence_after();
         const float inv = 1.0f / (st_l[r] + st_l[128 + r]);
         const bool fallback = s_ovf != 0;
-        constexpr uint32_t kRowBytes = D * 2;
-        constexpr uint32_t kU = kRowBytes / 16;
-        const uint32_t s_base = smem_u32(smem);
+        // this slot's half of the O columns, 32 at a time: normalise, stage in this tile's Q
+        // buffer (every QK^T of the tile is done); O is handed to the next tile's PV as soon as
+        // the last chunk is in registers
+        const uint32_t s_base = smem_u32(sQ + b * L::kQBytes);
         if (!fallback) {
 #pragma unroll 1
-            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
+            for (int c = 0; c < D / 64; ++c) {
+                const int cc = i * (D / 64) + c;
                 uint32_t o[32];
-                tmem_ld32(t_O + lane_off + c * 32, o);
+                tmem_ld32(t_O + lane_off + cc * 32, o);
                 tmem_ld_wait();
+                if (c == D / 64 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(o_free);
+                }
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
-                    const uint32_t unit = static_cast<uint32_t>(c * 4 + v);
+                    const uint32_t unit = static_cast<uint32_t>(cc * 4 + v);
                     const uint32_t a = s_base + static_cast<uint32_t>(r) * kRowBytes +
                                        ((unit ^ (static_cast<uint32_t>(r) & (kU - 1))) << 4);
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
@@ -1234,6 +1296,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 }
             }
         } else {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(o_free);  // O is not read on this path
             // exact recompute of this thread's row, columns [i D/2, (i + 1) D/2), from global
             // memory with a running max (rare path; see the kernel comment)
             const int qi = q_tile * kBQ + r;
@@ -1273,7 +1338,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                              : "memory");
             }
         }
-        named_bar_sync(1, 256);
+        named_bar_sync(1, 256);  // staged rows visible; every thread has read s_ovf and st_l
+        if (threadIdx.x == 128) s_ovf = 0;  // re-armed for the next tile
         const int tid = static_cast<int>(threadIdx.x) - 128;
 #pragma unroll 1
         for (int idx = tid; idx < kBQ * static_cast<int>(kU); idx += 256) {
@@ -1293,6 +1359,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                          static_cast<int64_t>(head) * D;
             *reinterpret_cast<uint4*>(drow + uu * 8) = w;
         }
+        // this thread's staging reads are done: the producer may load tile it + 2's Q here
+        // (generic-proxy reads before an async-proxy write: the mbarrier orders them)
+        mbar_arrive(&q_free[b]);
+        }  // tiles
     }
     tc_fence_before();
     __syncthreads();
@@ -1314,10 +1384,10 @@ void attn_v3_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
         SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(SmemV2<D, 0>::kBytes)));
+                                      static_cast<int>(SmemV3<D>::kBytes)));
         done[dev & 63] = true;
     }
-    launch_pdl(attn_fwd_v3_kernel<D>, grid, dim3(kThreadsV2), SmemV2<D, 0>::kBytes, stream, plan.map_q,
+    launch_pdl(attn_fwd_v3_kernel<D>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, plan.map_q,
                plan.map_k, plan.map_v, p);
 }
 
@@ -1415,6 +1485,15 @@ std::atomic<int> g_attn_v3{[] {
 }()};
 bool attn_v3_enabled() { return g_attn_v3.load(std::memory_order_relaxed) != 0; }
 void attn_set_v3(int on) { g_attn_v3.store(on, std::memory_order_relaxed); }
+
+// SPX_ATTN_V3_PERSISTENT=0: one CTA per query tile (the pre-persistent launch shape; A/B)
+bool v3_persistent() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPX_ATTN_V3_PERSISTENT");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
 
 std::atomic<int> g_forced_splits{[] {  // tuning override: SPX_ATTN_SPLITS=<1..8>
     const char* e = std::getenv("SPX_ATTN_SPLITS");
@@ -1654,11 +1733,12 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 attn_v2_launch<64, 5>(g2, plan, p, stream);
         } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
                    (g_attn_v3.load(std::memory_order_relaxed) == 2 || o.prefer_v3 || T >= sms)) {
-            // every tile unsplit: the shared-O / early-S kernel
+            // every tile unsplit: the shared-O / early-S kernel, persistent over the tiles
+            const dim3 gv3(static_cast<unsigned>(std::min<int64_t>(T, v3_persistent() ? sms : T)));
             if (o.head_dim == 128)
-                attn_v3_launch<128>(dim3(static_cast<unsigned>(T)), plan, p, stream);
+                attn_v3_launch<128>(gv3, plan, p, stream);
             else
-                attn_v3_launch<64>(dim3(static_cast<unsigned>(T)), plan, p, stream);
+                attn_v3_launch<64>(gv3, plan, p, stream);
         } else {  // mode 0: 1-D grid, n_full unsplit tiles then the split ones
             const dim3 g1(static_cast<unsigned>(p.n_full + (T - p.n_full) * p.splits));
             if (o.head_dim == 128)

@@ -39,6 +39,11 @@ for shape in sys.argv[1:]:
     wait_epi0 = (t[:, 0, 2] - t[:, 0, 1]) * clk
     last = ntile - 1
     tail = np.array([(cend[i] - t[i, last[i], 3]) * clk for i in range(n)])
+    # the first CTA's marks relative to its start (us): per tile [mma start, mma issued, epi start, epi end]
+    seq = [[round(float((t[0, i, k] - c0[0]) * clk), 2) if t[0, i, k] else None for k in range(4)]
+           for i in range(int(ntile[0]))]
+    print(json.dumps({"cta0_tiles_us": seq, "cta0_prologue_end_us": round(float((cpro[0] - c0[0]) * clk), 2),
+                      "cta0_end_us": round(float((cend[0] - c0[0]) * clk), 2)}))
     print(json.dumps({
         "shape": shape, "ctas": n, "span_us": round(float(ge.max()), 2),
         "tiles_per_cta(max)": int(ntile.max()),
