@@ -45,8 +45,10 @@ names = ["qkv_gemm", "attention", "o_gemm"]
 per = len(sp) // (layers * steps)
 dur = sp[:, 1] - sp[:, 0]
 gap = np.concatenate([[0.0], sp[1:, 0] - sp[:-1, 1]])
+inc = np.concatenate([[0.0], sp[1:, 1] - sp[:-1, 1]])  # last-CTA end to last-CTA end: the kernel's share of the chunk
 res = {"kernels_per_call": per, "chunk_span_ms": float((sp[-1, 1] - sp[0, 0]) / 1e3)}
 for k in range(per):
     res[names[k] if per == 3 else f"k{k}"] = {"dur_us": round(float(dur[k::per].mean()), 2),
-                                              "gap_before_us": round(float(gap[k::per][1:].mean()), 2)}
+                                              "gap_before_us": round(float(gap[k::per][1:].mean()), 2),
+                                              "end_to_end_us": round(float(inc[k::per][1:].mean()), 2)}
 print(json.dumps(res))
