@@ -208,7 +208,8 @@ __device__ __forceinline__ bf16* chunk_base(const GemmParams& p, const ChunkDst&
 // 8 rows x 64 contiguous bytes (full sectors) instead of 32 rows x 16 bytes.
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, int lane, int col0,
                                                const uint32_t (&r)[32], uint32_t stage,
-                                               const RopeRow& rr = RopeRow{}) {
+                                               const RopeRow& rr = RopeRow{},
+                                               const uint4* res_pre = nullptr) {
     if (col0 >= p.N) return;  // warp-uniform
     const int row = row0 + lane;
     float f[32];
@@ -229,28 +230,40 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, in
         if (d.which < 2 && rr.valid) rope_rotate_chunk(p.rope, rr, d.d0, f);
     } else if (p.epi_mode == 1 && row < p.M) {
         const uint4* res = reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col0);
+        float g[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {  // the gate: broadcast float4 loads
+            const float4 gv = p.gate ? __ldg(reinterpret_cast<const float4*>(p.gate + col0 + j))
+                                     : make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+            g[j] = gv.x;
+            g[j + 1] = gv.y;
+            g[j + 2] = gv.z;
+            g[j + 3] = gv.w;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint4 rv = res[q];
+            const uint4 rv = res_pre ? res_pre[q] : res[q];
             const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 float2 rs = unpack_bf16x2(rw[e]);
                 const int j = q * 8 + e * 2;
-                const float g0 = p.gate ? p.gate[col0 + j] : 1.0f;
-                const float g1 = p.gate ? p.gate[col0 + j + 1] : 1.0f;
-                f[j] = rs.x + g0 * f[j];
-                f[j + 1] = rs.y + g1 * f[j + 1];
+                f[j] = rs.x + g[j] * f[j];
+                f[j + 1] = rs.y + g[j + 1] * f[j + 1];
             }
         }
     } else if (p.epi_mode == 3) {
         // GELU, tanh approximation (torch.nn.GELU(approximate="tanh"), the Wan FFN):
         // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+        // tanh on the SFU (tanh.approx.f32: ~2^-11 relative, below the bf16 output rounding);
+        // tanhf's software sequence made this epilogue cost 20 us on the 1536 -> 8960 FFN
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             const float x = f[j];
             const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
-            f[j] = 0.5f * x * (1.0f + tanhf(u));
+            float t;
+            asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+            f[j] = 0.5f * x * (1.0f + t);
         }
     }
 #pragma unroll
@@ -421,10 +434,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t aphase = (it >> 1) & 1;
             const int m0 = tile_m(p, tile) * kBM;
             const int n0 = tile_n(p, tile) * BN;
+            const int row = m0 + ew * 32 + lane;
+            if (p.epi_mode == 1) {
+                // residual epilogue: this lane's residual row segments are loaded before the
+                // accumulator is waited for (one L2 round trip per tile, overlapping the MMA,
+                // instead of one per 32-column slice on the epilogue's critical path)
+                constexpr int kS = BN / 64;
+                uint4 res_pre[kS][4];
+#pragma unroll
+                for (int ci = 0; ci < kS; ++ci) {
+                    const int col = n0 + (half * kS + ci) * 32;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        res_pre[ci][q] = (row < p.M && col < p.N)
+                                             ? reinterpret_cast<const uint4*>(p.residual + row * p.ldr + col)[q]
+                                             : make_uint4(0, 0, 0, 0);
+                }
+                mbar_wait(&tfull[acc], aphase);
+                tc_fence_after();
+                if (warp == 4 && lane == 0) trace_mark(p, it, 2);
+                const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+#pragma unroll
+                for (int ci = 0; ci < kS; ++ci) {
+                    const int c = half * kS + ci;
+                    uint32_t r[32];
+                    tmem_ld32(t_row + c * 32, r);
+                    tmem_ld_wait();
+                    epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, RopeRow{}, res_pre[ci]);
+                }
+            } else {
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             if (warp == 4 && lane == 0) trace_mark(p, it, 2);
-            const int row = m0 + ew * 32 + lane;
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
             if (p.epi_mode == 2 && row < p.M) rr = rope_row(p.rope, rope_l, s_rope, row);
@@ -435,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld32(t_row + c * 32, r);
                 tmem_ld_wait();
                 epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, rr);
+            }
             }
             tc_fence_before();
             __syncwarp();

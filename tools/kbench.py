@@ -120,6 +120,31 @@ def gemm_variants(iters):
         print(json.dumps(row), flush=True)
 
 
+def gemm_epilogues(iters):
+    """the projection epilogues at the Wan shapes: plain, + bias, residual + gate (in place, as
+    the engine runs it), GELU"""
+    for M, K, N in [(4680, 1536, 1536), (4680, 8960, 1536), (4680, 1536, 8960)]:
+        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+        y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        res = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+        bias = torch.randn(N, device="cuda") * 0.1
+        gate = torch.randn(N, device="cuda") * 0.1
+        row = {"kernel": "gemm_epilogues", "M": M, "K": K, "N": N}
+        cases = {"plain": (None, 0, None, None), "bias": (bias, 0, None, None),
+                 "residual_gate": (bias, 1, res, gate), "gelu": (bias, 3, None, None)}
+        for name, (b, epi, r, g) in cases.items():
+            out = r if r is not None else y
+            ms = timeit(lambda: check(lib().spx_project_tokens_ex(
+                x.data_ptr(), w.data_ptr(), out.data_ptr(), M, K, N,
+                b.data_ptr() if b is not None else None, epi,
+                r.data_ptr() if r is not None else None,
+                g.data_ptr() if g is not None else None,
+                stream_handle())), iters)
+            row[name + "_us"] = round(ms * 1e3, 2)
+        print(json.dumps(row), flush=True)
+
+
 def attn_splits(iters):
     """attention at per-rank shapes, each forced kv split count 1..6 against the planner's"""
     for sq, skv, H in ATTN_SHAPES:
@@ -197,6 +222,8 @@ if __name__ == "__main__":
         attn(iters)
     if which == "gemmv":
         gemm_variants(iters)
+    if which == "gemmepi":
+        gemm_epilogues(iters)
     if which == "attnsplit":
         attn_splits(iters)
     if which in ("gemm", "all"):
