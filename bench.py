@@ -381,31 +381,50 @@ def main():
     barrier()
     sync_fps = F * args.steps / max_over_ranks(time.perf_counter() - ts0)
 
+    def sampled(fn):
+        # clocks + throttle reasons of an extension section (its own nvidia-smi sampler), so a
+        # section that ran throttled is visible in its own object
+        smp = ClockSampler(device)
+        smp.start()
+        time.sleep(0.1)
+        ta = time.perf_counter()
+        res = fn()
+        smp.mark(ta, time.perf_counter())
+        c = smp.stop()
+        return res, {k: c.get(k) for k in ("sm_mhz", "sm_min_mhz", "reasons")}
+
     # ---- C3: 5 s 480P video = 7 chunks, unlimited KV window (the ring grows to 21 frames) ----
-    video = video_5s(run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
-                               noise_dev, out_dev, barrier, max_over_ranks, blocks=7))
+    video_ms, video_clk = sampled(lambda: run_video(args, new_engine, spattn, lib, check, ptr_array, world,
+                                                    world_size, noise_dev, out_dev, barrier, max_over_ranks,
+                                                    blocks=7))
+    video = video_5s(video_ms)
+    video["clocks"] = video_clk
     # ---- C5: 60 s 480P (80 chunks) with a 21-frame rolling window, kernels already warm ----
     long_video = None
     if not args.skip_long_video:
-        long_video = video_60s(run_video(args, new_engine, spattn, lib, check, ptr_array, world,
-                                         world_size, noise_dev, out_dev, barrier, max_over_ranks,
-                                         blocks=80,
-                                         window=21, warmup=False), 21)
+        lv_ms, lv_clk = sampled(lambda: run_video(args, new_engine, spattn, lib, check, ptr_array, world,
+                                                  world_size, noise_dev, out_dev, barrier, max_over_ranks,
+                                                  blocks=80, window=21, warmup=False))
+        long_video = video_60s(lv_ms, 21)
+        long_video["clocks"] = lv_clk
 
     # ---- Wan mode (extensions): QK-RMSNorm + adaLN modulation + gated residual, C2 chunk ----
-    wan_ms = run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
-                       noise_dev, out_dev, barrier, max_over_ranks, blocks=2, wan=True)
+    wan_ms, wan_clk = sampled(lambda: run_video(args, new_engine, spattn, lib, check, ptr_array, world,
+                                                world_size, noise_dev, out_dev, barrier, max_over_ranks,
+                                                blocks=2, wan=True))
     wan_block = {"workload": "C2 chunk with the Wan block's self-attention extensions: adaLN "
                              "LayerNorm+modulation (K1), QK-RMSNorm + Causal-RoPE (K3), gated "
                              "residual in the O-projection epilogue (no reference counterpart)",
                  "first_frame_latency_ms": wan_ms[0],
                  "latent_frames_per_s": 3 / (wan_ms[0] / 1e3),
-                 "chunk_ms": wan_ms, "note": "frames/s of the first chunk (C2); chunk 2 attends 6 frames"}
+                 "chunk_ms": wan_ms, "note": "frames/s of the first chunk (C2); chunk 2 attends 6 frames",
+                 "clocks": wan_clk}
 
     # ---- the full Wan2.1 block (cross-attention to 512 cached text tokens, GELU FFN 8960,
     # timestep adaLN; device-seeded synthetic weights), C2 chunk ----
-    full_ms = run_video(args, new_engine, spattn, lib, check, ptr_array, world, world_size,
-                        noise_dev, out_dev, barrier, max_over_ranks, blocks=2, wan_full=True)
+    full_ms, full_clk = sampled(lambda: run_video(args, new_engine, spattn, lib, check, ptr_array, world,
+                                                  world_size, noise_dev, out_dev, barrier, max_over_ranks,
+                                                  blocks=2, wan_full=True))
     Lp_full = L // world_size
     gf_layer = (8 * Lp_full * C * C + 4 * L * L * C / world_size   # self-attn GEMMs + attention (chunk 0)
                 + 4 * Lp_full * C * C + 4 * Lp_full * 512 * C        # cross-attn q/o GEMMs + attention
@@ -417,7 +436,7 @@ def main():
                             "steps, device-seeded synthetic weights (no reference counterpart)",
                 "first_frame_latency_ms": full_ms[0], "latent_frames_per_s": 3 / (full_ms[0] / 1e3),
                 "chunk_ms": full_ms, "gflop_per_layer_call_per_rank": gf_layer,
-                "tflops_per_rank": gf_layer * 120 / full_ms[0]}
+                "tflops_per_rank": gf_layer * 120 / full_ms[0], "clocks": full_clk}
 
     # ---- C4: Causal-RoPE microbench (rank-local rows vs the full sequence), HBM GB/s ----
     peaks, peak_src = load_peaks()

@@ -1341,11 +1341,22 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         named_bar_sync(1, 256);  // staged rows visible; every thread has read s_ovf and st_l
         if (threadIdx.x == 128) s_ovf = 0;  // re-armed for the next tile
         const int tid = static_cast<int>(threadIdx.x) - 128;
+        // output chunks of this tile's rows: with chunks of >= 128 rows a tile spans at most two,
+        // split at row `split` (no division per store); smaller chunks divide per row
+        const int r0 = q_tile * kBQ;
+        const int rpc = p.rows_per_chunk;
+        const int c0 = r0 / rpc;
+        const int split = (c0 + 1) * rpc - r0;
+        const int64_t ostride = p.out_row_stride;
+        bf16* base0 = p.out_base[c0] + static_cast<int64_t>(r0 - c0 * rpc) * ostride + static_cast<int64_t>(head) * D;
+        bf16* base1 = split < kBQ && c0 + 1 < 8
+                          ? p.out_base[c0 + 1] - static_cast<int64_t>(split) * ostride + static_cast<int64_t>(head) * D
+                          : base0;
 #pragma unroll 1
         for (int idx = tid; idx < kBQ * static_cast<int>(kU); idx += 256) {
             const int row = idx / static_cast<int>(kU);
             const uint32_t uu = static_cast<uint32_t>(idx) % kU;
-            const int q_row = q_tile * kBQ + row;
+            const int q_row = r0 + row;
             if (q_row >= p.sq) continue;
             uint4 w;
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -1353,10 +1364,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                          : "r"(s_base + static_cast<uint32_t>(row) * kRowBytes +
                                ((uu ^ (static_cast<uint32_t>(row) & (kU - 1))) << 4))
                          : "memory");
-            const int chunk = q_row / p.rows_per_chunk;
-            bf16* drow = p.out_base[chunk] +
-                         static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
-                         static_cast<int64_t>(head) * D;
+            bf16* drow;
+            if (rpc >= kBQ) {
+                drow = (row < split ? base0 : base1) + static_cast<int64_t>(row) * ostride;
+            } else {
+                const int chunk = q_row / rpc;
+                drow = p.out_base[chunk] + static_cast<int64_t>(q_row - chunk * rpc) * ostride +
+                       static_cast<int64_t>(head) * D;
+            }
             *reinterpret_cast<uint4*>(drow + uu * 8) = w;
         }
         // this thread's staging reads are done: the producer may load tile it + 2's Q here

@@ -1,6 +1,8 @@
 // engine.cpp -- see engine.hpp.
 #include "engine.hpp"
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1011,6 +1013,19 @@ void Engine::run_step(int64_t start, int64_t step) {
         const cudaError_t ce = cudaStreamEndCapture(rs.stream, &g);
         cudaError_t ie = cudaErrorUnknown;
         if (ok && ce == cudaSuccess && g) ie = cudaGraphInstantiateWithFlags(&sg.exec, g, 0);
+        static const bool graph_debug = std::getenv("SPX_GRAPH_DEBUG") != nullptr;
+        if (graph_debug && g) {  // profiling: how many of the captured edges kept PDL
+            size_t nn = 0, ne = 0;
+            cudaGraphGetNodes(g, nullptr, &nn);
+            cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne);
+            std::vector<cudaGraphNode_t> from(ne), to(ne);
+            std::vector<cudaGraphEdgeData> ed(ne);
+            size_t ne2 = ne;
+            cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne2);
+            size_t prog = 0;
+            for (size_t i = 0; i < ne2; ++i) prog += ed[i].type == cudaGraphDependencyTypeProgrammatic;
+            std::fprintf(stderr, "step graph: %zu nodes, %zu edges, %zu programmatic\n", nn, ne2, prog);
+        }
         if (g) cudaGraphDestroy(g);
         sg.launches = launch_count() - l0;
         count_launch(static_cast<int>(-sg.launches));  // captured, not launched
