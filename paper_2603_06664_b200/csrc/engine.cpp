@@ -461,6 +461,17 @@ void Engine::build_plans() {
             o.K = static_cast<int>(C_);
             o.b_constant = true;
             gemm_plan(&rs.o_plan[l], o, sms);
+            // adaLN (not the full block): fuse the next layer's K1 into this projection
+            rs.oln_plan.resize(static_cast<size_t>(cfg_.layers));
+            static const bool fuse_ln = [] {  // SPX_FUSE_LN=0: K1 stays a separate launch (A/B)
+                const char* e = std::getenv("SPX_FUSE_LN");
+                return !(e && std::atoi(e) == 0);
+            }();
+            if (fuse_ln && cfg_.adaln && !cfg_.wan_block && l + 1 < cfg_.layers && gemm_ln_supported(o)) {
+                const float* mn = w.mod + (l + 1) * 3 * C_;  // [shift | scale | gate] of layer l + 1
+                gemm_ln_plan(&rs.oln_plan[static_cast<size_t>(l)], o, rs.xm, mn + C_, mn, false,
+                             static_cast<float>(cfg_.norm_eps));
+            }
 
             AttnOperands a{};
             a.q = rs.q_recv;
@@ -740,7 +751,9 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
             const float* m = rs.mod_step + layer * 6 * C_;
             ln_modulate_run(x_in[static_cast<size_t>(li)], rs.xm, Lp_, C_, m, m + C_, cfg_.norm_eps,
                             rs.stream, false, true);
-        } else if (cfg_.adaln) {  // K1: x_in = LN(x)(1 + scale) + shift, the QKV GEMM's A operand
+        } else if (cfg_.adaln && xm_ready_layer_ != layer) {
+            // K1: x_in = LN(x)(1 + scale) + shift, the QKV GEMM's A operand (unless the previous
+            // layer's fused O-projection already wrote it)
             const float* m = weights_.at(rs.device).mod + layer * 3 * C_;
             ln_modulate_run(x_in[static_cast<size_t>(li)], rs.xm, Lp_, C_, m, m + C_, cfg_.norm_eps,
                             rs.stream);
@@ -900,13 +913,26 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
     if (!capturing_) world_->add_stats(0, 1, 0, out_exchange_elements(part_), 1);
 
     // K8 output projection
+    bool fused_ln = true;  // every local rank ran the fused projection + next-layer K1
     for (int li = 0; li < nl; ++li) {
         RankState& rs = ranks_[static_cast<size_t>(li)];
         SPX_CUDA(cudaSetDevice(rs.device));
-        gemm_run(*oproj[static_cast<size_t>(li)], rs.stream);
+        // the step's own plan (not a caller's one-off layer call) with the next layer's K1 fused
+        const GemmLnPlan* ln = (oproj[static_cast<size_t>(li)] == &rs.o_plan[static_cast<size_t>(layer)] &&
+                                static_cast<size_t>(layer) < rs.oln_plan.size() &&
+                                rs.oln_plan[static_cast<size_t>(layer)].ok)
+                                   ? &rs.oln_plan[static_cast<size_t>(layer)]
+                                   : nullptr;
+        if (ln) {
+            gemm_ln_run(*ln, rs.stream);
+        } else {
+            gemm_run(*oproj[static_cast<size_t>(li)], rs.stream);
+        }
+        fused_ln = fused_ln && ln != nullptr;
         mark(li, 6);
         if (cfg_.wan_block) run_wan_tail(rs, layer);  // cross-attention + FFN (token-local)
     }
+    xm_ready_layer_ = fused_ln ? layer + 1 : -1;
 }
 
 void Engine::run_plan(RankState& rs, int64_t layer, const std::vector<Transfer>& plan) {
@@ -953,6 +979,7 @@ void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, v
         ov.push_back(&op[li]);
         xv.push_back(static_cast<const bf16*>(x[li]));
     }
+    xm_ready_layer_ = -1;  // a one-off layer call runs its own K1
     run_layer(layer, start_frame, qv, ov, xv);
 }
 
@@ -1073,6 +1100,7 @@ void Engine::drop_graphs() {
 }
 
 void Engine::run_step_eager(int64_t start, int64_t step) {
+    xm_ready_layer_ = -1;  // layer 0 of every step runs its own K1
     if (cfg_.wan_block) {  // this step's timestep embedding -> every layer's modulation
         for (RankState& rs : ranks_) {
             SPX_CUDA(cudaSetDevice(rs.device));

@@ -112,6 +112,9 @@ struct RankState {
     std::vector<KvRingStorage> rings; // per layer
     std::vector<GemmPlan> qkv_plan;   // per layer, A = x[layer % 2]
     std::vector<GemmPlan> o_plan;     // per layer, out = x[(layer + 1) % 2]
+    // Wan mode (adaLN): layer l's O-projection fused with layer l + 1's LayerNorm + modulation
+    // (gemm_ln.cu), writing x[(l + 1) % 2] and xm; ok = false where it does not apply
+    std::vector<GemmLnPlan> oln_plan;
     std::vector<AttnPlan> attn_plan;  // per layer
     void* attn_ws = nullptr;          // split-KV workspace (shared by the layers)
     size_t attn_ws_bytes = 0;
@@ -276,6 +279,8 @@ class Engine {
     std::set<std::array<int64_t, 8>> seen_;  // states run once (captured on the next run)
     uint64_t graph_clock_ = 0;
     bool capturing_ = false;
+    // the layer whose K1 output (xm) the previous fused O-projection already wrote (-1: none)
+    int64_t xm_ready_layer_ = -1;
     bool graphs_enabled_ = true;
     int* peer_error_host_ = nullptr;  // host-mapped: 1 + the rank a PEER barrier timed out on
     int* peer_error_dev_ = nullptr;

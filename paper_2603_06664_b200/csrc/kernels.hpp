@@ -59,6 +59,26 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count);
 // rotate-and-pack without its qkv round trip); requires gemm_rope_fusable()
 void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope = nullptr);
 bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope);
+
+// The residual projection fused with the next LayerNorm + modulation (gemm_ln.cu, Wan mode):
+//   out = residual + gate (A B^T + bias);  out2 = LN(out) (one + mul) + add   (one = 1 adaLN,
+// 0 affine). Needs N = 1536 (a 3-CTA cluster owns 128 full rows), the residual epilogue and
+// 16-byte alignment; ok = false when the clusters do not all fit on the device at once.
+struct GemmLnPlan {
+    CUtensorMap map_a, map_b, map_res, map_out, map_out2;
+    GemmOperands ops;
+    bf16* out2 = nullptr;
+    const float* mul = nullptr;
+    const float* add = nullptr;
+    bool affine = false;
+    float eps = 1e-6f;
+    int grid = 0;
+    bool ok = false;
+};
+bool gemm_ln_supported(const GemmOperands& ops);
+void gemm_ln_plan(GemmLnPlan* plan, const GemmOperands& ops, bf16* out2, const float* mul, const float* add,
+                  bool affine, float eps);
+void gemm_ln_run(const GemmLnPlan& plan, cudaStream_t stream);
 // planner override (tests / tuning): -1 = modelled choice, else a tile variant index
 int gemm_forced_variant();
 void gemm_force_variant(int v);

@@ -30,6 +30,12 @@ PFN_cuTensorMapEncodeTiled_v12000 resolve_encode() {
 bool make_tma_map_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                        const uint64_t* strides_bytes, const uint32_t* box, char* err,
                        size_t err_len) {
+    return make_tma_map_bf16_swizzle(map, base, rank, dims, strides_bytes, box, 128, err, err_len);
+}
+
+bool make_tma_map_bf16_swizzle(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                               const uint64_t* strides_bytes, const uint32_t* box, int swizzle_bytes,
+                               char* err, size_t err_len) {
     PFN_cuTensorMapEncodeTiled_v12000 encode = resolve_encode();
     if (!encode) {
         std::snprintf(err, err_len, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
@@ -47,7 +53,8 @@ bool make_tma_map_bf16(CUtensorMap* map, const void* base, int rank, const uint6
     }
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank),
                         const_cast<void*>(base), gdim, gstride, bdim, estride,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         std::snprintf(err, err_len,

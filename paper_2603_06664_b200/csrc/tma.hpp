@@ -14,5 +14,9 @@ namespace spx {
 bool make_tma_map_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                        const uint64_t* strides_bytes, const uint32_t* box, char* err,
                        size_t err_len);
+// the same with SWIZZLE_64B (swizzle_bytes = 64: 32-element boxes) or SWIZZLE_128B (128)
+bool make_tma_map_bf16_swizzle(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                               const uint64_t* strides_bytes, const uint32_t* box, int swizzle_bytes,
+                               char* err, size_t err_len);
 
 }  // namespace spx
