@@ -50,9 +50,11 @@ constexpr int kBKV = 128;    // kv rows per tile
 // unrolled exp loop is predicated, i.e. it costs issue slots on every element
 // the same share for v3 (separate tuning: A/B on one box, kbench attn, 2 reps: of 1 / 2 / 3 /
 // 4 / 5 -> 0.1043 / 0.1048 / 0.1054 / 0.1060 / 0.1094 ms at the Wan chunk and 0.670 / 0.680 /
-// 0.686 / 0.688 / 0.716 ms at 32760 keys)
+// 0.686 / 0.688 / 0.716 ms at 32760 keys). The persistent v3 re-tuned (profiles/r02aq, 2 reps):
+// 0 / 1 / 2 -> 0.1014 / 0.1016 / 0.1037 ms at the chunk, 0.669 / 0.677 / 0.690 ms at 32760 keys:
+// every exponential on the MUFU
 #ifndef SPX_V3_POLY_OF_8
-#define SPX_V3_POLY_OF_8 1
+#define SPX_V3_POLY_OF_8 0
 #endif
 #ifndef SPX_ATTN_PROFILING
 #define SPX_ATTN_PROFILING 0
