@@ -5,13 +5,16 @@
 // block causality is structural (the cache only exposes past + current frames). Softmax is
 // order-invariant, so the ring's two chronological segments are visited in storage order.
 //
-// The kernel (attn_fwd_v2_kernel below): one CTA = one 128-row query tile of one head, its kv
-// range split between two softmax warpgroups that ping-pong against one MMA thread. Template
-// modes (host selection in attn_run):
-//   0  1-D grid, unsplit tiles first, then split-KV tiles merged through a workspace
-//   5  every tile in exactly 2 splits: the splits are a 2-CTA cluster, merged through DSMEM
-// (Round 1 also measured CTA-pair MMAs, K/V multicast across a CTA pair and a persistent form;
-// all were slower on B200 and are gone from this file -- DESIGN.md section 5 has the numbers.)
+// Two kernels, one CTA per 128-row query tile of one head (or a piece of its kv range), the kv
+// range split between two softmax warpgroups that ping-pong against one MMA thread; host
+// selection in attn_run:
+//   attn_fwd_v3_kernel  one O accumulator shared by both warpgroups, separate P buffers;
+//                       persistent over the tiles when every tile is whole, or (kPair) a 2-CTA
+//                       cluster per tile, each CTA half of the kv range, merged through DSMEM
+//   attn_fwd_v2_kernel  per-warpgroup O; mixed layouts (unsplit tiles first, then split-KV tiles
+//                       merged through a workspace) and the single-wave unsplit layouts
+// (Measured slower and removed: CTA-pair MMAs, K/V multicast across a CTA pair, v2's own
+// DSMEM pair merge, stream-K pieces, a slot-1 epilogue -- DESIGN.md section 5 has the numbers.)
 #include <algorithm>
 
 #include <atomic>
@@ -279,7 +282,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
-    constexpr bool kSplitPair = kMode == 5;
     using L = SmemV2<D, kMode>;
     constexpr uint32_t kSlots = L::kSlots;
     extern __shared__ uint8_t smem_raw[];
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint64_t* p_full = s_full + 2;           // [2]
     uint64_t* pv_done = p_full + 2;          // [2]
     uint64_t* merge_bar = pv_done + 2;       // split-KV: other splits' partials landed
-    uint64_t* xfer_free = merge_bar + 1;     // mode 5, split 1: the merging CTA's buffers are free
+    uint64_t* xfer_free = merge_bar + 1;     // (unused since the DSMEM pair merge moved to v3)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfer_free + 1);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
@@ -309,13 +311,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         attn_mark_global(p, 7);
     }
     int q_tile, head, split, ns;
-    if constexpr (kSplitPair) {
-        const int t = static_cast<int>(blockIdx.x) >> 1;
-        split = static_cast<int>(cluster_ctarank());
-        ns = 2;
-        q_tile = t % p.qt;
-        head = t / p.qt;
-    } else {  // full tiles first (block order ~ issue order), then the split ones
+    {  // full tiles first (block order ~ issue order), then the split ones
         const int b = static_cast<int>(blockIdx.x);
         int t;
         if (b < p.n_full) {
@@ -359,10 +355,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
-    if constexpr (kSplitPair)
-        cluster_sync_all();
-    else
-        __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (warp == 3 && lane == 0) l2_prefetch_share(p);  // constant data: before the PDL wait
@@ -661,91 +654,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                              static_cast<int64_t>(head) * D;
                 *reinterpret_cast<uint4*>(drow + u * 8) = w;
             }
-        } else if constexpr (kSplitPair) {
-            // ---- 2 splits merged through DSMEM ----
-            // Both CTAs stage their normalised fp32 partial (128 rows x D, 16-byte units
-            // XOR-swizzled by row) at offset 0 of their own smem. Split 0 keeps its lse in
-            // registers and receives split 1's partial at offset kPartBytes and its lse at
-            // 2 kPartBytes (ring smem, idle once the PVs are done), then merges.
-            constexpr uint32_t kUnits = D / 4;
-            constexpr uint32_t kPartBytes = kBQ * D * 4;
-            static_assert(2 * kPartBytes + 1024 <= L::kOffBar, "mode 5: two partials + lse in smem");
-            const uint32_t s_base = smem_u32(smem);
-            auto unit_addr = [&](uint32_t buf, int row, uint32_t u) {
-                return s_base + buf * kPartBytes + static_cast<uint32_t>(row) * (kUnits * 16) +
-                       ((u ^ (static_cast<uint32_t>(row) & (kUnits - 1))) << 4);
-            };
-            const float lse_own = mm + __log2f(l0 * a0 + l1 * a1);
-            if (split == 0 && threadIdx.x == 128) {
-                // the partner may write our buffer 1 and lse slot now (our MMAs are done)
-                mbar_arrive_expect_tx(merge_bar, kPartBytes + kBQ * 4);
-                mbar_arrive_remote(peer_smem_addr(xfer_free, 1));
-            }
-#pragma unroll 1
-            for (int c = i * (D / 64); c < (i + 1) * (D / 64); ++c) {
-                uint32_t o0[32], o1[32];
-                tmem_ld32(t_o0 + c * 32, o0);
-                if (n1 > 0) tmem_ld32(t_o1 + c * 32, o1);
-                tmem_ld_wait();
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    float f[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        f[e] = __uint_as_float(o0[4 * v + e]) * w0 +
-                               (n1 > 0 ? __uint_as_float(o1[4 * v + e]) * w1 : 0.0f);
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                     unit_addr(0, r, static_cast<uint32_t>(c * 8 + v))),
-                                 "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3])
-                                 : "memory");
-                }
-            }
-            if (split == 1) {
-                if (i == 0)
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(s_base + 2 * kPartBytes + kBQ * 4 + r * 4),
-                                 "f"(lse_own)
-                                 : "memory");
-                fence_proxy_async_smem();  // generic-proxy smem writes -> the bulk copies' reads
-                named_bar_sync(1, 256);
-                if (threadIdx.x == 128) {
-                    attn_mark(p, 2);
-                    mbar_wait_cluster(xfer_free, 0);
-                    const uint32_t mb = peer_smem_addr(merge_bar, 0);
-                    bulk_copy_to_peer(peer_smem_addr(smem + kPartBytes, 0), s_base, kPartBytes, mb);
-                    bulk_copy_to_peer(peer_smem_addr(smem + 2 * kPartBytes, 0), s_base + 2 * kPartBytes + kBQ * 4,
-                                      kBQ * 4, mb);
-                }
-            } else {
-                named_bar_sync(1, 256);  // both warpgroups staged their halves of every row
-                mbar_wait(merge_bar, 0);
-                if (threadIdx.x == 128) attn_mark(p, 6);
-                float lse1;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lse1) : "r"(s_base + 2 * kPartBytes + r * 4));
-                const float lm = fmaxf(lse_own, lse1);
-                const float wa = ex2_approx(lse_own - lm), wb = ex2_approx(lse1 - lm);
-                const float inv_w = 1.0f / (wa + wb);
-                const float ca = wa * inv_w, cb = wb * inv_w;
-                if (dst) {
-                    uint4* d4 = reinterpret_cast<uint4*>(dst + i * (D / 2));
-#pragma unroll
-                    for (int v = 0; v < D / 16; ++v) {
-                        float4 x0, x1, y0, y1;
-                        const uint32_t u0 = static_cast<uint32_t>(i * (D / 8) + 2 * v);
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w) : "r"(unit_addr(0, r, u0)));
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w) : "r"(unit_addr(0, r, u0 + 1)));
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(y0.x), "=f"(y0.y), "=f"(y0.z), "=f"(y0.w) : "r"(unit_addr(1, r, u0)));
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(y1.x), "=f"(y1.y), "=f"(y1.z), "=f"(y1.w) : "r"(unit_addr(1, r, u0 + 1)));
-                        d4[v] = make_uint4(pack_bf16x2(ca * x0.x + cb * y0.x, ca * x0.y + cb * y0.y),
-                                           pack_bf16x2(ca * x0.z + cb * y0.z, ca * x0.w + cb * y0.w),
-                                           pack_bf16x2(ca * x1.x + cb * y1.x, ca * x1.y + cb * y1.y),
-                                           pack_bf16x2(ca * x1.z + cb * y1.z, ca * x1.w + cb * y1.w));
-                    }
-                }
-            }
         } else {
             // ---- split-KV ----
             // Each split CTA stages its normalised fp32 partial (128 rows x D) in the now idle
@@ -882,10 +790,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         attn_mark_global(p, 8);
     }
     tc_fence_before();
-    if constexpr (kSplitPair)  // mode 5: split 1's smem is read by its bulk copy
-        cluster_sync_all();
-    else
-        __syncthreads();
+    __syncthreads();
     span_end(p.span);
     if (warp == 2) {
         tc_fence_after();
@@ -904,27 +809,8 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
                                       static_cast<int>(SmemV2<D, kMode>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kMode == 5) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(kThreadsV2);
-        cfg.dynamicSmemBytes = SmemV2<D, kMode>::kBytes;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 2;
-        SPX_CUDA(cudaLaunchKernelEx(&cfg, attn_fwd_v2_kernel<D, kMode>, plan.map_q, plan.map_k,
-                                    plan.map_v, p));
-    } else {
-        launch_pdl(attn_fwd_v2_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV2<D, kMode>::kBytes,
-                   stream, plan.map_q, plan.map_k, plan.map_v, p);
-    }
+    launch_pdl(attn_fwd_v2_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV2<D, kMode>::kBytes,
+               stream, plan.map_q, plan.map_k, plan.map_v, p);
 }
 
 
@@ -957,13 +843,17 @@ struct SmemV3 {
     static constexpr uint32_t kOffQ = 0;  // [2] query tiles (also the epilogue's row staging)
     static constexpr uint32_t kOffRing = kOffQ + 2 * kQBytes;
     static constexpr uint32_t kOffBar = kOffRing + kSlots * kTileBytes;
-    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done/s_free[2], o_free, q_free[2]
-    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 8 + 1 + 2;
+    // q_full[2], slot_full/empty[kSlots], s_full/p_full/pv_done/s_free[2], o_free, q_free[2],
+    // merge, xfer_free (pair-split mode)
+    static constexpr uint32_t kNumBars = 2 + 2 * kSlots + 8 + 1 + 2 + 2;
     static constexpr uint32_t kOffStats = kOffBar + ((kNumBars * 8 + 8 + 15) / 16) * 16;
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
 
-template <int D>
+// kPair: a 2-CTA cluster per query tile, CTA r of the pair takes half of the kv range
+// (split-KV for grids that under-fill the SMs: the per-rank shapes of P = 4 / 8); the halves'
+// normalised fp32 partials merge lse-weighted through DSMEM in CTA 0 (launched as a cluster).
+template <int D, bool kPair>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v3_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
@@ -985,7 +875,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint64_t* s_free = pv_done + 2;          // [2]
     uint64_t* o_free = s_free + 2;           // the epilogue holds O in registers
     uint64_t* q_free = o_free + 1;           // [2] the epilogue's row staging in Q buffer b is done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_free + 2);
+    uint64_t* merge_bar = q_free + 2;        // pair: split 1's partial landed in CTA 0
+    uint64_t* xfer_free = merge_bar + 1;     // pair, split 1: CTA 0's ring is free for the partial
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfer_free + 1);
     float* st_m = reinterpret_cast<float*>(smem + L::kOffStats);  // [2][128]
     float* st_l = st_m + 256;                                     // [2][128]
     __shared__ int s_ovf;
@@ -999,7 +891,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         attn_mark_global(p, 7);
     }
     const int num_tiles = p.qt * p.heads;
-    const int n_total = p.total_tiles;
+    // the CTA's tiles and kv range: kPair -> tile blockIdx.x / 2 and half `split` of its kv
+    // tiles; otherwise tiles blockIdx.x, + gridDim.x, ... over the whole kv range
+    const int split = kPair ? static_cast<int>(cluster_ctarank()) : 0;
+    const int t_first = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int t_step = kPair ? num_tiles : static_cast<int>(gridDim.x);
+    const int kb = kPair && split ? (p.total_tiles + 1) / 2 : 0;
+    const int ke = kPair && !split ? (p.total_tiles + 1) / 2 : p.total_tiles;
+    const int n_total = ke - kb;
     const int n0 = (n_total + 1) / 2;
     const int n1 = n_total - n0;
 
@@ -1022,12 +921,17 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_init(&s_free[i], 4);   // one arrival per softmax warp
         }
         mbar_init(o_free, 8);  // one arrival per softmax warp
+        mbar_init(merge_bar, 1);
+        mbar_init(xfer_free, 1);
         s_ovf = 0;
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair)
+        cluster_sync_all();  // the partner's barriers exist before any remote arrival
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t t_O = tmem_base + 256;
@@ -1040,7 +944,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             // ---------------- TMA producer: the MMA consumption order ----------------
             uint32_t t = 0;
             int it = 0;
-            for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+            for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
                 const int q_tile = tile % p.qt;
                 const int head = tile / p.qt;
                 const int b = it & 1;
@@ -1064,14 +968,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                     c * 64, head, row);
                     ++t;
                 };
-                load(false, 0);
-                if (n1 > 0) load(false, n0);
+                load(false, kb);
+                if (n1 > 0) load(false, kb + n0);
                 for (int j = 0; j < n0; ++j) {
-                    if (j + 1 < n0) load(false, j + 1);
-                    load(true, j);
+                    if (j + 1 < n0) load(false, kb + j + 1);
+                    load(true, kb + j);
                     if (j < n1) {
-                        if (j + 1 < n1) load(false, n0 + j + 1);
-                        load(true, n0 + j);
+                        if (j + 1 < n1) load(false, kb + n0 + j + 1);
+                        load(true, kb + n0 + j);
                     }
                 }
             }
@@ -1092,7 +996,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 return slot;
             };
             int it = 0;
-            for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+            for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
                 const int b = it & 1;
                 const uint32_t q_addr = smem_u32(sQ + b * L::kQBytes);
                 bool first_pv = true;
@@ -1167,12 +1071,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const uint32_t t_s = tmem_base + i * 128 + lane_off;
         const uint32_t t_p = tmem_base + 384 + i * 64 + lane_off;
         const int n = i == 0 ? n0 : n1;
-        const int g0 = i == 0 ? 0 : n0;
+        const int g0 = kb + (i == 0 ? 0 : n0);
         const float scale = p.scale_log2;
         constexpr uint32_t kRowBytes = D * 2;
         constexpr uint32_t kU = kRowBytes / 16;
         int it = 0;
-        for (int tile = static_cast<int>(blockIdx.x); tile < num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+        for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
         const int q_tile = tile % p.qt;
         const int head = tile / p.qt;
         const int b = it & 1;
@@ -1268,6 +1172,147 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         tc_fence_after();
         const float inv = 1.0f / (st_l[r] + st_l[128 + r]);
         const bool fallback = s_ovf != 0;
+        if constexpr (kPair) {
+        // ---------------- pair split: merge the two kv halves through DSMEM ----------------
+        // normalised fp32 partials, 16-byte units XOR-swizzled by row (conflict-free both ways);
+        // split 1 stages its partial + lse at offset 0 of its shared memory and bulk-copies
+        // them into CTA 0's idle ring once CTA 0's MMAs are done; CTA 0 merges from TMEM +
+        // shared memory, stages bf16 rows at offset 0 and stores them. lse = +inf marks a half
+        // that overflowed: CTA 0 then recomputes the row exactly.
+        constexpr uint32_t kPartBytes = kBQ * D * 4;
+        constexpr uint32_t kPU = D / 4;  // 16-byte units per fp32 row
+        static_assert(2 * kPartBytes + kBQ * 4 <= L::kOffBar, "pair merge buffers in the Q + ring smem");
+        const uint32_t s0 = smem_u32(smem);
+        auto punit = [&](uint32_t base, uint32_t u) {
+            return base + static_cast<uint32_t>(r) * (kPU * 16) + ((u ^ (static_cast<uint32_t>(r) & (kPU - 1))) << 4);
+        };
+        const float l_sum = st_l[r] + st_l[128 + r];
+        const float lse_own = fallback ? INFINITY : m_run + __log2f(l_sum);
+        if (split == 1) {
+            if (!fallback) {
+#pragma unroll 1
+                for (int c = 0; c < D / 64; ++c) {
+                    const int cc = i * (D / 64) + c;
+                    uint32_t o[32];
+                    tmem_ld32(t_O + lane_off + cc * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(punit(s0, cc * 8 + v)),
+                                     "f"(__uint_as_float(o[4 * v]) * inv), "f"(__uint_as_float(o[4 * v + 1]) * inv),
+                                     "f"(__uint_as_float(o[4 * v + 2]) * inv), "f"(__uint_as_float(o[4 * v + 3]) * inv)
+                                     : "memory");
+                }
+            }
+            if (i == 0)
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(s0 + kPartBytes + r * 4), "f"(lse_own) : "memory");
+            fence_proxy_async_smem();  // generic-proxy smem writes -> the bulk copies' reads
+            named_bar_sync(1, 256);
+            if (threadIdx.x == 128) {
+                mbar_wait_cluster(xfer_free, 0);
+                const uint32_t mb = peer_smem_addr(merge_bar, 0);
+                bulk_copy_to_peer(peer_smem_addr(smem + kPartBytes, 0), s0, kPartBytes, mb);
+                bulk_copy_to_peer(peer_smem_addr(smem + 2 * kPartBytes, 0), s0 + kPartBytes, kBQ * 4, mb);
+            }
+        } else {
+            if (threadIdx.x == 128) {  // our MMAs are done: the partner may fill our ring
+                mbar_arrive_expect_tx(merge_bar, kPartBytes + kBQ * 4);
+                mbar_arrive_remote(peer_smem_addr(xfer_free, 1));
+            }
+            mbar_wait(merge_bar, 0);
+            float lse1;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lse1) : "r"(s0 + 2 * kPartBytes + r * 4) : "memory");
+            const bool exact = fallback || !(lse1 < INFINITY);
+            auto stage = [&](int cc, const float* f) {  // bf16 row r, columns [32 cc, 32 cc + 32)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t unit = static_cast<uint32_t>(cc * 4 + v);
+                    const uint32_t a = s0 + static_cast<uint32_t>(r) * kRowBytes +
+                                       ((unit ^ (static_cast<uint32_t>(r) & (kU - 1))) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                                 "r"(pack_bf16x2(f[8 * v + 0], f[8 * v + 1])), "r"(pack_bf16x2(f[8 * v + 2], f[8 * v + 3])),
+                                 "r"(pack_bf16x2(f[8 * v + 4], f[8 * v + 5])), "r"(pack_bf16x2(f[8 * v + 6], f[8 * v + 7]))
+                                 : "memory");
+                }
+            };
+            if (!exact) {
+                const float lm = fmaxf(lse_own, lse1);
+                const float wa = ex2_approx(lse_own - lm), wb = ex2_approx(lse1 - lm);
+                const float iw = 1.0f / (wa + wb);
+                const float ca = wa * iw * inv, cb = wb * iw;
+#pragma unroll 1
+                for (int c = 0; c < D / 64; ++c) {
+                    const int cc = i * (D / 64) + c;
+                    uint32_t o[32];
+                    tmem_ld32(t_O + lane_off + cc * 32, o);
+                    tmem_ld_wait();
+                    float f[32];
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        float4 y;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                                     : "r"(punit(s0 + kPartBytes, cc * 8 + v)));
+                        f[4 * v] = fmaf(__uint_as_float(o[4 * v]), ca, cb * y.x);
+                        f[4 * v + 1] = fmaf(__uint_as_float(o[4 * v + 1]), ca, cb * y.y);
+                        f[4 * v + 2] = fmaf(__uint_as_float(o[4 * v + 2]), ca, cb * y.z);
+                        f[4 * v + 3] = fmaf(__uint_as_float(o[4 * v + 3]), ca, cb * y.w);
+                    }
+                    stage(cc, f);
+                }
+            } else {
+                // exact recompute of row r over the whole kv range, columns [i D/2, (i+1) D/2)
+                const int qi = q_tile * kBQ + r;
+                float acc[D / 2];
+#pragma unroll
+                for (int d = 0; d < D / 2; ++d) acc[d] = 0.0f;
+                float m = -INFINITY, l = 0.0f;
+                if (qi < p.sq) {
+                    const bf16* qr = p.q_ptr + static_cast<int64_t>(qi) * p.q_row_stride + head * D;
+                    const int total = p.seg_len[0] + p.seg_len[1];
+                    for (int jj = 0; jj < total; ++jj) {
+                        const int kr = jj < p.seg_len[0] ? p.seg_start[0] + jj : p.seg_start[1] + (jj - p.seg_len[0]);
+                        const bf16* krow = p.k_ptr + static_cast<int64_t>(kr) * p.kv_row_stride + head * D;
+                        const bf16* vrow = p.v_ptr + static_cast<int64_t>(kr) * p.kv_row_stride + head * D + i * (D / 2);
+                        float sdot = 0.0f;
+                        for (int d = 0; d < D; ++d) sdot = fmaf(__bfloat162float(qr[d]), __bfloat162float(krow[d]), sdot);
+                        sdot *= scale;
+                        const float mn = fmaxf(m, sdot);
+                        const float a = exp2f(m - mn), e = exp2f(sdot - mn);
+                        l = l * a + e;
+#pragma unroll
+                        for (int d = 0; d < D / 2; ++d) acc[d] = acc[d] * a + e * __bfloat162float(vrow[d]);
+                        m = mn;
+                    }
+                }
+                const float il = 1.0f / l;
+#pragma unroll
+                for (int d = 0; d < D / 2; ++d) acc[d] *= il;
+#pragma unroll
+                for (int c = 0; c < D / 64; ++c) stage(i * (D / 64) + c, &acc[c * 32]);
+            }
+            named_bar_sync(1, 256);  // staged rows visible
+            const int tid = static_cast<int>(threadIdx.x) - 128;
+            const int r0 = q_tile * kBQ;
+#pragma unroll 1
+            for (int idx = tid; idx < kBQ * static_cast<int>(kU); idx += 256) {
+                const int row = idx / static_cast<int>(kU);
+                const uint32_t uu = static_cast<uint32_t>(idx) % kU;
+                const int q_row = r0 + row;
+                if (q_row >= p.sq) continue;
+                uint4 w;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                             : "r"(s0 + static_cast<uint32_t>(row) * kRowBytes +
+                                   ((uu ^ (static_cast<uint32_t>(row) & (kU - 1))) << 4))
+                             : "memory");
+                const int chunk = q_row / p.rows_per_chunk;
+                bf16* drow = p.out_base[chunk] + static_cast<int64_t>(q_row - chunk * p.rows_per_chunk) * p.out_row_stride +
+                             static_cast<int64_t>(head) * D;
+                *reinterpret_cast<uint4*>(drow + uu * 8) = w;
+            }
+        }
+        } else {
         // this slot's half of the O columns, 32 at a time: normalise, stage in this tile's Q
         // buffer (every QK^T of the tile is done); O is handed to the next tile's PV as soon as
         // the last chunk is in registers
@@ -1379,9 +1424,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         // this thread's staging reads are done: the producer may load tile it + 2's Q here
         // (generic-proxy reads before an async-proxy write: the mbarrier orders them)
         mbar_arrive(&q_free[b]);
+        }  // kPair
         }  // tiles
     }
     tc_fence_before();
+    // pair: split 1's shared memory is read by its bulk copies until CTA 0 has the partial
+    if constexpr (kPair) cluster_sync_all();
     __syncthreads();
     span_end(p.span);
     if (threadIdx.x == 128) {
@@ -1394,18 +1442,22 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
 }
 
-template <int D>
+template <int D, bool kPair = false>
 void attn_v3_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
     static bool done[64] = {};
     int dev = 0;
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(SmemV3<D>::kBytes)));
         done[dev & 63] = true;
     }
-    launch_pdl(attn_fwd_v3_kernel<D>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, plan.map_q,
-               plan.map_k, plan.map_v, p);
+    if constexpr (kPair)
+        launch_pdl_cluster(attn_fwd_v3_kernel<D, kPair>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, 2,
+                           plan.map_q, plan.map_k, plan.map_v, p);
+    else
+        launch_pdl(attn_fwd_v3_kernel<D, kPair>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, plan.map_q,
+                   plan.map_k, plan.map_v, p);
 }
 
 // head_dim 16 / 32 (the reference's default and desk configurations, GenerationConfig
@@ -1741,13 +1793,14 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
             return !(e && std::atoi(e) == 0);
         }();
-        if (pair_merge && p.n_full == 0 && p.splits == 2) {
-            // every tile in 2 splits: the two CTAs of a cluster merge through DSMEM
+        if (pair_merge && p.n_full == 0 && p.splits == 2 && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
+            (p.experiment == 0 || p.experiment == 5)) {
+            // every tile in 2 kv halves: the shared-O kernel as 2-CTA clusters merging via DSMEM
             const dim3 g2(static_cast<unsigned>(2 * T));
             if (o.head_dim == 128)
-                attn_v2_launch<128, 5>(g2, plan, p, stream);
+                attn_v3_launch<128, true>(g2, plan, p, stream);
             else
-                attn_v2_launch<64, 5>(g2, plan, p, stream);
+                attn_v3_launch<64, true>(g2, plan, p, stream);
         } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
                    (g_attn_v3.load(std::memory_order_relaxed) == 2 || o.prefer_v3 || T >= sms)) {
             // every tile unsplit: the shared-O / early-S kernel, persistent over the tiles
