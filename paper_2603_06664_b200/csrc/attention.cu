@@ -1545,9 +1545,9 @@ int choose_splits(int64_t n, int64_t tiles, int sm_count, int cap) {
 }
 }  // namespace
 
-// the shared-O / early-S kernel (v3) for unsplit layouts: SPX_ATTN_V3 = 0 never, 1 (default)
-// when the layout has at least one full wave of CTAs or the plan asks for it (exact SP
-// layouts: every partition must run the same kernel), 2 always
+// the shared-O / early-S kernel (v3) for unsplit and 2-split layouts: SPX_ATTN_V3 = 0 never
+// (v2 everywhere), otherwise always (the persistent v3 measured 3-5 % faster than v2 on the
+// single-wave layouts too: 4680 x 4680 x 3 0.0359 vs 0.0375 ms, profiles/r02au)
 std::atomic<int> g_attn_v3{[] {
     const char* e = std::getenv("SPX_ATTN_V3");
     return e ? std::atoi(e) : 1;
@@ -1801,8 +1801,8 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
                 attn_v3_launch<128, true>(g2, plan, p, stream);
             else
                 attn_v3_launch<64, true>(g2, plan, p, stream);
-        } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
-                   (g_attn_v3.load(std::memory_order_relaxed) == 2 || o.prefer_v3 || T >= sms)) {
+        } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) &&
+                   g_attn_v3.load(std::memory_order_relaxed) != 0) {
             // every tile unsplit: the shared-O / early-S kernel, persistent over the tiles
             const dim3 gv3(static_cast<unsigned>(std::min<int64_t>(T, v3_persistent() ? sms : T)));
             if (o.head_dim == 128)
