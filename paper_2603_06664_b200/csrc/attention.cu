@@ -814,6 +814,10 @@ void attn_v2_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaSt
 }
 
 
+// the v3 slots' exponent-offset exchange: one barrier instruction for both call sites (a slot
+// with no kv tiles joins from outside its loop), so the barrier is not seen as divergent
+__device__ __noinline__ void v3_offset_exchange_barrier() { named_bar_sync(1, 256); }
+
 // =========================================================================================
 // v3: the kv range of a 128-row query tile is split between two softmax warpgroups as in v2,
 // but the two slots accumulate into ONE O (TMEM) with a common exponent offset (the max over
@@ -1086,7 +1090,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         bool ovf = false;
         if (n == 0) {  // (a one-tile kv range: slot 1 idle) still joins the offset exchange
             st_m[i * 128 + r] = -INFINITY;
-            named_bar_sync(1, 256);
+            v3_offset_exchange_barrier();
         }
         for (int j = 0; j < n; ++j) {
             const uint32_t G = gbase + static_cast<uint32_t>(j);
@@ -1118,7 +1122,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                                         __uint_as_float(u[c + 2 * k4 + 1]));
                 }
                 st_m[i * 128 + r] = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * scale;
-                named_bar_sync(1, 256);
+                v3_offset_exchange_barrier();
                 m_run = fmaxf(st_m[r], st_m[128 + r]);
             }
             uint32_t pk[kBKV / 2];

@@ -1,6 +1,8 @@
 """A small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every
-kernel family once at small shapes -- GEMM variants and epilogues, attention v2 / v3 / split-KV
-/ small-D, K3 / K1, the engine (P = 1 and 2, the Wan block), the PEER-free paths."""
+kernel family once at small shapes -- GEMM variants and epilogues, attention v2 / v3 (persistent
+over several tiles per CTA, the 2-CTA pair split) / split-KV / small-D, K3 / K1, the engine (P = 1
+and 2, Wan mode incl. the fused O-projection + LayerNorm at C = 1536, the Wan block), the
+PEER-free paths."""
 import os
 import sys
 
@@ -42,6 +44,11 @@ for splits in (2, 3):
     o = torch.empty_like(q)
     check(lib().spx_attention(q.data_ptr(), k.data_ptr(), k.data_ptr(), o.data_ptr(), 1, 256, 1200, 2, 128, st))
 check(lib().spx_debug_set_attn_splits(0))
+# the persistent v3 with several tiles per CTA (more tiles than SMs)
+q = torch.randn(1, 128 * 10, 16, 128, device="cuda").to(torch.bfloat16)
+k = torch.randn(1, 256, 16, 128, device="cuda").to(torch.bfloat16)
+o = torch.empty_like(q)
+check(lib().spx_attention(q.data_ptr(), k.data_ptr(), k.data_ptr(), o.data_ptr(), 1, 1280, 256, 16, 128, st))
 for D in (16, 32):
     q = torch.randn(1, 48, 8, D, device="cuda").to(torch.bfloat16)
     o = torch.empty_like(q)
@@ -55,5 +62,11 @@ for kw in [dict(heads=4, head_dim=64, world_size=1), dict(heads=4, head_dim=64, 
     cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(3, 4, 8), num_blocks=2, layers=2,
                                   denoise_steps=2, **kw)
     spattn.Engine(cfg).generate()
+torch.cuda.synchronize()
+# Wan mode at C = 1536 with >= 25 row tiles: the O-projection fused with the next layer's
+# LayerNorm + modulation (gemm_ln.cu)
+cfg = spattn.GenerationConfig(grid_per_block=spattn.GridSpec(3, 32, 32), num_blocks=1, layers=2,
+                              denoise_steps=1, heads=12, head_dim=128, qk_norm=True, adaln=True)
+spattn.Engine(cfg).generate()
 torch.cuda.synchronize()
 print("sanitize workload done")
