@@ -113,7 +113,8 @@ struct RopeAux {
 // per CTA, so the per-row work is the table lookups, the math and the stores.
 template <int NV, bool KV, bool NORM>
 __global__ void __launch_bounds__(kPipeThreads, 1)
-    rope_norm_pack_kernel(const RopeLaunch l, const RowPipeShape sh, const RopeAux aux) {
+    rope_norm_pack_kernel(const RopeLaunch l, const RowPipeShape sh, const RopeAux aux,
+                          unsigned long long* span) {
     extern __shared__ __align__(16) uint8_t smem_rope[];
     const int C = l.heads * l.head_dim;
     const int nvec = C / 8;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     float4* s_nw = reinterpret_cast<float4*>(s_dst + 8 * 17);
     uint8_t* ring = reinterpret_cast<uint8_t*>(s_nw + (NORM ? 4 * nvec : 0));
     pdl_trigger();
+    span_begin(span);
     if (threadIdx.x == 0) row_pipe_init(bars, sh.stages);
     __syncthreads();
     if (threadIdx.x / 32 == kPipeWarps) {  // producer: the rows were written by the QKV projection
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
         }
       }
     });
+    span_end(span);  // (consumer thread 0: profiling only)
 }
 
 __global__ void rope_table_kernel(float2* b0, float2* b1, float2* b2, int r0, int r1, int r2,
@@ -313,7 +316,8 @@ void launch_rope_k(const RopeLaunch& l, const RowPipeShape& sh, const RopeAux& a
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         done[dev & 63] = true;
     }
-    launch_pdl(rope_norm_pack_kernel<NV, KV, NORM>, dim3(ctas), dim3(kPipeThreads), smem, stream, l, sh, aux);
+    launch_pdl(rope_norm_pack_kernel<NV, KV, NORM>, dim3(ctas), dim3(kPipeThreads), smem, stream, l, sh, aux,
+               span_slot());
 }
 
 template <int NV>

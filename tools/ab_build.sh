@@ -5,9 +5,9 @@ set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 WT=/tmp/spx_head_wt
 rm -rf $WT; git -C $ROOT worktree prune
-git -C $ROOT worktree add -f --detach $WT HEAD > /dev/null
+git -C $ROOT worktree add -f --detach $WT ${1:-HEAD} > /dev/null
 make -s -j16 -C $WT/paper_2603_06664_b200/csrc > /dev/null
 mkdir -p $ROOT/ab_libs
 cp $WT/paper_2603_06664_b200/libspx.so $ROOT/ab_libs/libspx_head.so
 git -C $ROOT worktree remove --force $WT
-echo "ab_libs/libspx_head.so <- $(git -C $ROOT rev-parse --short HEAD)"
+echo "ab_libs/libspx_head.so <- $(git -C $ROOT rev-parse --short ${1:-HEAD})"

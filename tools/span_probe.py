@@ -41,14 +41,15 @@ check(lib().spx_debug_spans(None, 0, ctypes.byref(n1)))
 buf = np.zeros(2 * n1.value, dtype=np.uint64)
 check(lib().spx_debug_spans(buf.ctypes.data, buf.size, ctypes.byref(n1)))
 sp = buf.reshape(-1, 2)[n0.value:n1.value].astype(np.float64) / 1e3  # us
-names = ["qkv_gemm", "attention", "o_gemm"]
+names = {3: ["qkv_gemm", "attention", "o_gemm"],
+         4: ["qkv_gemm", "k3_norm_rope", "attention", "o_gemm"]}
 per = len(sp) // (layers * steps)
 dur = sp[:, 1] - sp[:, 0]
 gap = np.concatenate([[0.0], sp[1:, 0] - sp[:-1, 1]])
 inc = np.concatenate([[0.0], sp[1:, 1] - sp[:-1, 1]])  # last-CTA end to last-CTA end: the kernel's share of the chunk
 res = {"kernels_per_call": per, "chunk_span_ms": float((sp[-1, 1] - sp[0, 0]) / 1e3)}
 for k in range(per):
-    res[names[k] if per == 3 else f"k{k}"] = {"dur_us": round(float(dur[k::per].mean()), 2),
+    res[names[per][k] if per in names else f"k{k}"] = {"dur_us": round(float(dur[k::per].mean()), 2),
                                               "gap_before_us": round(float(gap[k::per][1:].mean()), 2),
                                               "end_to_end_us": round(float(inc[k::per][1:].mean()), 2)}
 print(json.dumps(res))
