@@ -1,0 +1,8 @@
+O=gpurun_out/r02bb; mkdir -p $O
+SPX_GEMM_EXPERIMENT=8 SPX_GRAPHS=0 timeout 300 python tools/ln_trace.py > $O/ln_trace.txt 2>&1
+SPX_LIB=$PWD/ab_libs/libspx_head.so SPX_GEMM_EXPERIMENT=8 SPX_GRAPHS=0 timeout 300 python tools/ln_trace.py > $O/ln_trace_head.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_wan_parity.py tests/test_gpu_engine.py -x -q -m gpu -k "wan" > $O/pytest_wan.log 2>&1; echo "rc=$?" >> $O/pytest_wan.log
+for rep in 1 2; do
+SPX_LIB=$PWD/ab_libs/libspx_head.so SPX_SPAN_TRACE=1 SPX_GRAPHS=0 timeout 300 python tools/span_probe.py --wan >> $O/span_head.txt 2>&1
+SPX_SPAN_TRACE=1 SPX_GRAPHS=0 timeout 300 python tools/span_probe.py --wan >> $O/span_tree.txt 2>&1
+done
