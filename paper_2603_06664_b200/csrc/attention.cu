@@ -939,6 +939,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t t_O = tmem_base + 256;
+    if (warp == 3 && lane == 0) l2_prefetch_share(p);  // constant data (weights): before the PDL wait
     pdl_wait();  // q and the KV ring slots were written by the previous kernel(s)
     if (threadIdx.x == 0) attn_mark(p, 0);
 
