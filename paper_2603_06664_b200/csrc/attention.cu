@@ -854,10 +854,16 @@ struct SmemV3 {
     static constexpr uint32_t kBytes = kOffStats + 4 * 128 * 4 + 1024;
 };
 
-// kPair: a 2-CTA cluster per query tile, CTA r of the pair takes half of the kv range
-// (split-KV for grids that under-fill the SMs: the per-rank shapes of P = 4 / 8); the halves'
-// normalised fp32 partials merge lse-weighted through DSMEM in CTA 0 (launched as a cluster).
-template <int D, bool kPair>
+// kMode (the CTA's list of pieces = (tile, kv range)):
+//   0  persistent: tiles blockIdx.x, + gridDim.x, ..., each over its whole kv range
+//   1  pair split: a 2-CTA cluster per tile, CTA r takes half r of the kv range (the per-rank
+//      shapes of P = 8); the halves' normalised fp32 partials merge lse-weighted through DSMEM
+//      in CTA 0
+//   2  triple: cluster c owns tiles 3c, 3c + 1, 3c + 2; CTA r takes tile 3c + r whole, then
+//      half r of tile 3c + 2, merged as in mode 1 (1.5 tiles per SM: the P = 2 per-rank shape's
+//      222 tiles on 148 SMs)
+// Modes 1 and 2 launch as 2-CTA clusters.
+template <int D, int kMode>
 __global__ void __launch_bounds__(kThreadsV2, 1)
     attn_fwd_v3_kernel(const __grid_constant__ CUtensorMap map_q,
                        const __grid_constant__ CUtensorMap map_k,
@@ -894,17 +900,31 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         attn_mark(p, 4);  // CTA entry
         attn_mark_global(p, 7);
     }
+    constexpr bool kPair = kMode != 0;  // a 2-CTA cluster: the last piece merges through DSMEM
     const int num_tiles = p.qt * p.heads;
-    // the CTA's tiles and kv range: kPair -> tile blockIdx.x / 2 and half `split` of its kv
-    // tiles; otherwise tiles blockIdx.x, + gridDim.x, ... over the whole kv range
     const int split = kPair ? static_cast<int>(cluster_ctarank()) : 0;
-    const int t_first = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-    const int t_step = kPair ? num_tiles : static_cast<int>(gridDim.x);
-    const int kb = kPair && split ? (p.total_tiles + 1) / 2 : 0;
-    const int ke = kPair && !split ? (p.total_tiles + 1) / 2 : p.total_tiles;
-    const int n_total = ke - kb;
-    const int n0 = (n_total + 1) / 2;
-    const int n1 = n_total - n0;
+    const int NT = p.total_tiles;
+    const int half_b = (NT + 1) / 2;
+    // piece `it` of this CTA: tile, kv tiles [kb, ke); false past the last piece
+    auto piece = [&](int it, int& tile, int& kb, int& ke) -> bool {
+        if constexpr (kMode == 0) {
+            tile = static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
+            kb = 0;
+            ke = NT;
+            return tile < num_tiles;
+        } else {
+            const int c = static_cast<int>(blockIdx.x >> 1);
+            const int last = kMode == 1 ? 0 : 1;
+            if (it > last) return false;
+            tile = kMode == 1 ? c : (it == 0 ? 3 * c + split : 3 * c + 2);
+            const bool halved = it == last;
+            kb = halved && split ? half_b : 0;
+            ke = halved && !split ? half_b : NT;
+            return tile < num_tiles;
+        }
+    };
+    // the CTA's last piece is the merged half in modes 1 / 2
+    auto merged = [&](int it) { return kPair && it == (kMode == 1 ? 0 : 1); };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_q);
@@ -949,7 +969,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             // ---------------- TMA producer: the MMA consumption order ----------------
             uint32_t t = 0;
             int it = 0;
-            for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
+            for (int tile, kb, ke; piece(it, tile, kb, ke); ++it) {
+                const int n0 = (ke - kb + 1) / 2;
+                const int n1 = ke - kb - n0;
                 const int q_tile = tile % p.qt;
                 const int head = tile / p.qt;
                 const int b = it & 1;
@@ -1001,7 +1023,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 return slot;
             };
             int it = 0;
-            for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
+            for (int tile, kb, ke; piece(it, tile, kb, ke); ++it) {
+                const int n0 = (ke - kb + 1) / 2;
+                const int n1 = ke - kb - n0;
                 const int b = it & 1;
                 const uint32_t q_addr = smem_u32(sQ + b * L::kQBytes);
                 bool first_pv = true;
@@ -1075,17 +1099,18 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const uint32_t t_s = tmem_base + i * 128 + lane_off;
         const uint32_t t_p = tmem_base + 384 + i * 64 + lane_off;
-        const int n = i == 0 ? n0 : n1;
-        const int g0 = kb + (i == 0 ? 0 : n0);
         const float scale = p.scale_log2;
         constexpr uint32_t kRowBytes = D * 2;
         constexpr uint32_t kU = kRowBytes / 16;
         int it = 0;
-        for (int tile = t_first; tile < num_tiles; tile += t_step, ++it) {
+        uint32_t gbase = 0;  // this slot's kv tiles in the CTA's earlier pieces
+        for (int tile, kb, ke; piece(it, tile, kb, ke); ++it) {
+        const int n0 = (ke - kb + 1) / 2;
+        const int n = i == 0 ? n0 : ke - kb - n0;
+        const int g0 = kb + (i == 0 ? 0 : n0);
         const int q_tile = tile % p.qt;
         const int head = tile / p.qt;
         const int b = it & 1;
-        const uint32_t gbase = static_cast<uint32_t>(it * n);  // this slot's kv tiles before this tile
         float m_run = -INFINITY;
         float l_run = 0.0f;
         bool ovf = false;
@@ -1177,7 +1202,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         tc_fence_after();
         const float inv = 1.0f / (st_l[r] + st_l[128 + r]);
         const bool fallback = s_ovf != 0;
-        if constexpr (kPair) {
+        gbase += static_cast<uint32_t>(n);
+        if (merged(it)) {
         // ---------------- pair split: merge the two kv halves through DSMEM ----------------
         // normalised fp32 partials, 16-byte units XOR-swizzled by row (conflict-free both ways);
         // split 1 stages its partial + lse at offset 0 of its shared memory and bulk-copies
@@ -1429,7 +1455,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         // this thread's staging reads are done: the producer may load tile it + 2's Q here
         // (generic-proxy reads before an async-proxy write: the mbarrier orders them)
         mbar_arrive(&q_free[b]);
-        }  // kPair
+        }  // merged piece
         }  // tiles
     }
     tc_fence_before();
@@ -1447,21 +1473,21 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     }
 }
 
-template <int D, bool kPair = false>
+template <int D, int kMode = 0>
 void attn_v3_launch(dim3 grid, const AttnPlan& plan, const AttnParams& p, cudaStream_t stream) {
     static bool done[64] = {};
     int dev = 0;
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPX_CUDA(cudaFuncSetAttribute(attn_fwd_v3_kernel<D, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(SmemV3<D>::kBytes)));
         done[dev & 63] = true;
     }
-    if constexpr (kPair)
-        launch_pdl_cluster(attn_fwd_v3_kernel<D, kPair>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, 2,
+    if constexpr (kMode != 0)
+        launch_pdl_cluster(attn_fwd_v3_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, 2,
                            plan.map_q, plan.map_k, plan.map_v, p);
     else
-        launch_pdl(attn_fwd_v3_kernel<D, kPair>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, plan.map_q,
+        launch_pdl(attn_fwd_v3_kernel<D, kMode>, grid, dim3(kThreadsV2), SmemV3<D>::kBytes, stream, plan.map_q,
                    plan.map_k, plan.map_v, p);
 }
 
@@ -1798,14 +1824,34 @@ void attn_run(const AttnPlan& plan, cudaStream_t stream) {
             const char* e = std::getenv("SPX_ATTN_SPLIT_PAIR");
             return !(e && std::atoi(e) == 0);
         }();
-        if (pair_merge && p.n_full == 0 && p.splits == 2 && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
+        static const bool triple_on = [] {  // SPX_ATTN_TRIPLE=0: no triple layout (A/B)
+            const char* e = std::getenv("SPX_ATTN_TRIPLE");
+            return !(e && std::atoi(e) == 0);
+        }();
+        // triple layout: 1.5 tiles per SM (one whole tile per CTA plus half of a third per
+        // 2-CTA cluster) when the tiles are 3 per cluster and fill the SMs in 1-2 waves (the
+        // P = 2 per-rank shape: 222 tiles on 148 SMs). Measured (profiles/r02bh): 0.0662 ->
+        // 0.0638 ms at 4680 x 4680 x 6 (37 kv tiles), but 0.355 -> 0.360 ms at 256 kv tiles (the
+        // half pieces and the merge cost more than the balance gains there): short kv ranges only
+        const int64_t clusters3 = T / 3;
+        const bool triple = triple_on && !o.prefer_v3 && T % 3 == 0 && T > sms && clusters3 <= sms / 2 &&
+                            5 * clusters3 >= 4 * (sms / 2) && p.total_tiles >= 8 && p.total_tiles <= 48 &&
+                            (p.experiment == 0 || p.experiment == 5) && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
+                            !g_forced_splits.load(std::memory_order_relaxed);
+        if (triple) {
+            const dim3 g3(static_cast<unsigned>(2 * clusters3));
+            if (o.head_dim == 128)
+                attn_v3_launch<128, 2>(g3, plan, p, stream);
+            else
+                attn_v3_launch<64, 2>(g3, plan, p, stream);
+        } else if (pair_merge && p.n_full == 0 && p.splits == 2 && g_attn_v3.load(std::memory_order_relaxed) != 0 &&
             (p.experiment == 0 || p.experiment == 5)) {
             // every tile in 2 kv halves: the shared-O kernel as 2-CTA clusters merging via DSMEM
             const dim3 g2(static_cast<unsigned>(2 * T));
             if (o.head_dim == 128)
-                attn_v3_launch<128, true>(g2, plan, p, stream);
+                attn_v3_launch<128, 1>(g2, plan, p, stream);
             else
-                attn_v3_launch<64, true>(g2, plan, p, stream);
+                attn_v3_launch<64, 1>(g2, plan, p, stream);
         } else if (p.n_full == T && (p.experiment == 0 || p.experiment == 5) &&
                    g_attn_v3.load(std::memory_order_relaxed) != 0) {
             // every tile unsplit: the shared-O / early-S kernel, persistent over the tiles

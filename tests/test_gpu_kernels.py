@@ -90,7 +90,10 @@ def attn_kernel(request):
 
 
 @pytest.mark.parametrize("sq,skv,H,D", [(192, 192, 4, 64), (300, 450, 2, 64), (256, 640, 3, 128),
-                                        (4680, 4680, 12, 128), (1170, 9360, 3, 128), (128, 100, 1, 128)])
+                                        (4680, 4680, 12, 128), (1170, 9360, 3, 128), (128, 100, 1, 128),
+                                        # 222 tiles: v3's triple layout (whole tile + half of a third
+                                        # per CTA, halves merged through DSMEM); 57 tiles: the pair split
+                                        (4680, 4680, 6, 128), (4680, 14040, 6, 128), (2340, 4680, 3, 128)])
 def test_attention_matches_fp32(cuda, sq, skv, H, D, parity_log, attn_kernel):
     torch = _t()
     g = torch.Generator(device="cuda").manual_seed(sq + skv + H)
