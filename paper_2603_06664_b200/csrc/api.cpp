@@ -373,6 +373,11 @@ void attention_oneshot(spx::AttnOperands a, cudaStream_t st) {
         }
         a.workspace = slot.first;
         a.workspace_bytes = slot.second;
+        // the split counters sit at the front of the workspace, sized by this call's tiles; a
+        // previous call of another shape may have left partials (not re-armed counters) there
+        const size_t rows = static_cast<size_t>((ceil_div(static_cast<int64_t>(a.sq), 128) + 1) & ~1) * 128;
+        const size_t ctr = (rows / 128 * a.heads * sizeof(int) + 255) / 256 * 256;
+        SPX_CUDA(cudaMemsetAsync(slot.first, 0, std::min(ctr, slot.second), st));
     }
     AttnPlan plan;
     attn_plan(&plan, a, sms);

@@ -1194,7 +1194,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             tc_fence_after();
         }
         if (ovf) s_ovf = 1;
-        if (threadIdx.x == 128) attn_mark(p, 1);  // softmax loop done (last tile's)
+        if (threadIdx.x == 128) {
+            attn_mark(p, 1);  // softmax loop done (last tile's)
+            if (it < 4) attn_mark(p, 10 + it);  // per piece: loop end
+        }
         // ---------------- epilogue: O / (l0 + l1), rows staged in this tile's Q buffer ----------------
         st_l[i * 128 + r] = l_run;
         tc_fence_before();
@@ -1456,6 +1459,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         // (generic-proxy reads before an async-proxy write: the mbarrier orders them)
         mbar_arrive(&q_free[b]);
         }  // merged piece
+        if (threadIdx.x == 128 && it < 4) attn_mark(p, 20 + it);  // per piece: epilogue end
         }  // tiles
     }
     tc_fence_before();
