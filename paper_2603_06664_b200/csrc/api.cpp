@@ -2,6 +2,7 @@
 // function it replaces, converts spx::Error into a status code, and launches on the caller's
 // stream. No exception crosses this file.
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <cuda_runtime.h>
 
@@ -359,6 +360,7 @@ void attention_oneshot(spx::AttnOperands a, cudaStream_t st) {
         // is zeroed only when it is (re)allocated; growth waits for the stream first
         static std::mutex mu;
         static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+        static std::map<std::pair<int, cudaStream_t>, std::tuple<int64_t, int64_t, size_t>> last_shape;
         std::lock_guard<std::mutex> lock(mu);
         auto& slot = cache[{dev, st}];
         if (slot.second < ws) {
@@ -374,10 +376,16 @@ void attention_oneshot(spx::AttnOperands a, cudaStream_t st) {
         a.workspace = slot.first;
         a.workspace_bytes = slot.second;
         // the split counters sit at the front of the workspace, sized by this call's tiles; a
-        // previous call of another shape may have left partials (not re-armed counters) there
-        const size_t rows = static_cast<size_t>((ceil_div(static_cast<int64_t>(a.sq), 128) + 1) & ~1) * 128;
-        const size_t ctr = (rows / 128 * a.heads * sizeof(int) + 255) / 256 * 256;
-        SPX_CUDA(cudaMemsetAsync(slot.first, 0, std::min(ctr, slot.second), st));
+        // previous call of another shape may have left partials (not re-armed counters) there,
+        // so they are zeroed whenever the shape changes (a launch re-arms its own counters)
+        const auto shape = std::make_tuple(static_cast<int64_t>(a.sq), static_cast<int64_t>(a.heads), ws);
+        auto& prev = last_shape[{dev, st}];
+        if (prev != shape) {
+            const size_t rows = static_cast<size_t>((ceil_div(static_cast<int64_t>(a.sq), 128) + 1) & ~1) * 128;
+            const size_t ctr = (rows / 128 * a.heads * sizeof(int) + 255) / 256 * 256;
+            SPX_CUDA(cudaMemsetAsync(slot.first, 0, std::min(ctr, slot.second), st));
+            prev = shape;
+        }
     }
     AttnPlan plan;
     attn_plan(&plan, a, sms);
