@@ -653,7 +653,9 @@ RopeLaunch Engine::rope_launch(const RankState& rs, int64_t layer, int64_t start
         rl.tab[b] = t.band[b];
         rl.pairs[b] = static_cast<int>(table_->pairs(b));
     }
+    rl.tab_constant = 1;  // uploaded once at create time
     if (!(cfg_.ablation & SPX_ABLATION_PRECOMPUTED_FREQS)) {  // this call's recomputed slice
+        rl.tab_constant = 0;
         rl.tab[0] = rs.tab_scratch;
         rl.tab[1] = rl.tab[0] + (start_frame + F_) * rl.pairs[0];
         rl.tab[2] = rl.tab[1] + Hg_ * rl.pairs[1];

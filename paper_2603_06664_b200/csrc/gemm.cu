@@ -112,16 +112,30 @@ __device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, uint32_t 
     const RopeSmem r = rope_smem_layout(l);
     const int nt = r.n_t * l.pairs[0];
     const int total = rope_smem_pairs(l);
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-        float2 v;
-        if (i < nt)
-            v = __ldg(&l.tab[0][r.t_lo * l.pairs[0] + i]);
-        else if (i < r.off_w)
-            v = __ldg(&l.tab[1][i - r.off_h]);
-        else
-            v = __ldg(&l.tab[2][i - r.off_w]);
-        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(st + 8u * i), "f"(v.x), "f"(v.y)
-                     : "memory");
+    // all of a thread's loads are issued before its first store (the stores' "memory" clobber
+    // would otherwise serialise one L2 round trip per element)
+    constexpr int kBatch = 8;
+    for (int i0 = threadIdx.x; i0 < total; i0 += kBatch * blockDim.x) {
+        float2 v[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int i = i0 + b * blockDim.x;
+            v[b] = make_float2(0.0f, 0.0f);
+            if (i < nt)
+                v[b] = __ldg(&l.tab[0][r.t_lo * l.pairs[0] + i]);
+            else if (i < r.off_w)
+                v[b] = __ldg(&l.tab[1][i - r.off_h]);
+            else if (i < total)
+                v[b] = __ldg(&l.tab[2][i - r.off_w]);
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int i = i0 + b * blockDim.x;
+            if (i < total)
+                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(st + 8u * i), "f"(v[b].x),
+                             "f"(v[b].y)
+                             : "memory");
+        }
     }
 }
 
@@ -352,11 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+    // a constant (uploaded) RoPE table is staged while the previous kernel drains
+    if constexpr (kRopeSmem)
+        if (p.epi_mode == 2 && p.rope.tab_constant) rope_stage_tables(p.rope, s_rope);
     // the previous kernel's outputs (A operand, destinations, a per-call RoPE table) are
     // complete past this point; everything above overlapped its tail
     pdl_wait();
     if constexpr (kRopeSmem)
-        if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
+        if (p.epi_mode == 2 && !p.rope.tab_constant) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -566,12 +583,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
-    pdl_wait();
-    if (p.epi_mode == 2) rope_stage_tables(p.rope, s_rope);
+    // everything up to griddepcontrol.wait overlaps the previous kernel's tail: the barriers
+    // and the TMEM slot are published cluster-wide, a constant RoPE table is staged, and the
+    // producer streams the weight (B) halves of the first stages onto the leader's barriers
+    if (p.epi_mode == 2 && p.rope.tab_constant) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0 && lane == 0 && pair < num_tiles) {
+        const int n0 = tile_n(p, pair) * BN + cta * (BN / 2);
+        for (int kt = 0; kt < p.b_early; ++kt) {
+            // the leader arms the stage for both CTAs' A and B bytes; the peer's early B bytes
+            // may land first (the transaction count goes transiently negative, and the phase
+            // cannot complete before the leader's arrival)
+            if (leader) mbar_arrive_expect_tx(&full[kt], 2 * (kABytes + kBBytes));
+            tma_load_2d_pair(sB + kt * kBBytes, &map_b, &full[kt], kt * kBK, n0);
+        }
+    }
+    pdl_wait();
+    if (p.epi_mode == 2 && !p.rope.tab_constant) {
+        rope_stage_tables(p.rope, s_rope);
+        __syncthreads();  // the table is CTA-local: the epilogue warps read their own copy
+    }
     if (threadIdx.x == 0 && p.experiment == 5) p.trace[(blockIdx.x * 16 + 15) * 4 + 1] = clock64();
 
     if (warp == 0) {
@@ -583,11 +617,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int n0 = tile_n(p, tile) * BN + cta * (BN / 2);
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kABytes + kBBytes));
+                    const bool early = tile == pair && kt < p.b_early;
+                    if (leader && !early) mbar_arrive_expect_tx(&full[stage], 2 * (kABytes + kBBytes));
                     const int k0 = kt * kBK;
                     tma_load_3d_pair(sA + stage * kABytes, &map_a, &full[stage], k0 % p.k_inner, m0,
                                      k0 / p.k_inner);
-                    tma_load_2d_pair(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
+                    if (!early) tma_load_2d_pair(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
                     if (++stage == kPairStages) {
                         stage = 0;
                         phase ^= 1;
@@ -860,15 +895,16 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     if ((experiment == 5 && rope) || experiment == 7) p.trace = gemm_trace_buffer();
     p.experiment = p.trace ? 5 : (experiment == 5 || experiment == 7 ? 0 : experiment);
     p.span = span_slot();
-    // the pair kernel's B halves complete on the leader's barrier (initialised cluster-wide
-    // only after its prologue sync): early B loads are a single-CTA-kernel feature
-    static const bool early_env = [] {  // SPX_GEMM_EARLY_B=0 turns it off (A/B)
+    // early B loads: the weight tiles of the first stages stream in before griddepcontrol.wait
+    // (the pair kernel publishes its barriers cluster-wide first, then loads its B halves)
+    static const int early_env = [] {  // SPX_GEMM_EARLY_B: 0 off, 1 single-CTA only, 2 all (A/B)
         const char* e = std::getenv("SPX_GEMM_EARLY_B");
-        return !(e && std::atoi(e) == 0);
+        return e ? std::atoi(e) : 2;
     }();
-    p.b_early = (early_env && o.b_constant && !plan.pair)
-                    ? std::min(p.K / kBK, plan.bn == 192 && p.epi_mode != 2 ? 5 : kStages)
-                    : 0;
+    const bool early_ok = o.b_constant && (plan.pair ? early_env >= 2 : early_env >= 1);
+    p.b_early = !early_ok ? 0
+                : plan.pair ? std::min(p.K / kBK, kPairStages)
+                            : std::min(p.K / kBK, plan.bn == 192 && p.epi_mode != 2 ? 5 : kStages);
     if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         launch_pdl(gemm_bf16_tn_pair_kernel<256>, dim3(plan.grid), dim3(kThreads),

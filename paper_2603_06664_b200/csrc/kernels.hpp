@@ -174,6 +174,8 @@ struct RopeLaunch {
     // table (device, fp32 cos/sin interleaved per band)
     const float2* tab[3] = {};
     int pairs[3] = {0, 0, 0};
+    int tab_constant = 0;            // 1: no kernel writes tab (the precomputed table): the
+                                     // GEMM epilogue stages it before griddepcontrol.wait
     // optional QK-RMSNorm over the C = H*D channels
     const bf16* norm_w_q = nullptr;
     const bf16* norm_w_k = nullptr;

@@ -72,6 +72,10 @@ const DeviceRopeTable& RopeTable::on_device(int device) const {
         SPX_CUDA(cudaMemcpy(t.band[band], host.data(), host.size() * sizeof(float2),
                             cudaMemcpyHostToDevice));
     }
+    // a pageable H2D copy may return before its DMA lands and the engine streams are
+    // non-blocking: the table is complete before any kernel (which may read it before its
+    // griddepcontrol.wait, RopeLaunch::tab_constant) can be enqueued
+    SPX_CUDA(cudaDeviceSynchronize());
     SPX_CUDA(cudaSetDevice(prev));
     return device_.emplace(device, t).first->second;
 }
