@@ -274,6 +274,28 @@ def ref_generate(frames=3, grid_h=4, grid_w=4, num_blocks=5, layers=4, steps=2, 
     return out, dict(zip(keys, list(ledger)))
 
 
+REF_REPORT_SO = os.path.join(HERE, "_ref", "libspattn_ref_report.so")
+
+
+def ref_report_json(frames=3, grid_h=4, grid_w=4, num_blocks=5, layers=4, steps=2, heads=8,
+                    head_dim=16, world=1, window=None, variant="reference", ablation=7,
+                    force_start_frame_zero=False, seed=0) -> str:
+    """The reference's own report of a generate run: to_json(GenerationResult)
+    (report.cpp:161-175) with strip_timing_fields (report.cpp:246-262), indent 2, produced by
+    the unmodified report.cpp compiled into _ref/libspattn_ref_report.so."""
+    lib = ctypes.CDLL(REF_REPORT_SO)
+    lib.ref_report_json.restype = c_int
+    cfg = _i64([frames, grid_h, grid_w, num_blocks, layers, steps, heads, head_dim, world,
+                -1 if window is None else window, VARIANTS[variant], ablation,
+                int(force_start_frame_zero)])
+    buf = ctypes.create_string_buffer(1 << 20)
+    n = c_int64()
+    rc = lib.ref_report_json(cfg, ctypes.c_uint64(seed), buf, len(buf), ctypes.byref(n))
+    if rc != 0:
+        raise RuntimeError(f"reference report failed (code {rc})")
+    return buf.value.decode()
+
+
 def ref_sample_call(frames, grid_h, grid_w, heads, head_dim, kv_frames, tokens, rows, threads):
     """Reference operators timed on a bounded sample of one layer call (seconds, extrapolated)."""
     out = np.zeros(7, dtype=np.float64)

@@ -747,19 +747,31 @@ def tensor_checksum(x: np.ndarray) -> str:
 
 def generation_result_json(cfg: "GenerationConfig", block_outputs: np.ndarray, stats: dict,
                            stage_us_total: Optional[dict] = None, calls: Optional[int] = None,
-                           wall_ms: Optional[float] = None) -> dict:
+                           wall_ms: Optional[float] = None, variant: Optional[str] = None) -> dict:
     """to_json(GenerationResult) (report.cpp:87-175): the reference's report layout for a
     device run, so its report tooling reads GPU runs. block_outputs: (blocks, L, H, D) values
-    (bf16 bits or floats); stats: Engine.stats(); element width 2 (bf16)."""
+    (bf16 bits or floats); stats: Engine.stats(); element width 2 (bf16).
+
+    variant: the reference PipelineKind name (sp_attention.hpp:46-66). Default: "baseline"
+    when every ablation flag is off (the Alg. 1 schedule), else "optimized"; "reference" labels
+    a P = 1 run as reference_self_attention (no exchange stage, flags all on). Pinned against
+    reports the reference's own report.cpp wrote (tests/golden/reference_reports.json)."""
     out = np.asarray(block_outputs)
     if out.dtype == np.uint16:
         out = bf16_bits_to_float(out)
     bits = cfg.ablation.bits()
-    variant = "baseline" if bits == 0 else "optimized"
+    if variant is None:
+        variant = "baseline" if bits == 0 else "optimized"
+    if variant not in ("reference", "baseline", "optimized"):
+        raise ConfigError(f"unknown variant {variant!r}")
+    if variant == "reference" and (cfg.world_size != 1 or bits != 7):
+        raise ConfigError("the reference variant is the P = 1 path with every flag on")
     ab = {"use_fused_all_to_all": bool(bits & 1), "use_local_rope": bool(bits & 2),
           "use_precomputed_freqs": bool(bits & 4)}
     order = (["qkv", "rope", "gather_or_fused", "cache", "attention", "output_exchange"] if bits & 2
              else ["qkv", "gather_or_fused", "rope", "cache", "attention", "output_exchange"])
+    if variant == "reference":  # sp_attention.cpp:317-348: no exchange stage
+        order = ["qkv", "rope", "cache", "attention", "output_exchange"]
     g = cfg.grid_per_block
     conf = {"frames_per_block": g.frames, "grid_h": g.height, "grid_w": g.width,
             "num_blocks": cfg.num_blocks, "layers": cfg.layers, "denoise_steps": cfg.denoise_steps,
@@ -774,11 +786,36 @@ def generation_result_json(cfg: "GenerationConfig", block_outputs: np.ndarray, s
                        "shape": [1, int(out.shape[1]), cfg.heads, cfg.head_dim],
                        "checksum": tensor_checksum(out[b])})
     ledger = dict(stats)
+    if variant == "reference":
+        # reference_self_attention calls no collective (sp_attention.cpp:317-348); the P = 1
+        # device run moves no data either (its exchange rounds are local no-ops)
+        if ledger.get("elements_sent", 0) != 0:
+            raise ConfigError("a reference-variant report needs a run that moved no data")
+        ledger = {k: 0 for k in ("all_gather", "all_to_all", "fused_all_to_all", "elements_sent",
+                                 "rounds")}
     ledger["bytes_sent_at_width"] = ledger["elements_sent"] * 2
     profile = {"calls": calls if calls is not None else cfg.total_calls(),
                "wall_ms": wall_ms, "stage_order": order,
                "stage_us_total": stage_us_total or {k: 0.0 for k in order}, "ledger": ledger}
     return {"config": conf, "blocks": blocks, "profile": profile}
+
+
+_TIMING_KEYS = ("wall_ms", "wall_ms_all", "mean_stage_us", "stage_us_total", "stage_times_us",
+                "total_us", "time_us", "deltas", "speedup_vs_baseline")
+
+
+def strip_timing_fields(j):
+    """strip_timing_fields (report.cpp:246-262): drops every timing key, recursively, in
+    place, so two reports compare on their deterministic content. Returns j."""
+    if isinstance(j, dict):
+        for k in _TIMING_KEYS:
+            j.pop(k, None)
+        for v in j.values():
+            strip_timing_fields(v)
+    elif isinstance(j, list):
+        for v in j:
+            strip_timing_fields(v)
+    return j
 
 
 def bf16_bits_to_float(bits: np.ndarray) -> np.ndarray:

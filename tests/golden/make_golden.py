@@ -48,6 +48,30 @@ def main():
     with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_golden.json"), "w") as f:
         json.dump(g, f, indent=1, sort_keys=True)
     print("wrote", len(g), "entries")
+    reports()
+
+
+# the reference's own run reports (report.cpp to_json(GenerationResult), timing fields
+# stripped) for the report-layout parity tests (tests/test_report.py, test_gpu_engine.py)
+REPORTS = {
+    "tiny_steps2_opt_p2": dict(TINY, steps=2, world=2, variant="optimized"),
+    "tiny_steps2_p1_reference": dict(TINY, steps=2),
+    "desk_base_p4": dict(DESK, world=4, variant="baseline"),
+    "desk_opt_p8_window6": dict(DESK, world=8, variant="optimized", window=6),
+    "desk_fault_p2": dict(DESK, world=2, variant="optimized", force_start_frame_zero=True),
+    "desk_opt_p2_ablation_5": dict(DESK, world=2, variant="optimized", ablation=5),
+}
+
+
+def reports():
+    r = {"source": "reference proj/src/report.cpp to_json(GenerationResult) + strip_timing_fields, "
+                   "compiled from /root/reference by oracle/Makefile (_ref/libspattn_ref_report.so)",
+         "configs": {k: {kk: vv for kk, vv in v.items()} for k, v in REPORTS.items()}}
+    for name, kw in REPORTS.items():
+        r[name] = json.loads(oracle.ref_report_json(**kw))
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_reports.json"), "w") as f:
+        json.dump(r, f, indent=1, sort_keys=True)
+    print("wrote", len(REPORTS), "reports")
 
 
 if __name__ == "__main__":

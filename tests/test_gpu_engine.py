@@ -4,6 +4,7 @@ Tiers: bit-exact for indices / permutations / ring order, bf16 to
 activations, RMS-level for deep stacks (the reference model's activations collapse toward
 the block mean of V). The oracle always consumes the bf16-rounded inputs.
 """
+import json
 import math
 
 import numpy as np
@@ -698,3 +699,29 @@ def test_small_head_dim_attention_matches_fp32(cuda, D, parity_log):
     e = float((o.float()[0] - ref).norm() / ref.norm())
     parity_log(rel_l2=e, bar=5e-3)
     assert e < 5e-3
+
+
+@pytest.mark.parametrize("name", ["tiny_steps2_opt_p2", "tiny_steps2_p1_reference", "desk_base_p4",
+                                  "desk_opt_p8_window6", "desk_fault_p2", "desk_opt_p2_ablation_5"])
+def test_device_report_equals_reference_report(cuda, name):
+    """A device run's report (generation_result_json, stripped) against the report the
+    reference's own report.cpp wrote for the same configuration
+    (tests/golden/reference_reports.json): config, block shapes and start frames, call count,
+    stage order and the exchange ledger equal; the block checksums are of bf16 outputs, so they
+    are compared against the checksum of the device output itself instead."""
+    import test_report as tr
+
+    s = spattn()
+    gold = tr.reports()
+    cfg, variant = tr.cfg_from_report_kw(gold["configs"][name])
+    eng = s.Engine(cfg)
+    out = eng.generate()
+    rep = s.strip_timing_fields(s.generation_result_json(cfg, out, eng.stats(), variant=variant))
+    ref = json.loads(json.dumps(gold[name]))
+    vals = s.bf16_bits_to_float(out)
+    for i, b in enumerate(rep["blocks"]):
+        assert b["checksum"] == s.tensor_checksum(vals[i])
+        b.pop("checksum")
+    for b in ref["blocks"]:
+        b.pop("checksum")
+    assert rep == ref
