@@ -86,63 +86,10 @@ constexpr size_t gemm_smem_bytes() {
 }
 
 
-// ---- RoPE band tables staged in smem (epi_mode 2) ----
-struct RopeSmem {
-    int t_lo, n_t;  // frames [t_lo, t_lo + n_t) of the T band
-    int off_h, off_w;
-};
-
-__host__ __device__ inline RopeSmem rope_smem_layout(const RopeLaunch& l) {
-    RopeSmem r;
-    const int64_t first = l.row_offset, last = l.row_offset + l.rows_per_batch - 1;
-    r.t_lo = static_cast<int>(l.start_frame + first / l.hw);
-    r.n_t = static_cast<int>(last / l.hw - first / l.hw + 1);
-    r.off_h = r.n_t * l.pairs[0];
-    r.off_w = r.off_h + static_cast<int>(l.hw / l.grid_w) * l.pairs[1];
-    return r;
-}
-
-__host__ __device__ inline int rope_smem_pairs(const RopeLaunch& l) {
-    const RopeSmem r = rope_smem_layout(l);
-    return r.off_w + static_cast<int>(l.grid_w) * l.pairs[2];
-}
-
+// ---- RoPE band tables staged in smem (epi_mode 2; layout in rope_device.cuh) ----
 // every thread of the CTA: copy the slice (before the CTA-wide barrier that follows setup)
 __device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, uint32_t st) {
-    const RopeSmem r = rope_smem_layout(l);
-    const int nt = r.n_t * l.pairs[0];
-    const int total = rope_smem_pairs(l);
-    // all of a thread's loads are issued before its first store (the stores' "memory" clobber
-    // would otherwise serialise one L2 round trip per element)
-    constexpr int kBatch = 8;
-    for (int i0 = threadIdx.x; i0 < total; i0 += kBatch * blockDim.x) {
-        float2 v[kBatch];
-#pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            const int i = i0 + b * blockDim.x;
-            v[b] = make_float2(0.0f, 0.0f);
-            if (i < nt)
-                v[b] = __ldg(&l.tab[0][r.t_lo * l.pairs[0] + i]);
-            else if (i < r.off_w)
-                v[b] = __ldg(&l.tab[1][i - r.off_h]);
-            else if (i < total)
-                v[b] = __ldg(&l.tab[2][i - r.off_w]);
-        }
-#pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            const int i = i0 + b * blockDim.x;
-            if (i < total)
-                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(st + 8u * i), "f"(v[b].x),
-                             "f"(v[b].y)
-                             : "memory");
-        }
-    }
-}
-
-__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-    return v;
+    rope_stage_tables(l, st, static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x));
 }
 
 // a token row's three band rows in the staged tables (shared-memory byte addresses, computed

@@ -44,4 +44,65 @@ __device__ __forceinline__ void rope_thw(const RopeLaunch& l, int row, int& t, i
     w = rem - h * gw;
 }
 
+// ---- the band-table slice one launch reads, staged in shared memory ----
+// frames [t_lo, t_lo + n_t) of the T band (the launch's rows), then the whole H and W bands;
+// entries are (cos, sin) pairs, pair-index offsets off_h / off_w
+struct RopeSmem {
+    int t_lo, n_t;
+    int off_h, off_w;
+};
+
+__host__ __device__ inline RopeSmem rope_smem_layout(const RopeLaunch& l) {
+    RopeSmem r;
+    const int64_t first = l.row_offset, last = l.row_offset + l.rows_per_batch - 1;
+    r.t_lo = static_cast<int>(l.start_frame + first / l.hw);
+    r.n_t = static_cast<int>(last / l.hw - first / l.hw + 1);
+    r.off_h = r.n_t * l.pairs[0];
+    r.off_w = r.off_h + static_cast<int>(l.hw / l.grid_w) * l.pairs[1];
+    return r;
+}
+
+__host__ __device__ inline int rope_smem_pairs(const RopeLaunch& l) {
+    const RopeSmem r = rope_smem_layout(l);
+    return r.off_w + static_cast<int>(l.grid_w) * l.pairs[2];
+}
+
+// threads tid = 0 .. nthreads - 1 copy the slice to shared-memory byte address st. All of a
+// thread's loads are issued before its first store (the stores' "memory" clobber would
+// otherwise serialise one L2 round trip per element).
+__device__ __forceinline__ void rope_stage_tables(const RopeLaunch& l, uint32_t st, int tid, int nthreads) {
+    const RopeSmem r = rope_smem_layout(l);
+    const int nt = r.n_t * l.pairs[0];
+    const int total = rope_smem_pairs(l);
+    constexpr int kBatch = 8;
+    for (int i0 = tid; i0 < total; i0 += kBatch * nthreads) {
+        float2 v[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int i = i0 + b * nthreads;
+            v[b] = make_float2(0.0f, 0.0f);
+            if (i < nt)
+                v[b] = __ldg(&l.tab[0][r.t_lo * l.pairs[0] + i]);
+            else if (i < r.off_w)
+                v[b] = __ldg(&l.tab[1][i - r.off_h]);
+            else if (i < total)
+                v[b] = __ldg(&l.tab[2][i - r.off_w]);
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int i = i0 + b * nthreads;
+            if (i < total)
+                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(st + 8u * i), "f"(v[b].x),
+                             "f"(v[b].y)
+                             : "memory");
+        }
+    }
+}
+
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
 }  // namespace spx
