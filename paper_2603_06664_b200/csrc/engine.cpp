@@ -427,6 +427,7 @@ void Engine::build_plans() {
             q.K = static_cast<int>(C_);
             q.b_constant = true;  // weights: uploaded synchronously, never written by a kernel
             if (cfg_.wan_block) q.bias = w.wan.b_qkv + l * 3 * C_;
+            q.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.qkv_plan[l], q, sms);
 
             GemmOperands o{};
@@ -460,6 +461,7 @@ void Engine::build_plans() {
             o.N = static_cast<int>(C_);
             o.K = static_cast<int>(C_);
             o.b_constant = true;
+            o.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.o_plan[l], o, sms);
             // adaLN (not the full block): fuse the next layer's K1 into this projection
             rs.oln_plan.resize(static_cast<size_t>(cfg_.layers));
@@ -972,10 +974,12 @@ void Engine::layer_external(int64_t layer, int64_t block, int64_t start_frame, v
         SPX_CUDA(cudaSetDevice(rs.device));
         GemmOperands q = rs.qkv_plan[static_cast<size_t>(layer)].ops;
         if (!cfg_.adaln) q.a = static_cast<const bf16*>(x[li]);  // adaLN: A is K1's output
+        q.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
         gemm_plan(&qp[li], q, device_sm_count(rs.device));
         GemmOperands o = rs.o_plan[static_cast<size_t>(layer)].ops;
         o.out = static_cast<bf16*>(y[li]);
         if (cfg_.adaln) o.residual = static_cast<const bf16*>(x[li]);
+        o.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
         gemm_plan(&op[li], o, device_sm_count(rs.device));
         qv.push_back(&qp[li]);
         ov.push_back(&op[li]);

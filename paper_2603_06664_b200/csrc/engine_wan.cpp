@@ -161,6 +161,7 @@ void Engine::build_wan_plans() {
             // cross-attention q = LN_affine(x) Wq^T + bq
             GemmOperands cq = base(rs.xm, C_, w.cq + l * C_ * C_, rs.ca_q, C_);
             cq.bias = w.bcq + l * C_;
+            cq.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.cq_plan[static_cast<size_t>(l)], cq, sms);
             // x += ca_o Wo^T + bo (in place, no gate)
             GemmOperands co = base(rs.ca_o, C_, w.co + l * C_ * C_, xo, C_);
@@ -168,11 +169,13 @@ void Engine::build_wan_plans() {
             co.residual = xo;
             co.residual_row_stride = C_;
             co.bias = w.bco + l * C_;
+            co.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.co_plan[static_cast<size_t>(l)], co, sms);
             // h = GELU(LN(x)(1 + scale_mlp) + shift_mlp) W1^T + b1)
             GemmOperands f1 = base(rs.xm, C_, w.w1 + l * FF_ * C_, rs.ffn_h, FF_);
             f1.epi_mode = 3;
             f1.bias = w.b1 + l * FF_;
+            f1.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.f1_plan[static_cast<size_t>(l)], f1, sms);
             // x += gate_mlp * (h W2^T + b2) (in place)
             GemmOperands f2 = base(rs.ffn_h, FF_, w.w2 + l * C_ * FF_, xo, C_);
@@ -181,6 +184,7 @@ void Engine::build_wan_plans() {
             f2.residual_row_stride = C_;
             f2.gate = rs.mod_step + (l * 6 + 5) * C_;
             f2.bias = w.b2 + l * C_;
+            f2.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&rs.f2_plan[static_cast<size_t>(l)], f2, sms);
             // cross attention of this rank's rows (all heads) over the layer's context K/V;
             // no workspace: one CTA per (query tile, head), the same arithmetic at every P
@@ -281,6 +285,7 @@ void Engine::compute_context() {
             g.bias = bias;
             g.epi_mode = epi;
             GemmPlan plan;
+            g.allow_split_k = !cfg_.sp_bit_exact;  // split-K changes the k order
             gemm_plan(&plan, g, sms);
             gemm_run(plan, st);
         };

@@ -79,10 +79,11 @@ __device__ __forceinline__ void trace_mark(const GemmParams& p, int it, int kind
 // 18.6 -> 18.3 us standalone, -0.8 us per layer call in the engine)
 template <int BN, bool kRopeSmem>
 __host__ __device__ constexpr int gemm_stages() { return (!kRopeSmem && BN == 192) ? 5 : kStages; }
-template <int BN, bool kRopeSmem = true>
+template <int BN, bool kRopeSmem = true, int kSplit = 1>
 constexpr size_t gemm_smem_bytes() {
     return 1024 + static_cast<size_t>(gemm_stages<BN, kRopeSmem>()) * (kBM * kBK * 2 + BN * kBK * 2) +
-           256 + (kRopeSmem ? kRopeSmemPairs * 8 : 0) + kEpiWarps * kEpiStageBytes;
+           256 + (kRopeSmem ? kRopeSmemPairs * 8 : 0) + kEpiWarps * kEpiStageBytes +
+           (kSplit > 1 ? static_cast<size_t>(kBM) * BN * 4 : 0);
 }
 
 
@@ -256,10 +257,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row0, in
     __syncwarp();  // the slice's shared memory is read before the next slice overwrites it
 }
 
-template <int BN, bool kRopeSmem = true>
+// kSplit = 2 (split-K, launched as 2-CTA clusters, BN = 128): both CTAs of a cluster own the
+// same output tile; CTA r accumulates k-blocks [r K/2, (r+1) K/2) in its own TMEM. CTA 1's
+// epilogue warps store their fp32 partial into CTA 0's shared memory (DSMEM, a [chunk][4-column
+// group][row] float4 layout: conflict-free on both sides) and arrive on CTA 0's pfull; CTA 0 adds
+// it to its accumulator and runs the epilogue, then hands the buffer back (pempty in CTA 1). For
+// the short-M per-rank shapes (585-1170 rows at P = 4 / 8), whose tiles cannot fill the SMs: each
+// SM streams half the operand bytes of the tile (the L2 -> SM inflow is what bounds them).
+template <int BN, bool kRopeSmem = true, int kSplit = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+    static_assert(kSplit == 1 || (kSplit == 2 && BN == 128), "split-K: 2-CTA clusters, BN = 128");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -273,14 +282,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* pfull = tempty + 2;   // split-K (CTA 0): CTA 1's partial landed
+    uint64_t* pempty = pfull + 1;   // split-K (CTA 1): CTA 0 has consumed the partial buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 1);
     const uint32_t s_rope = smem_u32(reinterpret_cast<uint8_t*>(full) + 256);
     const uint32_t s_stage =
         s_rope + (kRopeSmem ? kRopeSmemPairs * 8 : 0) + (threadIdx.x / 32 - 4) * kEpiStageBytes;
+    const uint32_t s_part = s_rope + (kRopeSmem ? kRopeSmemPairs * 8 : 0) + kEpiWarps * kEpiStageBytes;
     const RopeSmem rope_l = p.epi_mode == 2 ? rope_smem_layout(p.rope) : RopeSmem{};
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const int split = kSplit > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int tile0 = static_cast<int>(blockIdx.x) / kSplit;   // this CTA's first tile
+    const int tile_step = static_cast<int>(gridDim.x) / kSplit;
     pdl_trigger();  // the next kernel may launch; it waits for this grid before its main loop
     span_begin(p.span);
     if (threadIdx.x == 0 && p.experiment == 5) {
@@ -288,7 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.trace[(blockIdx.x * 16 + 14) * 4 + 0] = static_cast<long long>(globaltimer_ns());
     }
     const int num_tiles = p.num_m_tiles * p.num_n_tiles;
-    const int num_kt = p.K / kBK;
+    const int num_kt_all = p.K / kBK;
+    const int kt_begin = split * num_kt_all / kSplit;  // this CTA's k-blocks
+    const int num_kt = (split + 1) * num_kt_all / kSplit - kt_begin;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_a);
@@ -301,14 +318,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], kEpiWarps);  // one arrival per epilogue warp
         }
+        mbar_init(pfull, kEpiWarps * 32);   // every epilogue thread of CTA 1
+        mbar_init(pempty, kEpiWarps * 32);  // every epilogue thread of CTA 0
         fence_mbar_init();
         // B (weights) of this CTA's first tile: not produced by the previous kernel, so it
         // streams in while that kernel drains; A follows after the PDL wait
-        if (static_cast<int>(blockIdx.x) < num_tiles) {
-            const int n0 = tile_n(p, static_cast<int>(blockIdx.x)) * BN;
+        if (tile0 < num_tiles) {
+            const int n0 = tile_n(p, tile0) * BN;
             for (int kt = 0; kt < p.b_early; ++kt) {
                 mbar_arrive_expect_tx(&full[kt], kABytes + kBBytes);
-                tma_load_2d(sB + kt * kBBytes, &map_b, &full[kt], kt * kBK, n0);
+                tma_load_2d(sB + kt * kBBytes, &map_b, &full[kt], (kt_begin + kt) * kBK, n0);
             }
         }
     }
@@ -322,7 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (kRopeSmem)
         if (p.epi_mode == 2 && !p.rope.tab_constant) rope_stage_tables(p.rope, s_rope);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kSplit > 1)
+        cluster_sync_all();  // the peer's pfull / pempty exist before any remote arrival
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0 && p.experiment == 5) p.trace[(blockIdx.x * 16 + 15) * 4 + 1] = clock64();
@@ -331,14 +353,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = tile0; tile < num_tiles; tile += tile_step) {
                 const int m0 = tile_m(p, tile) * kBM;
                 const int n0 = tile_n(p, tile) * BN;
                 for (int kt = 0; kt < num_kt; ++kt) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    const bool early = tile == static_cast<int>(blockIdx.x) && kt < p.b_early;
+                    const bool early = tile == tile0 && kt < p.b_early;
                     if (!early) mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
-                    const int k0 = kt * kBK;
+                    const int k0 = (kt_begin + kt) * kBK;
                     tma_load_3d(sA + stage * kABytes, &map_a, &full[stage], k0 % p.k_inner, m0,
                                 k0 / p.k_inner);
                     if (!early) tma_load_2d(sB + stage * kBBytes, &map_b, &full[stage], k0, n0);
@@ -357,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
                 const int acc = it & 1;
                 const uint32_t aphase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], aphase ^ 1);
@@ -392,13 +414,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         const int ew = warp % 4;         // TMEM lane quarter this warp may access
         const int half = (warp - 4) / 4;  // which half of the tile's columns
+        // split-K partial buffer: [chunk][4-column group][row] float4, this thread's row
+        const uint32_t part_row = s_part + static_cast<uint32_t>(ew * 32 + lane) * 16u;
+        // the accumulator chunk c of this thread's row (+ CTA 1's partial on CTA 0)
+        auto load_acc = [&](uint32_t t_row, int c, uint32_t (&r)[32]) {
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld_wait();
+            if constexpr (kSplit > 1) {
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    float4 v;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                 : "r"(part_row + static_cast<uint32_t>(c * 8 + j4) * (kBM * 16u)));
+                    r[4 * j4 + 0] = __float_as_uint(__uint_as_float(r[4 * j4 + 0]) + v.x);
+                    r[4 * j4 + 1] = __float_as_uint(__uint_as_float(r[4 * j4 + 1]) + v.y);
+                    r[4 * j4 + 2] = __float_as_uint(__uint_as_float(r[4 * j4 + 2]) + v.z);
+                    r[4 * j4 + 3] = __float_as_uint(__uint_as_float(r[4 * j4 + 3]) + v.w);
+                }
+            }
+        };
         int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             const int m0 = tile_m(p, tile) * kBM;
             const int n0 = tile_n(p, tile) * BN;
             const int row = m0 + ew * 32 + lane;
+            if constexpr (kSplit > 1) {
+                if (split == 1) {
+                    // ship the partial into CTA 0's buffer once CTA 0 has consumed the last one
+                    mbar_wait(&tfull[acc], aphase);
+                    tc_fence_after();
+                    mbar_wait_cluster(pempty, (it & 1) ^ 1);
+                    uint32_t peer_row;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(peer_row) : "r"(part_row));
+                    const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+#pragma unroll
+                    for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+                        uint32_t r[32];
+                        tmem_ld32(t_row + c * 32, r);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4)
+                            asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             peer_row + static_cast<uint32_t>(c * 8 + j4) * (kBM * 16u)),
+                                         "r"(r[4 * j4]), "r"(r[4 * j4 + 1]), "r"(r[4 * j4 + 2]), "r"(r[4 * j4 + 3])
+                                         : "memory");
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    uint32_t peer_full;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(peer_full) : "r"(smem_u32(pfull)));
+                    mbar_arrive_remote(peer_full);  // release.cluster: the stores above are visible
+                    continue;
+                }
+            }
             if (p.epi_mode == 1) {
                 // residual epilogue: this lane's residual row segments are loaded before the
                 // accumulator is waited for (one L2 round trip per tile, overlapping the MMA,
@@ -416,19 +488,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mbar_wait(&tfull[acc], aphase);
                 tc_fence_after();
+                if constexpr (kSplit > 1) mbar_wait_cluster(pfull, it & 1);
                 if (warp == 4 && lane == 0) trace_mark(p, it, 2);
                 const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
 #pragma unroll
                 for (int ci = 0; ci < kS; ++ci) {
                     const int c = half * kS + ci;
                     uint32_t r[32];
-                    tmem_ld32(t_row + c * 32, r);
-                    tmem_ld_wait();
+                    load_acc(t_row, c, r);
                     epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, RopeRow{}, res_pre[ci]);
                 }
             } else {
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
+            if constexpr (kSplit > 1) mbar_wait_cluster(pfull, it & 1);
             if (warp == 4 && lane == 0) trace_mark(p, it, 2);
             const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             RopeRow rr{};
@@ -437,18 +510,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
                 uint32_t r[32];
-                tmem_ld32(t_row + c * 32, r);
-                tmem_ld_wait();
+                load_acc(t_row, c, r);
                 epilogue_chunk(p, m0 + ew * 32, lane, n0 + c * 32, r, s_stage, rr);
             }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if constexpr (kSplit > 1) {  // the partial buffer is free for CTA 1's next tile
+                uint32_t peer_empty;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(peer_empty) : "r"(smem_u32(pempty)));
+                mbar_arrive_remote(peer_empty);
+            }
             if (warp == 4 && lane == 0) trace_mark(p, it, 3);
         }
     }
-    __syncthreads();
+    if constexpr (kSplit > 1)
+        cluster_sync_all();  // no CTA exits while its peer may still arrive on its barriers
+    else
+        __syncthreads();
     span_end(p.span);
     if (threadIdx.x == 0 && p.experiment == 5) {
         p.trace[(blockIdx.x * 16 + 15) * 4 + 2] = clock64();
@@ -682,15 +762,15 @@ void set_pair_smem_attr() {
     }
 }
 
-template <int BN, bool kRopeSmem = true>
+template <int BN, bool kRopeSmem = true, int kSplit = 1>
 void set_smem_attr() {
     static bool done[64] = {};  // the attribute is per function per device
     int dev = 0;
     SPX_CUDA(cudaGetDevice(&dev));
     if (!done[dev & 63]) {
-        SPX_CUDA(cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, kRopeSmem>,
+        SPX_CUDA(cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, kRopeSmem, kSplit>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(gemm_smem_bytes<BN, kRopeSmem>())));
+                                      static_cast<int>(gemm_smem_bytes<BN, kRopeSmem, kSplit>())));
         done[dev & 63] = true;
     }
 }
@@ -719,7 +799,7 @@ long long* gemm_trace_buffer() {
 
 int gemm_forced_variant() { return g_forced_variant.load(std::memory_order_relaxed); }
 void gemm_force_variant(int v) { g_forced_variant.store(v, std::memory_order_relaxed); }
-int gemm_num_variants() { return 5; }
+int gemm_num_variants() { return 6; }
 
 void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
     require(ops.M > 0 && ops.N > 0 && ops.K > 0, SPX_ERR_SHAPE, "gemm: empty problem");
@@ -733,25 +813,34 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
     // Variant: modelled time = waves x per-SM tile work / efficiency, over
     //   pair (cta_group::2) 256 x {256, 128} tiles and single-CTA 128 x {256, 192, 128} tiles.
     // The single-CTA kernels stream 1.5-2x the operand bytes per MMA cycle (L2 -> SM bound).
-    struct Cand { bool pair; int bn; double eff; };
+    struct Cand { bool pair; int bn; double eff; int split; };
     // efficiencies measured on B200 (tools/kbench.py gemm, K = 1536): pair-256 1358 TFLOP/s
     // at 4680x4608, pair-128 908, single-256 1237, single-128 1077; single-192 estimated
-    // between them (its 2-wave fit of the 4680x1536 O-projection is what it is for)
-    static const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.65}, {false, 256, 0.88},
-                                 {false, 128, 0.72}, {false, 192, 0.85}};
+    // between them (its 2-wave fit of the 4680x1536 O-projection is what it is for).
+    // Split-K (2-CTA clusters, 128 x 128): half the k-blocks per SM plus the 64 KB partial
+    // hand-off through DSMEM. Measured (r02ce): 585 x 8960 x 1536 (the Wan FFN down-projection
+    // per rank at P = 8) 23.8 us against 29.6 for the best unsplit tile, but slower at K = 1536
+    // (585 x 1536 x 1536: 10.8 vs 9.2 us), where the hand-off and the pipeline fill of the short
+    // halves dominate: used from 64 k-blocks (K >= 4096), where the caller allows the changed
+    // rounding
+    static const Cand cands[] = {{true, 256, 1.0, 1}, {true, 128, 0.65, 1}, {false, 256, 0.88, 1},
+                                 {false, 128, 0.72, 1}, {false, 192, 0.85, 1}, {false, 128, 0.9, 2}};
     const int forced = gemm_forced_variant();
     double best = 1e30;
-    for (int ci = 0; ci < 5; ++ci) {
+    for (int ci = 0; ci < 6; ++ci) {
         const Cand& c = cands[ci];
         if (ops.N % 32 != 0) continue;
+        if (c.split > 1 && (ops.K / kBK < 2 || (forced != ci && (!ops.allow_split_k || ops.K / kBK < 64))))
+            continue;
         const int64_t bm = c.pair ? 256 : 128;
         const int64_t tiles = ceil_div(static_cast<int64_t>(ops.M), bm) * ceil_div(ops.N, c.bn);
-        const int64_t slots = c.pair ? sm_count / 2 : sm_count;
+        const int64_t slots = c.pair || c.split > 1 ? sm_count / 2 : sm_count;
         const double t = static_cast<double>(ceil_div(tiles, slots)) * 128.0 * c.bn / c.eff;
         if ((forced < 0 && t < best) || forced == ci) {
             best = forced == ci ? -1.0 : t;
             plan->pair = c.pair;
             plan->bn = c.bn;
+            plan->ksplit = c.split;
         }
     }
     const int bm = plan->pair ? 256 : 128;
@@ -773,7 +862,7 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count) {
                 SPX_ERR_ALIGNMENT, err);
     }
     const int64_t tiles = ceil_div(static_cast<int64_t>(ops.M), bm) * ceil_div(ops.N, plan->bn);
-    if (plan->pair) {
+    if (plan->pair || plan->ksplit > 1) {
         const int64_t pairs = sm_count / 2;
         plan->grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
     } else {
@@ -852,7 +941,12 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     p.b_early = !early_ok ? 0
                 : plan.pair ? std::min(p.K / kBK, kPairStages)
                             : std::min(p.K / kBK, plan.bn == 192 && p.epi_mode != 2 ? 5 : kStages);
-    if (plan.pair && plan.bn == 256) {
+    if (plan.ksplit > 1) {
+        p.b_early = 0;
+        set_smem_attr<128, true, 2>();
+        launch_pdl_cluster(gemm_bf16_tn_kernel<128, true, 2>, dim3(plan.grid), dim3(kThreads),
+                           gemm_smem_bytes<128, true, 2>(), stream, 2, plan.map_a, plan.map_b, p);
+    } else if (plan.pair && plan.bn == 256) {
         set_pair_smem_attr<256>();
         launch_pdl(gemm_bf16_tn_pair_kernel<256>, dim3(plan.grid), dim3(kThreads),
                    gemm_pair_smem_bytes<256>(), stream, plan.map_a, plan.map_b, p);

@@ -41,6 +41,9 @@ struct GemmOperands {
     // B is not written by the kernel launched just before (e.g. weights): its first pipeline
     // stages are loaded before griddepcontrol.wait, overlapping the previous kernel's tail
     bool b_constant = false;
+    // the planner may split K across a 2-CTA cluster (short-M shapes): the sum of two partial
+    // accumulators, so the rounding differs from an unsplit tile (sp_bit_exact turns it off)
+    bool allow_split_k = true;
 };
 
 struct GemmPlan {
@@ -49,6 +52,7 @@ struct GemmPlan {
     GemmOperands ops;
     int bn = 256;
     bool pair = false;  // cta_group::2 CTA-pair kernel (256-row tiles)
+    int ksplit = 1;     // 2: split-K over a 2-CTA cluster (single-CTA 128 x 128 tiles)
     int grid = 0;
 };
 

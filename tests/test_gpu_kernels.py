@@ -58,11 +58,12 @@ def test_project_tokens_matches_fp32(cuda, M, K, N, parity_log):
     assert float((y.float() - ref).abs().max()) <= 2 ** -7 * float(ref.abs().max())
 
 
-@pytest.mark.parametrize("variant", range(5))
-@pytest.mark.parametrize("M,K,N", [(300, 128, 1600), (4680, 1536, 1536), (585, 1536, 4608)])
+@pytest.mark.parametrize("variant", range(6))
+@pytest.mark.parametrize("M,K,N", [(300, 128, 1600), (4680, 1536, 1536), (585, 1536, 4608),
+                                   (585, 8960, 1536)])
 def test_project_tokens_every_tile_variant(cuda, variant, M, K, N):
-    """each tile variant (pair 256x{256,128}, single 128x{256,128,192}) on ragged M and an N
-    that no tile width divides, forced through the planner override"""
+    """each tile variant (pair 256x{256,128}, single 128x{256,128,192}, split-K 2 x 128x128) on
+    ragged M and an N that no tile width divides, forced through the planner override"""
     torch = _t()
     g = torch.Generator(device="cuda").manual_seed(M + N + variant)
     x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
@@ -201,3 +202,33 @@ def test_attention_offset_guard_on_growing_logits(cuda, skv, attn_kernel):
     got = o.float()[0].transpose(0, 1)
     assert bool(torch.isfinite(got).all())
     assert rel_l2(got, ref) < 5e-3
+
+
+@pytest.mark.parametrize("epilogue", [0, 1, 3])
+@pytest.mark.parametrize("M,K,N", [(585, 1536, 1536), (1170, 8960, 1536), (200, 1024, 4000)])
+def test_split_k_epilogues(cuda, epilogue, M, K, N, parity_log):
+    """split-K (variant 5: a 2-CTA cluster per 128 x 128 tile, CTA 1's fp32 partial added in
+    CTA 0 through DSMEM) with the bias, in-place gated residual and GELU epilogues, persistent
+    over more tiles than clusters (1170 x 1536: 120 tiles on 74 clusters) and ragged M / N"""
+    torch = _t()
+    g = torch.Generator(device="cuda").manual_seed(M + K + N + epilogue)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    gate = torch.rand(N, device=cuda, generator=g) + 0.5
+    r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    y = r.clone() if epilogue == 1 else torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+    _check(_lib().spx_debug_set_gemm_variant(5))
+    try:
+        _check(_lib().spx_project_tokens_ex(x.data_ptr(), w.data_ptr(), y.data_ptr(), M, K, N, b.data_ptr(),
+                                            epilogue, y.data_ptr() if epilogue == 1 else None,
+                                            gate.data_ptr() if epilogue == 1 else None, _stream()))
+        torch.cuda.synchronize()
+    finally:
+        _check(_lib().spx_debug_set_gemm_variant(-1))
+    acc = x.float() @ w.float().t() + b
+    ref = {0: acc, 1: r.float() + gate * acc, 3: torch.nn.functional.gelu(acc, approximate="tanh")}[epilogue]
+    e = rel_l2(y.float(), ref)
+    parity_log(rel_l2=e, bar=3e-3)
+    assert bool(torch.isfinite(y.float()).all())
+    assert e < 3e-3
