@@ -15,7 +15,7 @@ from paper_2603_06664_b200._lib import check, lib  # noqa: E402
 st = torch.cuda.current_stream().cuda_stream
 torch.manual_seed(0)
 # GEMM: every tile variant, bias / GELU / residual epilogues
-for v in range(5):
+for v in range(6):  # 5 = split-K (2-CTA clusters)
     check(lib().spx_debug_set_gemm_variant(v))
     M, K, N = 300, 128, 512
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
