@@ -99,7 +99,8 @@ def test_wan_block_wan21_shape_vs_fp64(cuda, parity_log):
 @pytest.mark.parametrize("world", [2, 8])
 def test_wan_block_wan21_shape_sp_bit_identical(cuda, world, parity_log):
     """sp_bit_exact layouts: the full block at P = 2 and P = 8 equals P = 1 bit for bit; the
-    default (split-KV) layouts agree to bf16 rounding"""
+    default layouts (split-KV attention; at P = 8 also the split-K FFN down-projection, 585 x
+    8960 x 1536 per rank) agree to bf16 rounding"""
     base = run(WAN, 2, 2, 2, 1, 512, 4096, 256, 8960, seed=34, sp_bit_exact=True)[0]
     got = run(WAN, 2, 2, 2, world, 512, 4096, 256, 8960, seed=34, sp_bit_exact=True)[0]
     fast = run(WAN, 2, 2, 2, world, 512, 4096, 256, 8960, seed=34)[0]
