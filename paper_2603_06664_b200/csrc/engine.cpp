@@ -556,6 +556,15 @@ void Engine::seed_weights() {
     if (cfg_.wan_block) seed_wan_weights();
 }
 
+// SPX_WAN_VPACK=0: K3 packs v too (A/B of the v-pack epilogue)
+static bool vpack_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPX_WAN_VPACK");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void Engine::set_modulation(int64_t layer, const float* shift, const float* scale,
                             const float* gate) {
     require(layer >= 0 && layer < cfg_.layers, SPX_ERR_RANGE, "layer out of range");
@@ -779,6 +788,13 @@ void Engine::run_layer(int64_t layer, int64_t start_frame,
             // K2+K3 in one kernel: RoPE + pack in the QKV GEMM epilogue (no qkv round trip)
             gemm_run(qp, rs.stream, &rl);
             mark(li, 1);
+        } else if (rl.norm && fused && vpack_enabled() && gemm_vpack_fusable(qp, rl)) {
+            // QK-norm: K3 needs whole q / k rows, but v only moves -- the QKV epilogue packs v
+            // into the KV ring and K3 streams q | k (2/3 of the qkv round trip)
+            rl.skip_v = 1;
+            gemm_run(qp, rs.stream, &rl);
+            mark(li, 1);
+            rope_run(rl, rs.stream);
         } else {
             gemm_run(qp, rs.stream);
             mark(li, 1);

@@ -146,10 +146,11 @@ struct ChunkDst {
 };
 
 __device__ __forceinline__ ChunkDst chunk_dst(const GemmParams& p, int col0) {
-    if (p.epi_mode != 2) return {-1, 0, 1, 0, col0, p.ldo};
+    if (p.epi_mode != 2 && p.epi_mode != 4) return {-1, 0, 1, 0, col0, p.ldo};
     const RopeLaunch& l = p.rope;
     const int C = l.heads << p.head_shift;
     const int which = (col0 >= C) + (col0 >= 2 * C);
+    if (p.epi_mode == 4 && which < 2) return {-1, 0, 1, 0, col0, p.ldo};  // q | k: plain output
     const int c = col0 - which * C;
     const int head = c >> p.head_shift;
     const int d0 = c & ((1 << p.head_shift) - 1);
@@ -878,6 +879,13 @@ bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope) {
            rope.rows < (int64_t(1) << 31) && rope.row_offset + rope.rows_per_batch < (int64_t(1) << 31);
 }
 
+bool gemm_vpack_fusable(const GemmPlan& plan, const RopeLaunch& rope) {
+    const int C = rope.heads * rope.head_dim;
+    return rope.has_kv == 1 && rope.head_dim % 32 == 0 && C % plan.bn == 0 && C % 32 == 0 &&
+           plan.ops.N == 3 * C && plan.ops.M == rope.rows && plan.ops.groups == 1 &&
+           plan.ops.epi_mode == 0 && plan.ops.out_row_stride == 3 * C;
+}
+
 void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope) {
     const GemmOperands& o = plan.ops;
     GemmParams p{};
@@ -907,11 +915,18 @@ void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope)
     require(o.epi_mode != 1 || o.residual, SPX_ERR_CONFIG, "gemm: residual epilogue without residual");
     require(!o.bias || (reinterpret_cast<uintptr_t>(o.bias) & 15) == 0, SPX_ERR_ALIGNMENT,
             "gemm: bias must be 16-byte aligned");
-    if (rope) {
+    if (rope && rope->skip_v) {
+        require(gemm_vpack_fusable(plan, *rope), SPX_ERR_UNSUPPORTED,
+                "gemm: v-pack epilogue needs 3C outputs of stride 3C, C % BN == 0, D % 32 == 0");
+        p.epi_mode = 4;
+        p.rope = *rope;
+    } else if (rope) {
         require(gemm_rope_fusable(plan, *rope), SPX_ERR_UNSUPPORTED,
                 "gemm: rope epilogue needs 3C outputs, C % BN == 0, D % 32 == 0, no QK-norm");
         p.epi_mode = 2;
         p.rope = *rope;
+    }
+    if (rope) {
         require(rope->heads <= 16 && (rope->head_dim & (rope->head_dim - 1)) == 0, SPX_ERR_UNSUPPORTED,
                 "gemm: rope epilogue needs <= 16 heads and a power-of-two head_dim");
         p.head_shift = 0;

@@ -63,6 +63,9 @@ void gemm_plan(GemmPlan* plan, const GemmOperands& ops, int sm_count);
 // rotate-and-pack without its qkv round trip); requires gemm_rope_fusable()
 void gemm_run(const GemmPlan& plan, cudaStream_t stream, const RopeLaunch* rope = nullptr);
 bool gemm_rope_fusable(const GemmPlan& plan, const RopeLaunch& rope);
+// rope->skip_v: the epilogue packs only the v columns (into rope->dst.v, the KV ring) and stores
+// q | k unrotated to the plain output (bias allowed); K3 then normalises and rotates q | k
+bool gemm_vpack_fusable(const GemmPlan& plan, const RopeLaunch& rope);
 
 // The residual projection fused with the next LayerNorm + modulation (gemm_ln.cu, Wan mode):
 //   out = residual + gate (A B^T + bias);  out2 = LN(out) (one + mul) + add   (one = 1 adaLN,
@@ -186,6 +189,8 @@ struct RopeLaunch {
     float norm_eps = 1e-6f;
     int norm = 0;
     int rotate = 1;                  // 0: pack only (the exchange-first ablation rotates later)
+    int skip_v = 0;                  // K3: v was already packed by the QKV GEMM's epilogue
+                                     // (gemm_run with this launch): the rows are read as q | k
     RopeDest dst;
     int64_t dst_row_stride = 0;      // elements between rows in a destination slab (H/G * D)
 };

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const int v = lane_ + 32 * i;
-                if (v >= nvec) continue;
+                if (v >= nvec || l.skip_v) continue;  // skip_v: the QKV epilogue packed v
                 const uint4 yv = lds128(src + 2 * nvec + v);
                 bf16** dg = s_dst + v_g[i] * 17;
 #pragma unroll 1
@@ -369,7 +369,8 @@ void rope_run(const RopeLaunch& l, cudaStream_t stream) {
         SPX_CUDA(cudaGetDevice(&dev));
         sms = device_sm_count(dev);
     }
-    const uint32_t row_bytes = static_cast<uint32_t>(C) * 2u * (l.has_kv ? 3u : 1u);
+    // skip_v: only the q | k part of each 3C input row is streamed
+    const uint32_t row_bytes = static_cast<uint32_t>(C) * 2u * (l.has_kv ? (l.skip_v ? 2u : 3u) : 1u);
     const RowPipeShape sh = row_pipe_shape(l.rows, row_bytes, sms);
     const int64_t nblk = ceil_div(l.rows, static_cast<int64_t>(sh.rb));
     const unsigned ctas = static_cast<unsigned>(std::min<int64_t>(nblk, sms));
